@@ -1,0 +1,413 @@
+"""Benchmark of the ATP linear block (attention projections + MLP, fwd+bwd) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl atp|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, one rank per GPU)
+
+One step = one GPT layer's linear block forward + backward on DeviceMesh(d1, d2)
+(F3..F12, B1..B6 of SURVEY.md §8(a)) through libatp's C ABI.  Prints ONE JSON
+line on rank 0.  Timing: W untimed warm-up steps, then K steps bracketed by
+barrier + cudaDeviceSynchronize, CUDA events on the launching stream, max over
+ranks.  The working set (weights 0.4 GB + activations > 1 GB at h=4096) is far
+larger than the 126 MB L2, so no explicit flush is done (stated in `config`).
+
+Extra passes after the timed region (reported, never mixed into `value`):
+  * comm-disabled twin  -> exposed_comm_ms = t - t(no all-reduce)       (N > 1)
+  * profiled pass       -> per-kernel-class CUDA-event durations -> roofline
+  * e2e pass            -> same step through the public API with the step's
+                           inputs (X, dZ) copied H2D from pinned memory and its
+                           result (the bias gradients) read D2H each step
+  * cpu_baseline        -> the CPU oracle on a bounded token sample (rank 0, N = 1)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "1")  # P:345, set before CUDA init
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TFLOP/s/GPU and exposed-comm ms per GPT layer fwd+bwd at 1/2/4/8 B200 per mesh"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="atp", choices=["atp", "reference"])
+    p.add_argument("--hidden", type=int, default=4096)
+    p.add_argument("--heads", type=int, default=32)
+    p.add_argument("--ffn", type=int, default=0, help="default 4*hidden")
+    p.add_argument("--batch", type=int, default=4)
+    p.add_argument("--seq", type=int, default=2048)
+    p.add_argument("--mesh", default="", help="d1xd2; default: atp_search on a single-layer NVSwitch HCM")
+    p.add_argument("--chunks", type=int, default=0, help="default 1 at N=1, 4 otherwise")
+    p.add_argument("--gemm-ctas", type=int, default=-1, help="GEMM CTA cap (default: all SMs at N=1, SMs-16 else)")
+    p.add_argument("--seed", type=int, default=2301)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-oracle sample duration")
+    p.add_argument("--peaks", default=os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def layer_flops(T: int, h: int, F: int) -> float:
+    """Linear-block FLOPs of one layer fwd+bwd: fwd 2T(3h^2 + h^2 + 2hF), bwd 2x (= 72Th^2 at F=4h)."""
+    return 3.0 * 2.0 * T * (3 * h * h + h * h + 2 * h * F)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during a region."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.lines = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={device_index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.5)
+        except (OSError, ValueError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self, t0: float, t1: float) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons, n = [], [], set(), 0
+        for (tw, line) in self.lines:
+            if not (t0 - 0.15 <= tw <= t1 + 0.15):
+                continue
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            n += 1
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": n}
+
+
+def peaks(path: str) -> dict:
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return {"bf16_tflops": p["bf16_tflops"], "bf16_tflops_sustained": p.get("bf16_tflops_sustained"),
+                "hbm_gbs": p["hbm_gbs"], "source": "measured"}
+    except (OSError, KeyError, ValueError):
+        # /opt/skills/guides/B200_PROFILING.md fallback
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def cpu_oracle_run(T_s: int, h: int, F: int, heads: int, seed: int, g_full=None):
+    """Time the CPU oracle (fp64 NumPy SPMD simulation at mesh (1,1)) on T_s tokens."""
+    import numpy as np
+    import datagen
+    from oracle import layer as olayer
+
+    if g_full is None:
+        g_full = {k: datagen.tensor(k, s, seed=seed, rows=(np.arange(T_s) if k in ("x", "dz") else None))
+                  for k, s in datagen.layer_shapes(T_s, h, F).items()}
+    g = {k: v.astype(np.float64) for k, v in g_full.items()}
+    t0 = time.perf_counter()
+    olayer.run_layer(g, 1, 1, heads, 1)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(h: int, F: int, heads: int, seed: int, target_s: float) -> dict:
+    import numpy as np
+    import datagen
+
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        threads = os.cpu_count()
+    # weights once (not timed), then a short calibration sample and the bounded sample
+    shapes = datagen.layer_shapes(8, h, F)
+    g = {k: datagen.tensor(k, s, seed=seed) for k, s in shapes.items() if k not in ("x", "dz")}
+
+    def with_rows(n):
+        gg = dict(g)
+        gg["x"] = datagen.tensor("x", (n, h), seed=seed)
+        gg["dz"] = datagen.tensor("dz", (n, h), seed=seed)
+        return gg
+
+    t_cal = cpu_oracle_run(16, h, F, heads, seed, with_rows(16))
+    T_s = int(max(16, min(8192, target_s / max(t_cal, 1e-3) * 16)) // 8 * 8)
+    t = cpu_oracle_run(T_s, h, F, heads, seed, with_rows(T_s))
+    fl = layer_flops(T_s, h, F)
+    return {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": f"{T_s} of {8192} tokens of the same layer (h={h}, F={F}), fp64 NumPy SPMD simulation at "
+                      f"DeviceMesh(1,1), {t:.1f} s", "seconds": t, "tokens": T_s}
+
+
+def emit(obj: dict) -> None:
+    print(json.dumps(obj), flush=True)
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(a) -> None:
+    """The CPU oracle, as it stands, timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    h = a.hidden
+    F = a.ffn or 4 * h
+    heads = a.heads
+    import numpy as np
+    import datagen
+
+    shapes = datagen.layer_shapes(8, h, F)
+    g = {k: datagen.tensor(k, s, seed=a.seed) for k, s in shapes.items() if k not in ("x", "dz")}
+    # one bounded sample per step, sized so the whole run stays within a few minutes
+    t_cal = cpu_oracle_run(16, h, F, heads, a.seed, dict(g, x=datagen.tensor("x", (16, h), seed=a.seed),
+                                                           dz=datagen.tensor("dz", (16, h), seed=a.seed)))
+    budget = 150.0 / max(1, a.steps + a.warmup)
+    T_s = int(max(8, min(8192, budget / max(t_cal, 1e-3) * 16)) // 8 * 8)
+    gg = dict(g, x=datagen.tensor("x", (T_s, h), seed=a.seed), dz=datagen.tensor("dz", (T_s, h), seed=a.seed))
+    for _ in range(a.warmup):
+        cpu_oracle_run(T_s, h, F, heads, a.seed, gg)
+    times = [cpu_oracle_run(T_s, h, F, heads, a.seed, gg) for _ in range(a.steps)]
+    t = sum(times) / len(times)
+    v = layer_flops(T_s, h, F) / t / 1e12
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        threads = os.cpu_count()
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
+          "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+          "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+          "config": {"workload": f"gpt-layer linear block h{h} a{heads} ffn{F}, {T_s}-token sample per step "
+                                 f"(of b{a.batch} s{a.seq})", "mesh": [1, 1], "tokens_per_step": T_s},
+          "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                           "sample": f"{T_s} tokens per step, fp64 NumPy SPMD simulation"},
+          "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+          "gpu_launches": 0})
+
+
+# ----------------------------------------------------------------------------- ATP arm
+def main() -> None:
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_08658_b200 as atp
+    from paper_2301_08658_b200 import _abi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    h, heads = a.hidden, a.heads
+    F = a.ffn or 4 * h
+    T = a.batch * a.seq
+    chunks = a.chunks or (1 if world == 1 else 4)
+
+    # ---- mesh: explicit, or ATP's search on the single-layer NVSwitch HCM
+    plan = None
+    if a.mesh:
+        d1, d2 = (int(v) for v in a.mesh.lower().split("x"))
+    elif world == 1:
+        d1, d2 = 1, 1
+    else:
+        plan = atp.atp_search([atp.HcmLayer(world, 900.0, 900.0)], 1, a.batch, a.seq, h, heads, 2)
+        d1, d2 = plan["chosen"]
+    assert d1 * d2 == world
+
+    uid = atp.atp_get_unique_id() if rank == 0 else bytes(128)
+    if world > 1:
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    mesh = atp.Mesh.distributed(d1, d2, rank, uid, local_rank)
+    ctas = a.gemm_ctas if a.gemm_ctas >= 0 else (0 if world == 1 else 132)
+    mesh.set_gemm_ctas(ctas)
+
+    bufs = atp.alloc_layer_rank(d1, d2, rank, T, h, F, dev, a.seed)
+    call = atp.LayerCall(mesh, [bufs], T, h, F, heads, chunks, True)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(n_steps: int) -> float:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_steps):
+            call(stream)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / n_steps
+        barrier()
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(max(3, a.warmup)):
+        call(stream)
+    torch.cuda.synchronize()
+
+    # ---- timed region (clocks sampled during it)
+    sampler = ClockSampler(local_rank)
+    c0 = C_u64 = None
+    import ctypes as C
+
+    n0 = C.c_uint64()
+    _abi.check(_abi.lib().atp_launch_count(C.byref(n0)))
+    t0 = time.time()
+    ms = timed(a.steps)
+    t1 = time.time()
+    n1 = C.c_uint64()
+    _abi.check(_abi.lib().atp_launch_count(C.byref(n1)))
+    clocks = sampler.stop(t0, t1)
+    launches = int(n1.value - n0.value)
+
+    fl = layer_flops(T, h, F)
+    value = fl / (ms * 1e-3) / 1e12
+    per_gpu = value / world
+
+    # ---- comm-disabled twin (exposed communication)
+    exposed = 0.0
+    ms_nocomm = ms
+    if d1 > 1 or d2 > 1:
+        _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 0))
+        ms_nocomm = timed(max(10, a.steps // 2))
+        _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 1))
+        exposed = max(0.0, ms - ms_nocomm)
+
+    # ---- profiled pass: per-class device time from CUDA events on the launching streams
+    prof = _abi.Profile()
+    n_prof = max(5, min(a.steps, 30))
+    _abi.check(_abi.lib().atp_profile_begin(mesh.handle))
+    ms_prof = timed(n_prof)
+    _abi.check(_abi.lib().atp_profile_end(mesh.handle, C.byref(prof)))
+    pk = peaks(a.peaks)
+    gemm_ms = prof.ms[0] / n_prof
+    gemm_launch_ms = prof.ms[0] / max(1, prof.launches[0])
+    gemm_tflops = (prof.flops[0] / n_prof) / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    peak_tc = pk["bf16_tflops_sustained"] or pk["bf16_tflops"]
+    roofline = {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_tc, "unit": "TFLOP/s",
+                "frac": gemm_tflops / peak_tc, "traffic": None,
+                "kernel": "gemm_sm100_kernel (tcgen05, all GEMM launches of the step)",
+                "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside a long step)",
+                "gemm_share_of_step": gemm_ms / ms_prof if ms_prof > 0 else None,
+                "gemm_launches_per_step": prof.launches[0] / n_prof, "avg_gemm_launch_ms": gemm_launch_ms,
+                "elementwise_ms_per_step": prof.ms[1] / n_prof,
+                "elementwise_gbs": (prof.bytes[1] / max(prof.ms[1], 1e-9)) / 1e6,
+                "allreduce_ms_per_step": prof.ms[2] / n_prof,
+                "allreduce_busbw_gbs": (prof.bytes[2] / max(prof.ms[2], 1e-9)) / 1e6 if prof.ms[2] > 0 else None,
+                "profiled_ms_per_step": ms_prof,
+                "layer_roofline_frac": (fl / world / (peak_tc * 1e12)) / (ms * 1e-3)}
+
+    # ---- e2e: inputs H2D from pinned memory, result D2H, every step
+    e2e = None
+    if not a.no_e2e:
+        hx = bufs["x"].cpu().pin_memory()
+        hdz = bufs["dz"].cpu().pin_memory()
+        res = [bufs[k] for k in ("dbqkv", "dbo", "db1", "db2")]
+        hres = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res]
+        h2d = hx.numel() * hx.element_size() + hdz.numel() * hdz.element_size()
+        d2h = sum(r.numel() * r.element_size() for r in res)
+
+        def e2e_step():
+            bufs["x"].copy_(hx, non_blocking=True)
+            bufs["dz"].copy_(hdz, non_blocking=True)
+            call(stream)
+            for r, hr in zip(res, hres):
+                hr.copy_(r, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(5, min(a.steps, 50))
+        e0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / n_e2e
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
+               "api": "paper_2301_08658_b200.LayerCall -> atp_layer_fwd_bwd (C ABI)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(h, F, heads, a.seed, a.cpu_seconds)
+
+    mesh.destroy()
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"gpt-layer linear block (QKV/Out/FC1/FC2 fwd+bwd) h{h} a{heads} ffn{F} "
+                                   f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}",
+                       "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
+                       "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
+                       "mesh_source": "flag" if a.mesh else ("N=1" if world == 1 else "atp_search(uniform 900 GB/s HCM)"),
+                       "l2": "working set > 126 MB L2 (weights+activations ~1-2 GB), no flush"},
+            "tflops_per_gpu": per_gpu, "exposed_comm_ms": exposed, "ms_per_step_comm_disabled": ms_nocomm,
+            "flops_per_step": fl, "clocks": clocks, "gpu_launches": launches,
+            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        if plan is not None:
+            out["search"] = {"chosen": plan["chosen"], "ranked": [(r["d1"], r["d2"], r["t_comm"]) for r in plan["ranked"]]}
+        emit(out)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

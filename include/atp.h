@@ -1,0 +1,325 @@
+/*
+ * atp.h — C ABI of libatp: the B200-native hot path of ATP, Adaptive Tensor
+ * Parallelism (arXiv 2301.08658).  "P:n" cites /root/reference/PAPER.md line n.
+ *
+ * The library implements the column-first / row-first tensor-parallel
+ * transformer linear block on a DeviceMesh(d1, d2), forward and backward,
+ * with chunk-based communication/computation overlap, plus the paper's
+ * communication cost model and mesh search.
+ *
+ * Conventions (all entry points)
+ *   - Status codes, never exceptions or aborts.  On failure atp_last_error()
+ *     returns a thread-local message.  Shapes are validated BEFORE anything is
+ *     enqueued, so a failed call has no device side effects.
+ *   - Device pointers: bf16 (`ATP_BF16`) row-major, contiguous rows, 16-byte
+ *     aligned.  The caller owns every buffer (activations, weights, saved
+ *     tensors, gradients, workspace) and the stream; the library owns only the
+ *     communicators it creates, its communication stream(s) and its events.
+ *   - Calls are asynchronous: they enqueue on the caller's `stream` and return;
+ *     results are valid in stream order.  No hidden allocation on the hot path.
+ *   - Weights are in math orientation W[in, out] (y = x W), sharded per P:218:
+ *       column-first W: [Shard(1), Shard(0)] -> local [in/d2, out/d1]
+ *       row-first    W: [Shard(0), Shard(1)] -> local [in/d1, out/d2]
+ *     Activations between blocks are [Replicate, Shard(1)]: rank
+ *     (i1, i2) holds the column block i2, i.e. a local [T, h/d2] matrix.
+ *   - rank = i1*d2 + i2.  Dim-1 groups = ranks sharing i2 (d1 members);
+ *     dim-2 groups = ranks sharing i1 (d2 members).
+ *   - Mesh handles come in two kinds.  A *distributed* mesh (atp_mesh_init)
+ *     is one rank of an SPMD job, one process per GPU, collectives through
+ *     NCCL; the per-rank argument pointer `args` points to ONE struct.  A
+ *     *virtual* mesh (atp_vmesh_init) holds all d1*d2 ranks in one process on
+ *     one device (test/validation vehicle: same schedule, same kernels, the
+ *     group sums done by a library kernel); `args` points to an ARRAY of d1*d2
+ *     structs in rank order.
+ */
+#ifndef ATP_H_
+#define ATP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ATP_VERSION "0.1.0"
+
+typedef enum {
+  ATP_OK = 0,
+  ATP_ERR_INVALID = 1,     /* bad argument (mesh size, dim, null pointer ...) */
+  ATP_ERR_SHAPE = 2,       /* divisibility / alignment precondition violated  */
+  ATP_ERR_CUDA = 3,        /* CUDA runtime error                              */
+  ATP_ERR_NCCL = 4,        /* NCCL error                                      */
+  ATP_ERR_EMPTY = 5,       /* search: no admissible candidate mesh            */
+  ATP_ERR_UNSUPPORTED = 6  /* feature not built / not available              */
+} atp_status;
+
+typedef enum { ATP_BF16 = 0 } atp_dtype;
+
+typedef struct atp_mesh atp_mesh; /* opaque */
+
+const char* atp_last_error(void);
+const char* atp_version(void);
+
+/* ------------------------------------------------------------------ mesh
+ * DeviceMesh(d1, d2).  atp_get_unique_id fills 128 bytes (an
+ * ncclUniqueId) on rank 0; the caller broadcasts them (e.g. over
+ * torch.distributed) and every rank calls atp_mesh_init with the same bytes.
+ * The library creates the world communicator on `cuda_device`, splits it into
+ * the dim-1 communicator (color = i2, key = i1) and the dim-2 communicator
+ * (color = i1, key = i2), and creates its communication stream and events.
+ * Errors: ATP_ERR_INVALID if d1 < 1, d2 < 1 or world_rank out of range;
+ * ATP_ERR_NCCL / ATP_ERR_CUDA on library failures.
+ */
+atp_status atp_get_unique_id(uint8_t uid_out[128]);
+atp_status atp_mesh_init(int d1, int d2, int world_rank, const uint8_t uid[128], int cuda_device,
+                         atp_mesh** out);
+/* All d1*d2 ranks of a mesh in this process on `cuda_device` (see header). */
+atp_status atp_vmesh_init(int d1, int d2, int cuda_device, atp_mesh** out);
+atp_status atp_mesh_destroy(atp_mesh* mesh);
+/* Coordinates of a distributed mesh's rank (virtual mesh: ATP_ERR_INVALID). */
+atp_status atp_mesh_coords(const atp_mesh* mesh, int* i1, int* i2);
+atp_status atp_mesh_dims(const atp_mesh* mesh, int* d1, int* d2, int* is_virtual);
+/* Pure: groups of mesh dimension `dim` (1 or 2), written as consecutive
+ * member lists into out[d1*d2] (dim 1: d2 groups of d1; dim 2: d1 groups of
+ * d2), members in ascending mesh coordinate. */
+atp_status atp_mesh_groups(int d1, int d2, int dim, int* out);
+/* Cap the CTAs of the persistent GEMMs (0 = all SMs) so that an overlapped
+ * NCCL kernel keeps SMs of its own (SURVEY §7 "SM sharing"). */
+atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas);
+
+/* Measurement hooks (bench.py).  atp_mesh_set_comm_enabled(mesh, 0) replaces
+ * every all-reduce by a no-op (events still recorded, so the schedule and its
+ * dependencies are unchanged): the comm-disabled twin of SURVEY §8(d) that
+ * gives exposed communication = t(layer) - t(layer, comm disabled); results
+ * are then wrong by construction.  atp_profile_begin(mesh) makes the executor
+ * bracket every kernel / all-reduce it enqueues with CUDA timing events on the
+ * stream it is launched on; atp_profile_end synchronises on those events and
+ * returns, per class (0 = tcgen05 GEMM, 1 = elementwise, 2 = all-reduce),
+ * the launch count, summed device milliseconds, and the algorithmic FLOPs
+ * (GEMM: 2MNK) and bytes (GEMM: A+B+C; elementwise: reads+writes; all-reduce:
+ * ring bytes sent 2(p-1)/p*n*2) of those launches.  atp_launch_count() is a
+ * process-wide count of kernels libatp has launched (NCCL's not included). */
+typedef struct {
+  int64_t launches[3];
+  double ms[3];
+  double flops[3];
+  double bytes[3];
+} atp_profile;
+
+atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled);
+atp_status atp_profile_begin(atp_mesh* mesh);
+atp_status atp_profile_end(atp_mesh* mesh, atp_profile* out);
+atp_status atp_launch_count(uint64_t* out);
+
+/* ------------------------------------------------------------------ local GEMM
+ * One local shard contraction on the tcgen05 tensor cores (the building block
+ * of F3/F6/F8/F11 and of dX = dY W^T, dW = X^T dY):
+ *     C[M,N] = A[M,K] * B[N,K]^T (+ bias[N]),  bf16 in, fp32 accumulate.
+ * a_mn = 0: A stored row-major [M,K] with pitch lda; 1: A stored [K,M].
+ * b_mn = 0: B stored row-major [N,K] with pitch ldb; 1: B stored [K,N].
+ * out_f32 = 1 writes fp32 C (pitch ldc), else bf16.  (a_mn, b_mn) = (1, 0)
+ * is unsupported.  N, K multiples of 8 (M too when a_mn).  max_ctas = 0: all SMs.
+ */
+atp_status atp_gemm(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
+                    void* C, int64_t ldc, int out_f32, const void* bias, int64_t M, int64_t N,
+                    int64_t K, int max_ctas, void* stream);
+
+/* ------------------------------------------------------------------ linears
+ * Column-first TP linear (Fig. 5 right): x [M, K/d2] ([Replicate,
+ * Shard(1)]), w [K/d2, N/d1] ([Shard(1), Shard(0)]), bias [N/d1] or NULL;
+ * y [M, N/d1] = all-reduce over mesh dim 2 of x w (+ bias once), i.e.
+ * [Shard(1), Replicate].  Row-first (Fig. 5 left): x [M, K/d1]
+ * ([Shard(1), Replicate]), w [K/d1, N/d2], y [M, N/d2] all-reduced over dim 1
+ * ([Replicate, Shard(1)]).  The M rows are processed in `chunks` chunks; the
+ * all-reduce of chunk k overlaps the GEMM of chunk k+1 (§4.1).
+ * Backward: dx = all-reduce over the conjugate dim (column-first: 1,
+ * row-first: 2) of dy w^T; dw = x^T dy (fp32, local, no communication);
+ * dbias = column sums of dy (fp32) or NULL.  The dw GEMM runs after the dx
+ * chunks are enqueued so it overlaps their all-reduces (§4.2).
+ * Errors: ATP_ERR_SHAPE if K % d, N % d, M % chunks, or the 8-element
+ * alignment of the GEMM fails.
+ */
+typedef struct {
+  const void* x;
+  const void* w;
+  const void* bias; /* may be NULL */
+  void* y;
+} atp_linear_fwd_args;
+
+typedef struct {
+  const void* x;  /* saved forward input */
+  const void* w;
+  const void* dy;
+  void* dx;       /* bf16 */
+  float* dw;      /* fp32 */
+  float* dbias;   /* fp32 or NULL */
+} atp_linear_bwd_args;
+
+atp_status atp_linear_colfirst_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, int64_t M,
+                                   int64_t K, int64_t N, int chunks, atp_dtype dtype, void* stream);
+atp_status atp_linear_rowfirst_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, int64_t M,
+                                   int64_t K, int64_t N, int chunks, atp_dtype dtype, void* stream);
+atp_status atp_linear_colfirst_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, int64_t M,
+                                   int64_t K, int64_t N, int chunks, atp_dtype dtype, void* stream);
+atp_status atp_linear_rowfirst_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, int64_t M,
+                                   int64_t K, int64_t N, int chunks, atp_dtype dtype, void* stream);
+
+/* ------------------------------------------------------------------ composites
+ * Feed-forward block (Fig. 6b): FC1 column-first + f3 (dim 2),
+ * U = . + b1 (saved), H = GeLU(U) (exact erf, saved), FC2 row-first + f4
+ * (dim 1), Z = X + . + b2 (residual added after the all-reduce).
+ * Local shapes (T tokens, h, F): x, z, dz, dx [T, h/d2]; w1 [h/d2, F/d1];
+ * b1 [F/d1]; w2 [F/d1, h/d2]; b2 [h/d2]; u, h_act [T, F/d1];
+ * dw1 fp32 [h/d2, F/d1]; db1 fp32 [F/d1]; dw2 fp32 [F/d1, h/d2]; db2 fp32 [h/d2];
+ * workspace dh [T, F/d1] bf16.
+ * Errors: ATP_ERR_SHAPE unless h % d2 == 0, F % d1 == 0, T % chunks == 0 and
+ * all local widths are multiples of 8.
+ */
+typedef struct {
+  const void* x; const void* w1; const void* b1; const void* w2; const void* b2;
+  void* u; void* h_act; void* z;
+} atp_mlp_fwd_args;
+
+typedef struct {
+  const void* x; const void* w1; const void* w2; const void* u; const void* h_act; const void* dz;
+  void* dx; float* dw1; float* db1; float* dw2; float* db2;
+  void* ws_dh;
+} atp_mlp_bwd_args;
+
+atp_status atp_mlp_fwd(atp_mesh* mesh, const atp_mlp_fwd_args* args, int64_t T, int64_t h,
+                       int64_t F, int chunks, atp_dtype dtype, void* stream);
+atp_status atp_mlp_bwd(atp_mesh* mesh, const atp_mlp_bwd_args* args, int64_t T, int64_t h,
+                       int64_t F, int chunks, atp_dtype dtype, void* stream);
+
+/* Attention projections (Fig. 6a): QKV column-first + f1 (dim 2), the
+ * attention core, Output row-first + f2 (dim 1), Y = X + . + bo.
+ * Wqkv columns are head-interleaved (head*3d + {q,k,v}*d + j) so that the
+ * column-first split gives rank i1 the heads [i1*a/d1, (i1+1)*a/d1).
+ * core = ATP_CORE_SUM_QKV: zero-FLOP stand-in ctx = Q + K + V per head
+ * (the softmax core of Eq. 1 is outside this path).
+ * Local shapes: x, y, dy, dx [T, h/d2]; wqkv [h/d2, 3h/d1]; bqkv [3h/d1];
+ * wo [h/d1, h/d2]; bo [h/d2]; qkv [T, 3h/d1]; ctx [T, h/d1];
+ * dwqkv fp32 [h/d2, 3h/d1]; dbqkv fp32 [3h/d1]; dwo fp32 [h/d1, h/d2];
+ * dbo fp32 [h/d2]; workspaces dctx [T, h/d1], dqkv [T, 3h/d1] bf16.
+ * Errors: ATP_ERR_SHAPE unless heads % d1 == 0, h % heads == 0, h % d2 == 0,
+ * T % chunks == 0 and local widths are multiples of 8.
+ */
+typedef enum { ATP_CORE_SUM_QKV = 0 } atp_core;
+
+typedef struct {
+  const void* x; const void* wqkv; const void* bqkv; const void* wo; const void* bo;
+  void* qkv; void* ctx; void* y;
+} atp_attn_fwd_args;
+
+typedef struct {
+  const void* x; const void* wqkv; const void* wo; const void* ctx; const void* dy;
+  void* dx; float* dwqkv; float* dbqkv; float* dwo; float* dbo;
+  void* ws_dctx; void* ws_dqkv;
+} atp_attn_bwd_args;
+
+atp_status atp_attn_proj_fwd(atp_mesh* mesh, const atp_attn_fwd_args* args, int64_t T, int64_t h,
+                             int64_t heads, int chunks, atp_core core, atp_dtype dtype,
+                             void* stream);
+atp_status atp_attn_proj_bwd(atp_mesh* mesh, const atp_attn_bwd_args* args, int64_t T, int64_t h,
+                             int64_t heads, int chunks, atp_core core, atp_dtype dtype,
+                             void* stream);
+
+/* Whole linear block of one GPT layer, forward then backward, as ONE chunk
+ * pipeline: chunk k of a block waits only on chunk k's all-reduce of the
+ * block before it (Fig. 7; reading G14), so the last all-reduce of the
+ * attention block overlaps the first FC1 GEMM.  Shapes as above (F = ffn). */
+typedef struct {
+  atp_attn_fwd_args attn;   /* attn.y is the MLP input (y1)              */
+  atp_mlp_fwd_args mlp;     /* mlp.x must equal attn.y                   */
+  atp_mlp_bwd_args mlp_b;   /* mlp_b.dz = upstream grad, mlp_b.dx = dy1  */
+  atp_attn_bwd_args attn_b; /* attn_b.dy must equal mlp_b.dx             */
+} atp_layer_args;
+
+atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t T, int64_t h,
+                             int64_t F, int64_t heads, int chunks, int do_backward,
+                             atp_dtype dtype, void* stream);
+
+/* ------------------------------------------------------------------ cost model
+ * Hierarchical communication matrix (§3.4): layers outermost
+ * first; layer j: R_j ranks, P2P bandwidth between two layer-j ranks and the
+ * group bandwidth of one layer-j rank, GB/s per direction.
+ */
+#define ATP_MAX_HCM_LAYERS 8
+#define ATP_MAX_PLAN 64
+
+typedef struct {
+  int n_layers;
+  int ranks[ATP_MAX_HCM_LAYERS];
+  double p2p_gbps[ATP_MAX_HCM_LAYERS];
+  double group_gbps[ATP_MAX_HCM_LAYERS];
+} atp_hcm;
+
+typedef struct {
+  int64_t L, b, s, h, heads, bytes_per_elem;
+} atp_model;
+
+/* Measured algorithm bandwidths (P:482 calibration, reading G11); a value
+ * <= 0 means "not calibrated" for that dimension. */
+typedef struct {
+  int n;
+  int d1[ATP_MAX_PLAN], d2[ATP_MAX_PLAN];
+  double b1[ATP_MAX_PLAN], b2[ATP_MAX_PLAN];
+} atp_calib;
+
+typedef struct {
+  int d1, d2;
+  double b1_prime, b2_prime; /* Eq. 3 (GB/s); 0 when NoComm or calibrated */
+  double b1, b2;             /* Eq. 4 algorithm bandwidth (GB/s); 0 = NoComm */
+  double t_f[4];             /* Eq. 2 terms f1..f4 (seconds, x 2Lbs*bytes)   */
+  double t_comm;             /* seconds                                      */
+  int calibrated;
+} atp_cost;
+
+typedef struct {
+  int n_ranked;
+  atp_cost ranked[ATP_MAX_PLAN]; /* ascending t_comm; ties: larger d1 first */
+  int chosen;                    /* index into ranked (always 0)            */
+  int n_rejected;
+  int rejected_d1[ATP_MAX_PLAN], rejected_d2[ATP_MAX_PLAN];
+} atp_plan;
+
+/* ATP mesh search (§3.5): Eq. 3 -> Eq. 4 -> Eq. 2 for every
+ * (d1, d2) with d1*d2 = n_devices (= product of HCM ranks), argmin T_comm.
+ * calib may be NULL.  Deterministic; doubles evaluated in the canonical order
+ * documented in DESIGN.md so they equal the oracle's bit for bit.
+ * Errors: ATP_ERR_INVALID (HCM product != n_devices, non-positive bandwidth,
+ * bad model); ATP_ERR_EMPTY if no mesh is admissible. */
+atp_status atp_search(const atp_hcm* hcm, const atp_model* model, int n_devices,
+                      const atp_calib* calib, atp_plan* out);
+
+/* Eq. 3 alone for one mesh (NoComm -> 0). ATP_ERR_SHAPE on misalignment. */
+atp_status atp_effective_bandwidth(const atp_hcm* hcm, int d1, int d2, double* b1_prime,
+                                   double* b2_prime);
+
+/* Executed collective list of one layer fwd+bwd (reading G4): up to `cap`
+ * entries of (phase 0=fwd/1=bwd, block 0=qkv/1=out/2=fc1/3=fc2, dim, p,
+ * elements per rank); *n_calls = the full count.  Totals are int64 exact. */
+typedef struct {
+  int phase, block, dim, p;
+  int64_t elems;
+} atp_call;
+
+atp_status atp_comm_volume(int d1, int d2, int64_t T, int64_t h, int64_t F, int chunks,
+                           atp_call* calls, int cap, int* n_calls, int64_t* dim1_elems,
+                           int64_t* dim2_elems);
+
+/* ------------------------------------------------------------------ probe
+ * Bandwidth probe feeding the HCM (§3.4) and the calibration, on a
+ * distributed mesh spanning all ranks: times ncclAllReduce on each mesh
+ * dimension's communicator with every group active concurrently.
+ * msg_bytes: message size per rank; result bus bandwidths (GB/s, per
+ * direction, = algBW * 2(p-1)/p) for dim 1 and dim 2 (0 if size 1), and the
+ * algorithm bandwidths (bytes / time).  Collective call: all ranks. */
+atp_status atp_probe_allreduce(atp_mesh* mesh, int dim, size_t msg_bytes, int iters, void* buf,
+                               double* busbw_gbps, double* algbw_gbps, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATP_H_ */

@@ -1,0 +1,12 @@
+"""B200-native ATP (Adaptive Tensor Parallelism, arXiv 2301.08658) hot path.
+
+The product is ``libatp.so`` (C ABI, include/atp.h): tcgen05/TMEM/TMA GEMMs,
+HBM-bound epilogue kernels, the chunked dual-stream pipeline over NCCL, and
+the Eq. 2-4 mesh search.  This package is a thin ctypes binding to it.
+"""
+from .api import (  # noqa: F401
+    HcmLayer, LayerCall, Mesh, alloc_layer_rank, atp_attn_proj_bwd, atp_attn_proj_fwd, atp_comm_volume,
+    atp_effective_bandwidth, atp_gemm, atp_get_unique_id, atp_layer_fwd_bwd, atp_linear_bwd, atp_linear_fwd,
+    atp_mesh_groups, atp_mlp_bwd, atp_mlp_fwd, atp_probe_allreduce, atp_search,
+)
+from ._abi import AtpError, LIB_PATH  # noqa: F401

@@ -1,0 +1,284 @@
+"""Thin Python binding over libatp (same names as include/atp.h).
+
+Argument marshalling only: every step of the hot path runs in libatp's CUDA
+kernels / NCCL calls.  PyTorch supplies device memory, streams and (in
+bench.py) the process group used to broadcast the NCCL unique id.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+from . import _abi
+from ._abi import check, lib
+from . import layout
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# ------------------------------------------------------------------ mesh
+def atp_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().atp_get_unique_id(buf))
+    return buf.raw
+
+
+class Mesh:
+    """DeviceMesh(d1, d2) handle.  ``Mesh.virtual`` holds all ranks in this
+    process on one GPU; ``Mesh.distributed`` is one rank of an SPMD job."""
+
+    def __init__(self, handle, d1: int, d2: int, is_virtual: bool, rank: int = 0):
+        self.handle = handle
+        self.d1, self.d2 = d1, d2
+        self.is_virtual = is_virtual
+        self.rank = rank
+
+    @classmethod
+    def virtual(cls, d1: int, d2: int, device: int = 0) -> "Mesh":
+        h = C.c_void_p()
+        check(lib().atp_vmesh_init(d1, d2, device, C.byref(h)))
+        return cls(h, d1, d2, True)
+
+    @classmethod
+    def distributed(cls, d1: int, d2: int, rank: int, uid: bytes, device: int) -> "Mesh":
+        h = C.c_void_p()
+        check(lib().atp_mesh_init(d1, d2, rank, uid, device, C.byref(h)))
+        return cls(h, d1, d2, False, rank)
+
+    @property
+    def n_local_ranks(self) -> int:
+        return self.d1 * self.d2 if self.is_virtual else 1
+
+    def local_ranks(self) -> list[int]:
+        return list(range(self.d1 * self.d2)) if self.is_virtual else [self.rank]
+
+    def coords(self) -> tuple[int, int]:
+        i1, i2 = C.c_int(), C.c_int()
+        check(lib().atp_mesh_coords(self.handle, C.byref(i1), C.byref(i2)))
+        return i1.value, i2.value
+
+    def set_gemm_ctas(self, n: int) -> None:
+        check(lib().atp_mesh_set_gemm_ctas(self.handle, n))
+
+    def destroy(self) -> None:
+        if self.handle:
+            check(lib().atp_mesh_destroy(self.handle))
+            self.handle = None
+
+
+def atp_mesh_groups(d1: int, d2: int, dim: int) -> list[list[int]]:
+    out = (C.c_int * (d1 * d2))()
+    check(lib().atp_mesh_groups(d1, d2, dim, out))
+    flat = list(out)
+    size = d1 if dim == 1 else d2
+    return [flat[i:i + size] for i in range(0, len(flat), size)]
+
+
+# ------------------------------------------------------------------ local GEMM
+def atp_gemm(A, B, Cout, a_mn: bool = False, b_mn: bool = False, bias=None, max_ctas: int = 0, stream=None):
+    """Cout[M,N] = A[M,K] B[N,K]^T (+bias) on the tcgen05 tensor cores.
+
+    a_mn: A is given as its transpose [K,M]; b_mn: B given as [K,N]."""
+    import torch
+
+    M, N = Cout.shape
+    K = A.shape[0] if a_mn else A.shape[1]
+    check(lib().atp_gemm(A.data_ptr(), A.stride(0), int(a_mn), B.data_ptr(), B.stride(0), int(b_mn),
+                         Cout.data_ptr(), Cout.stride(0), int(Cout.dtype == torch.float32), _ptr(bias),
+                         M, N, K, max_ctas, _stream(stream)))
+
+
+# ------------------------------------------------------------------ linears
+def _arr(struct_cls, items):
+    arr = (struct_cls * len(items))()
+    for i, it in enumerate(items):
+        arr[i] = it
+    return arr
+
+
+def atp_linear_fwd(mesh: Mesh, colfirst: bool, per_rank: list[dict], M: int, K: int, N: int, chunks: int = 1,
+                   stream=None):
+    """per_rank: [{x, w, bias (or None), y}] — one dict per local rank (torch tensors)."""
+    a = _arr(_abi.LinearFwdArgs, [_abi.LinearFwdArgs(d["x"].data_ptr(), d["w"].data_ptr(), _ptr(d.get("bias")),
+                                                     d["y"].data_ptr()) for d in per_rank])
+    f = lib().atp_linear_colfirst_fwd if colfirst else lib().atp_linear_rowfirst_fwd
+    check(f(mesh.handle, a, M, K, N, chunks, _abi.ATP_BF16, _stream(stream)))
+
+
+def atp_linear_bwd(mesh: Mesh, colfirst: bool, per_rank: list[dict], M: int, K: int, N: int, chunks: int = 1,
+                   stream=None):
+    """per_rank: [{x, w, dy, dx, dw (fp32), dbias (fp32 or None)}]."""
+    a = _arr(_abi.LinearBwdArgs, [_abi.LinearBwdArgs(d["x"].data_ptr(), d["w"].data_ptr(), d["dy"].data_ptr(),
+                                                     d["dx"].data_ptr(), _ptr(d.get("dw")), _ptr(d.get("dbias")))
+                                  for d in per_rank])
+    f = lib().atp_linear_colfirst_bwd if colfirst else lib().atp_linear_rowfirst_bwd
+    check(f(mesh.handle, a, M, K, N, chunks, _abi.ATP_BF16, _stream(stream)))
+
+
+# ------------------------------------------------------------------ layer buffers
+def _attn_fwd(b):
+    return _abi.AttnFwdArgs(b["x"].data_ptr(), b["wqkv"].data_ptr(), _ptr(b.get("bqkv")), b["wo"].data_ptr(),
+                            _ptr(b.get("bo")), b["qkv"].data_ptr(), b["ctx"].data_ptr(), b["y1"].data_ptr())
+
+
+def _mlp_fwd(b):
+    return _abi.MlpFwdArgs(b["y1"].data_ptr(), b["w1"].data_ptr(), _ptr(b.get("b1")), b["w2"].data_ptr(),
+                           _ptr(b.get("b2")), b["u"].data_ptr(), b["h"].data_ptr(), b["z"].data_ptr())
+
+
+def _mlp_bwd(b):
+    return _abi.MlpBwdArgs(b["y1"].data_ptr(), b["w1"].data_ptr(), b["w2"].data_ptr(), b["u"].data_ptr(),
+                           b["h"].data_ptr(), b["dz"].data_ptr(), b["dy1"].data_ptr(), _ptr(b["dw1"]),
+                           _ptr(b["db1"]), _ptr(b["dw2"]), _ptr(b["db2"]), b["ws_dh"].data_ptr())
+
+
+def _attn_bwd(b):
+    return _abi.AttnBwdArgs(b["x"].data_ptr(), b["wqkv"].data_ptr(), b["wo"].data_ptr(), b["ctx"].data_ptr(),
+                            b["dy1"].data_ptr(), b["dx"].data_ptr(), _ptr(b["dwqkv"]), _ptr(b["dbqkv"]),
+                            _ptr(b["dwo"]), _ptr(b["dbo"]), b["ws_dctx"].data_ptr(), b["ws_dqkv"].data_ptr())
+
+
+def alloc_layer_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, device, seed: int, with_bias: bool = True,
+                     inputs: bool = True) -> dict:
+    """Allocate one rank's layer buffers; fill inputs/weights from the seeded
+    counter-based generator (datagen) directly on the device."""
+    import torch
+    import datagen
+
+    w = layout.local_widths(d1, d2, h, F)
+    hc, h1, q1, F1 = w["hc"], w["h1"], w["q1"], w["F1"]
+    bf, f32 = torch.bfloat16, torch.float32
+    box = layout.shard_boxes(d1, d2, rank, T, h, F)
+    shapes = datagen.layer_shapes(T, h, F)
+    b = {}
+    for name in ("x", "dz", "wqkv", "wo", "w1", "w2") + (("bqkv", "bo", "b1", "b2") if with_bias else ()):
+        r0, nr, c0, nc = box[name]
+        if inputs:
+            t = datagen.torch_block(name, shapes[name], r0, nr, c0, nc, device, seed=seed)
+        else:
+            t = torch.empty((nr, nc), dtype=bf, device=device)
+        b[name] = t.reshape(-1) if name.startswith("b") else t
+    E = lambda *s, dt=bf: torch.empty(s, dtype=dt, device=device)
+    b.update(qkv=E(T, q1), ctx=E(T, h1), y1=E(T, hc), u=E(T, F1), h=E(T, F1), z=E(T, hc),
+             dy1=E(T, hc), dx=E(T, hc), ws_dh=E(T, F1), ws_dctx=E(T, h1), ws_dqkv=E(T, q1),
+             dwqkv=E(hc, q1, dt=f32), dbqkv=E(q1, dt=f32), dwo=E(h1, hc, dt=f32), dbo=E(hc, dt=f32),
+             dw1=E(hc, F1, dt=f32), db1=E(F1, dt=f32), dw2=E(F1, hc, dt=f32), db2=E(hc, dt=f32))
+    return b
+
+
+def atp_attn_proj_fwd(mesh, bufs, T, h, heads, chunks=1, stream=None):
+    a = _arr(_abi.AttnFwdArgs, [_attn_fwd(b) for b in bufs])
+    check(lib().atp_attn_proj_fwd(mesh.handle, a, T, h, heads, chunks, _abi.ATP_CORE_SUM_QKV, _abi.ATP_BF16,
+                                  _stream(stream)))
+
+
+def atp_attn_proj_bwd(mesh, bufs, T, h, heads, chunks=1, stream=None):
+    a = _arr(_abi.AttnBwdArgs, [_attn_bwd(b) for b in bufs])
+    check(lib().atp_attn_proj_bwd(mesh.handle, a, T, h, heads, chunks, _abi.ATP_CORE_SUM_QKV, _abi.ATP_BF16,
+                                  _stream(stream)))
+
+
+def atp_mlp_fwd(mesh, bufs, T, h, F, chunks=1, stream=None):
+    a = _arr(_abi.MlpFwdArgs, [_mlp_fwd(b) for b in bufs])
+    check(lib().atp_mlp_fwd(mesh.handle, a, T, h, F, chunks, _abi.ATP_BF16, _stream(stream)))
+
+
+def atp_mlp_bwd(mesh, bufs, T, h, F, chunks=1, stream=None):
+    a = _arr(_abi.MlpBwdArgs, [_mlp_bwd(b) for b in bufs])
+    check(lib().atp_mlp_bwd(mesh.handle, a, T, h, F, chunks, _abi.ATP_BF16, _stream(stream)))
+
+
+class LayerCall:
+    """Pre-marshalled argument array for repeated atp_layer_fwd_bwd calls (bench loop)."""
+
+    def __init__(self, mesh, bufs, T, h, F, heads, chunks=1, backward=True):
+        self.mesh = mesh
+        self.args = _arr(_abi.LayerArgs, [_abi.LayerArgs(_attn_fwd(b), _mlp_fwd(b), _mlp_bwd(b), _attn_bwd(b))
+                                          for b in bufs])
+        self.dims = (T, h, F, heads, chunks, int(backward))
+        self._f = lib().atp_layer_fwd_bwd
+
+    def __call__(self, stream=None):
+        T, h, F, heads, chunks, bwd = self.dims
+        check(self._f(self.mesh.handle, self.args, T, h, F, heads, chunks, bwd, _abi.ATP_BF16, _stream(stream)))
+
+
+def atp_layer_fwd_bwd(mesh, bufs, T, h, F, heads, chunks=1, backward=True, stream=None):
+    LayerCall(mesh, bufs, T, h, F, heads, chunks, backward)(stream)
+
+
+# ------------------------------------------------------------------ cost model
+@dataclass
+class HcmLayer:
+    ranks: int
+    p2p_gbps: float
+    group_gbps: float
+
+
+def _hcm(layers) -> _abi.Hcm:
+    H = _abi.Hcm()
+    H.n_layers = len(layers)
+    for j, l in enumerate(layers):
+        H.ranks[j] = l.ranks
+        H.p2p_gbps[j] = l.p2p_gbps
+        H.group_gbps[j] = l.group_gbps
+    return H
+
+
+def atp_effective_bandwidth(layers, d1: int, d2: int):
+    b1, b2 = C.c_double(), C.c_double()
+    check(lib().atp_effective_bandwidth(C.byref(_hcm(layers)), d1, d2, C.byref(b1), C.byref(b2)))
+    return (b1.value if d1 > 1 else None), (b2.value if d2 > 1 else None)
+
+
+def atp_search(layers, L=1, b=4, s=2048, h=4096, heads=32, bytes_per_elem=2, calibration: dict | None = None):
+    """Ranked plan: list of dicts (ascending t_comm) and the chosen (d1, d2)."""
+    n = 1
+    for l in layers:
+        n *= l.ranks
+    m = _abi.Model(L, b, s, h, heads, bytes_per_elem)
+    cal = None
+    if calibration:
+        cal = _abi.Calib()
+        cal.n = len(calibration)
+        for i, ((d1, d2), (b1, b2)) in enumerate(calibration.items()):
+            cal.d1[i], cal.d2[i] = d1, d2
+            cal.b1[i] = b1 if b1 else 0.0
+            cal.b2[i] = b2 if b2 else 0.0
+    plan = _abi.Plan()
+    check(lib().atp_search(C.byref(_hcm(layers)), C.byref(m), n, C.byref(cal) if cal else None, C.byref(plan)))
+    ranked = []
+    for i in range(plan.n_ranked):
+        c = plan.ranked[i]
+        ranked.append({"d1": c.d1, "d2": c.d2, "b1_prime": c.b1_prime, "b2_prime": c.b2_prime, "b1": c.b1,
+                       "b2": c.b2, "t_f": list(c.t_f), "t_comm": c.t_comm, "calibrated": bool(c.calibrated)})
+    rejected = [(plan.rejected_d1[i], plan.rejected_d2[i]) for i in range(plan.n_rejected)]
+    return {"ranked": ranked, "chosen": (ranked[0]["d1"], ranked[0]["d2"]), "rejected": rejected}
+
+
+def atp_comm_volume(d1, d2, T, h, F=None, chunks=1):
+    F = 4 * h if F is None else F
+    n = C.c_int()
+    e1, e2 = C.c_int64(), C.c_int64()
+    check(lib().atp_comm_volume(d1, d2, T, h, F, chunks, None, 0, C.byref(n), C.byref(e1), C.byref(e2)))
+    calls = (_abi.Call * max(n.value, 1))()
+    check(lib().atp_comm_volume(d1, d2, T, h, F, chunks, calls, n.value, C.byref(n), C.byref(e1), C.byref(e2)))
+    names = ["qkv", "out", "fc1", "fc2"]
+    out = [(("fwd", "bwd")[c.phase], names[c.block], c.dim, c.p, c.elems) for c in calls[:n.value]]
+    return out, e1.value, e2.value
+
+
+def atp_probe_allreduce(mesh: Mesh, dim: int, buf, msg_bytes: int, iters: int = 20):
+    bus, alg, sec = C.c_double(), C.c_double(), C.c_double()
+    check(lib().atp_probe_allreduce(mesh.handle, dim, msg_bytes, iters, buf.data_ptr(), C.byref(bus),
+                                    C.byref(alg), C.byref(sec)))
+    return {"busbw_gbps": bus.value, "algbw_gbps": alg.value, "seconds": sec.value}

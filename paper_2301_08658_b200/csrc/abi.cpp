@@ -1,0 +1,370 @@
+// extern "C" entry points of libatp (declared and documented in include/atp.h).
+// Every entry validates its arguments before anything is enqueued.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/atp.h"
+#include "schedule.h"
+
+using atp::Sched;
+
+namespace {
+
+atp_status fail(atp_status s, const std::string& msg) {
+  atp::set_error(msg);
+  return s;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int n_ranks(const atp_mesh* m) { return static_cast<int>(m->rs.size()); }
+
+template <class Build>
+atp_status run(atp_mesh* m, void* stream, Build build) {
+  const int n = n_ranks(m);
+  std::vector<Sched> s(n);
+  for (int r = 0; r < n; ++r) {
+    int rc = build(atp::rank_view(m, r), r, s[r]);
+    if (rc) return static_cast<atp_status>(rc);
+  }
+  cudaSetDevice(m->device);
+  return static_cast<atp_status>(atp::execute(m, s, as_stream(stream)));
+}
+
+atp_status check_mesh(const atp_mesh* m, const void* args) {
+  if (m == nullptr) return fail(ATP_ERR_INVALID, "mesh is NULL");
+  if (args == nullptr) return fail(ATP_ERR_INVALID, "args is NULL");
+  return ATP_OK;
+}
+
+bool w8(int64_t x) { return x > 0 && x % 8 == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* atp_last_error(void) { return atp::last_error(); }
+const char* atp_version(void) { return ATP_VERSION; }
+
+// ---------------------------------------------------------------- mesh
+atp_status atp_get_unique_id(uint8_t uid_out[128]) {
+  if (uid_out == nullptr) return fail(ATP_ERR_INVALID, "atp_get_unique_id: NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(ATP_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  std::memcpy(uid_out, &id, 128);
+  return ATP_OK;
+}
+
+atp_status atp_mesh_init(int d1, int d2, int world_rank, const uint8_t uid[128], int cuda_device, atp_mesh** out) {
+  if (uid == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_init: uid is NULL");
+  return static_cast<atp_status>(atp::mesh_create(d1, d2, world_rank, uid, cuda_device, false, out));
+}
+
+atp_status atp_vmesh_init(int d1, int d2, int cuda_device, atp_mesh** out) {
+  return static_cast<atp_status>(atp::mesh_create(d1, d2, 0, nullptr, cuda_device, true, out));
+}
+
+atp_status atp_mesh_destroy(atp_mesh* mesh) { return static_cast<atp_status>(atp::mesh_destroy(mesh)); }
+
+atp_status atp_mesh_coords(const atp_mesh* mesh, int* i1, int* i2) {
+  if (mesh == nullptr || i1 == nullptr || i2 == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_coords: NULL");
+  if (mesh->is_virtual) return fail(ATP_ERR_INVALID, "atp_mesh_coords: virtual mesh has no single rank");
+  *i1 = mesh->i1;
+  *i2 = mesh->i2;
+  return ATP_OK;
+}
+
+atp_status atp_mesh_dims(const atp_mesh* mesh, int* d1, int* d2, int* is_virtual) {
+  if (mesh == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_dims: NULL");
+  if (d1) *d1 = mesh->d1;
+  if (d2) *d2 = mesh->d2;
+  if (is_virtual) *is_virtual = mesh->is_virtual ? 1 : 0;
+  return ATP_OK;
+}
+
+atp_status atp_mesh_groups(int d1, int d2, int dim, int* out) {
+  if (d1 < 1 || d2 < 1 || out == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_groups: bad arguments");
+  if (dim == 1) {
+    int o = 0;
+    for (int i2 = 0; i2 < d2; ++i2)
+      for (int i1 = 0; i1 < d1; ++i1) out[o++] = i1 * d2 + i2;
+    return ATP_OK;
+  }
+  if (dim == 2) {
+    int o = 0;
+    for (int i1 = 0; i1 < d1; ++i1)
+      for (int i2 = 0; i2 < d2; ++i2) out[o++] = i1 * d2 + i2;
+    return ATP_OK;
+  }
+  return fail(ATP_ERR_INVALID, "atp_mesh_groups: dim must be 1 or 2");
+}
+
+atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas) {
+  if (mesh == nullptr || max_ctas < 0) return fail(ATP_ERR_INVALID, "atp_mesh_set_gemm_ctas: bad arguments");
+  mesh->gemm_ctas = max_ctas;
+  return ATP_OK;
+}
+
+// ---------------------------------------------------------------- measurement hooks
+atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled) {
+  if (mesh == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_set_comm_enabled: NULL mesh");
+  mesh->comm_enabled = enabled != 0;
+  return ATP_OK;
+}
+
+atp_status atp_profile_begin(atp_mesh* mesh) {
+  if (mesh == nullptr) return fail(ATP_ERR_INVALID, "atp_profile_begin: NULL mesh");
+  mesh->profiling = true;
+  mesh->prof_used = 0;
+  return ATP_OK;
+}
+
+atp_status atp_profile_end(atp_mesh* mesh, atp_profile* out) {
+  if (mesh == nullptr || out == nullptr) return fail(ATP_ERR_INVALID, "atp_profile_end: NULL argument");
+  *out = atp_profile{};
+  cudaSetDevice(mesh->device);
+  for (size_t i = 0; i < mesh->prof_used; ++i) {
+    const atp::ProfRec& r = mesh->prof[i];
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("atp_profile_end: ") + cudaGetErrorString(e));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    out->launches[r.cls] += 1;
+    out->ms[r.cls] += ms;
+    out->flops[r.cls] += r.flops;
+    out->bytes[r.cls] += r.bytes;
+  }
+  mesh->profiling = false;
+  mesh->prof_used = 0;
+  return ATP_OK;
+}
+
+atp_status atp_launch_count(uint64_t* out) {
+  if (out == nullptr) return fail(ATP_ERR_INVALID, "atp_launch_count: NULL");
+  *out = atp::launch_count();
+  return ATP_OK;
+}
+
+// ---------------------------------------------------------------- local GEMM
+atp_status atp_gemm(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, void* C, int64_t ldc,
+                    int out_f32, const void* bias, int64_t M, int64_t N, int64_t K, int max_ctas, void* stream) {
+  if (A == nullptr || B == nullptr || C == nullptr) return fail(ATP_ERR_INVALID, "atp_gemm: NULL operand");
+  if (M <= 0 || N <= 0 || K <= 0 || M > (1 << 30) || N > (1 << 30) || K > (1 << 30))
+    return fail(ATP_ERR_SHAPE, "atp_gemm: sizes out of range");
+  if (ldc % 8 || !aligned16(C) || (bias && !aligned16(bias))) return fail(ATP_ERR_SHAPE, "atp_gemm: C/bias alignment");
+  atp::GemmDesc d;
+  d.max_ctas = max_ctas;
+  d.epi = out_f32 ? atp::EPI_F32 : atp::EPI_BF16;
+  d.ep.C = C;
+  d.ep.ldc = ldc;
+  d.ep.bias = static_cast<const __nv_bfloat16*>(bias);
+  const char* m = atp::gemm_prepare(d, A, lda, a_mn != 0, B, ldb, b_mn != 0, (int)M, (int)N, (int)K);
+  if (m) return fail(ATP_ERR_SHAPE, m);
+  atp::count_launch(1);
+  cudaError_t e = atp::gemm_launch(d, as_stream(stream));
+  if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("atp_gemm: ") + cudaGetErrorString(e));
+  return ATP_OK;
+}
+
+// ---------------------------------------------------------------- linears
+static atp_status linear_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, int64_t M, int64_t K, int64_t N,
+                             int chunks, atp_dtype dtype, void* stream, bool colfirst) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "linear: only ATP_BF16");
+  const int din = colfirst ? mesh->d2 : mesh->d1, dout = colfirst ? mesh->d1 : mesh->d2;
+  if (chunks < 1 || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) || !w8(N / dout))
+    return fail(ATP_ERR_SHAPE, "linear fwd: need M % chunks == 0, K % d_in == 0, N % d_out == 0, local widths % 8 == 0");
+  for (int r = 0; r < n_ranks(mesh); ++r)
+    if (!args[r].x || !args[r].w || !args[r].y) return fail(ATP_ERR_INVALID, "linear fwd: NULL buffer");
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    return atp::build_linear_fwd(rv, colfirst, args[r], M, K, N, chunks, out);
+  });
+}
+
+static atp_status linear_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, int64_t M, int64_t K, int64_t N,
+                             int chunks, atp_dtype dtype, void* stream, bool colfirst) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "linear: only ATP_BF16");
+  const int din = colfirst ? mesh->d2 : mesh->d1, dout = colfirst ? mesh->d1 : mesh->d2;
+  if (chunks < 1 || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) || !w8(N / dout) || M % 8)
+    return fail(ATP_ERR_SHAPE, "linear bwd: need M % chunks == 0, M % 8 == 0, K % d_in, N % d_out, local widths % 8 == 0");
+  for (int r = 0; r < n_ranks(mesh); ++r)
+    if (!args[r].x || !args[r].w || !args[r].dy || !args[r].dx) return fail(ATP_ERR_INVALID, "linear bwd: NULL buffer");
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    return atp::build_linear_bwd(rv, colfirst, args[r], M, K, N, chunks, out);
+  });
+}
+
+atp_status atp_linear_colfirst_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, int64_t M, int64_t K, int64_t N,
+                                   int chunks, atp_dtype dtype, void* stream) {
+  return linear_fwd(mesh, args, M, K, N, chunks, dtype, stream, true);
+}
+atp_status atp_linear_rowfirst_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, int64_t M, int64_t K, int64_t N,
+                                   int chunks, atp_dtype dtype, void* stream) {
+  return linear_fwd(mesh, args, M, K, N, chunks, dtype, stream, false);
+}
+atp_status atp_linear_colfirst_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, int64_t M, int64_t K, int64_t N,
+                                   int chunks, atp_dtype dtype, void* stream) {
+  return linear_bwd(mesh, args, M, K, N, chunks, dtype, stream, true);
+}
+atp_status atp_linear_rowfirst_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, int64_t M, int64_t K, int64_t N,
+                                   int chunks, atp_dtype dtype, void* stream) {
+  return linear_bwd(mesh, args, M, K, N, chunks, dtype, stream, false);
+}
+
+// ---------------------------------------------------------------- composites
+static atp_status check_layer_shapes(const atp_mesh* m, int64_t T, int64_t h, int64_t F, int64_t heads, int chunks,
+                                     bool attn, bool mlp) {
+  if (chunks < 1 || T < 1 || h < 1 || T % chunks || (T / chunks) % 8 || h % m->d2 || !w8(h / m->d2))
+    return fail(ATP_ERR_SHAPE, "layer: need T % chunks == 0, (T/chunks) % 8 == 0, h % d2 == 0, (h/d2) % 8 == 0");
+  if (mlp && (F < 1 || F % m->d1 || !w8(F / m->d1)))
+    return fail(ATP_ERR_SHAPE, "mlp: need F % d1 == 0 and (F/d1) % 8 == 0");
+  if (attn && (heads < 1 || heads % m->d1 || h % heads || (h / heads) % 8 || !w8(h / m->d1)))
+    return fail(ATP_ERR_SHAPE, "attn: need heads % d1 == 0, h % heads == 0, head dim % 8 == 0, (h/d1) % 8 == 0");
+  return ATP_OK;
+}
+
+atp_status atp_mlp_fwd(atp_mesh* mesh, const atp_mlp_fwd_args* args, int64_t T, int64_t h, int64_t F, int chunks,
+                       atp_dtype dtype, void* stream) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "mlp: only ATP_BF16");
+  if ((s = check_layer_shapes(mesh, T, h, F, 1, chunks, false, true))) return s;
+  for (int r = 0; r < n_ranks(mesh); ++r) {
+    const auto& a = args[r];
+    if (!a.x || !a.w1 || !a.w2 || !a.u || !a.h_act || !a.z) return fail(ATP_ERR_INVALID, "mlp fwd: NULL buffer");
+  }
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    atp::LayerParts p;
+    p.mlp_fwd = &args[r];
+    return atp::build_layer(rv, p, T, h, F, 1, chunks, out);
+  });
+}
+
+atp_status atp_mlp_bwd(atp_mesh* mesh, const atp_mlp_bwd_args* args, int64_t T, int64_t h, int64_t F, int chunks,
+                       atp_dtype dtype, void* stream) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "mlp: only ATP_BF16");
+  if ((s = check_layer_shapes(mesh, T, h, F, 1, chunks, false, true))) return s;
+  for (int r = 0; r < n_ranks(mesh); ++r) {
+    const auto& a = args[r];
+    if (!a.x || !a.w1 || !a.w2 || !a.u || !a.h_act || !a.dz || !a.dx || !a.ws_dh)
+      return fail(ATP_ERR_INVALID, "mlp bwd: NULL buffer");
+  }
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    atp::LayerParts p;
+    p.mlp_bwd = &args[r];
+    return atp::build_layer(rv, p, T, h, F, 1, chunks, out);
+  });
+}
+
+atp_status atp_attn_proj_fwd(atp_mesh* mesh, const atp_attn_fwd_args* args, int64_t T, int64_t h, int64_t heads,
+                             int chunks, atp_core core, atp_dtype dtype, void* stream) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_BF16");
+  if (core != ATP_CORE_SUM_QKV) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_CORE_SUM_QKV");
+  if ((s = check_layer_shapes(mesh, T, h, 8, heads, chunks, true, false))) return s;
+  for (int r = 0; r < n_ranks(mesh); ++r) {
+    const auto& a = args[r];
+    if (!a.x || !a.wqkv || !a.wo || !a.qkv || !a.ctx || !a.y) return fail(ATP_ERR_INVALID, "attn fwd: NULL buffer");
+  }
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    atp::LayerParts p;
+    p.attn_fwd = &args[r];
+    return atp::build_layer(rv, p, T, h, 8, heads, chunks, out);
+  });
+}
+
+atp_status atp_attn_proj_bwd(atp_mesh* mesh, const atp_attn_bwd_args* args, int64_t T, int64_t h, int64_t heads,
+                             int chunks, atp_core core, atp_dtype dtype, void* stream) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_BF16");
+  if (core != ATP_CORE_SUM_QKV) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_CORE_SUM_QKV");
+  if ((s = check_layer_shapes(mesh, T, h, 8, heads, chunks, true, false))) return s;
+  for (int r = 0; r < n_ranks(mesh); ++r) {
+    const auto& a = args[r];
+    if (!a.x || !a.wqkv || !a.wo || !a.ctx || !a.dy || !a.dx || !a.ws_dctx || !a.ws_dqkv)
+      return fail(ATP_ERR_INVALID, "attn bwd: NULL buffer");
+  }
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    atp::LayerParts p;
+    p.attn_bwd = &args[r];
+    return atp::build_layer(rv, p, T, h, 8, heads, chunks, out);
+  });
+}
+
+atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t T, int64_t h, int64_t F,
+                             int64_t heads, int chunks, int do_backward, atp_dtype dtype, void* stream) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "layer: only ATP_BF16");
+  if ((s = check_layer_shapes(mesh, T, h, F, heads, chunks, true, true))) return s;
+  for (int r = 0; r < n_ranks(mesh); ++r) {
+    const auto& a = args[r];
+    if (a.mlp.x != a.attn.y) return fail(ATP_ERR_INVALID, "layer: mlp.x must equal attn.y");
+    if (do_backward && (a.attn_b.dy != a.mlp_b.dx || a.mlp_b.x != a.attn.y))
+      return fail(ATP_ERR_INVALID, "layer: attn_b.dy must equal mlp_b.dx and mlp_b.x must equal attn.y");
+  }
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    atp::LayerParts p;
+    p.attn_fwd = &args[r].attn;
+    p.mlp_fwd = &args[r].mlp;
+    if (do_backward) {
+      p.mlp_bwd = &args[r].mlp_b;
+      p.attn_bwd = &args[r].attn_b;
+    }
+    return atp::build_layer(rv, p, T, h, F, heads, chunks, out);
+  });
+}
+
+// ---------------------------------------------------------------- probe
+atp_status atp_probe_allreduce(atp_mesh* mesh, int dim, size_t msg_bytes, int iters, void* buf, double* busbw_gbps,
+                               double* algbw_gbps, double* seconds) {
+  if (mesh == nullptr || buf == nullptr || iters < 1 || msg_bytes < 2 || (dim != 1 && dim != 2))
+    return fail(ATP_ERR_INVALID, "atp_probe_allreduce: bad arguments");
+  if (mesh->is_virtual) return fail(ATP_ERR_INVALID, "atp_probe_allreduce: needs a distributed mesh");
+  const int p = dim == 1 ? mesh->d1 : mesh->d2;
+  if (busbw_gbps) *busbw_gbps = 0.0;
+  if (algbw_gbps) *algbw_gbps = 0.0;
+  if (seconds) *seconds = 0.0;
+  if (p == 1) return ATP_OK;
+  cudaSetDevice(mesh->device);
+  ncclComm_t comm = dim == 1 ? mesh->dim1 : mesh->dim2;
+  cudaStream_t st = mesh->rs[0].comm;
+  const size_t count = msg_bytes / 2;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclBfloat16, ncclSum, comm, st);  // warm-up
+  cudaEventRecord(a, st);
+  for (int i = 0; i < iters && r == ncclSuccess; ++i) r = ncclAllReduce(buf, buf, count, ncclBfloat16, ncclSum, comm, st);
+  cudaEventRecord(b, st);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (r != ncclSuccess) return fail(ATP_ERR_NCCL, std::string("probe: ") + ncclGetErrorString(r));
+  if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("probe: ") + cudaGetErrorString(e));
+  const double t = (ms * 1e-3) / iters;
+  const double alg = static_cast<double>(count * 2) / t / 1e9;
+  if (algbw_gbps) *algbw_gbps = alg;
+  if (busbw_gbps) *busbw_gbps = alg * 2.0 * (p - 1) / p;
+  if (seconds) *seconds = t;
+  return ATP_OK;
+}
+
+}  // extern "C"

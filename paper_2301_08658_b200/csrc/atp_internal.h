@@ -1,0 +1,50 @@
+// Internal (non-ABI) declarations shared by the library's translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace atp {
+
+// GEMM epilogue kinds (gemm_sm100.cu).
+enum EpiKind : int {
+  EPI_BF16 = 0,       // C = bf16(acc + bias)
+  EPI_F32 = 1,        // C = fp32(acc + bias)
+  EPI_RESID = 2,      // C = bf16(aux + acc + bias)            residual fused (no all-reduce follows)
+  EPI_BIAS_GELU = 3,  // C = U = bf16(acc + bias), C2 = H = bf16(GeLU(U))
+  EPI_DGELU = 4,      // C = bf16(bf16(acc) * GeLU'(aux))      aux = saved U
+};
+
+struct EpiParams {
+  void* C = nullptr;
+  int64_t ldc = 0;
+  const __nv_bfloat16* bias = nullptr;
+  const __nv_bfloat16* aux = nullptr;
+  int64_t ldaux = 0;
+  void* C2 = nullptr;
+  int64_t ldc2 = 0;
+};
+
+struct GemmDesc {
+  alignas(64) CUtensorMap tmA;
+  alignas(64) CUtensorMap tmB;
+  int M = 0, N = 0, K = 0;
+  bool a_mn = false, b_mn = false;
+  int bn = 0;        // 128 or 256 (0 = choose)
+  int max_ctas = 0;  // persistent grid cap (0 = all SMs)
+  int epi = EPI_BF16;
+  EpiParams ep;
+};
+
+// C[M,N] = A[M,K] * B[N,K]^T.
+//   a_mn == false: A stored row-major [M,K] (pitch lda);  true: A stored [K,M]
+//   b_mn == false: B stored row-major [N,K] (pitch ldb);  true: B stored [K,N]
+const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, const void* B,
+                         int64_t ldb, bool b_mn, int M, int N, int K);
+cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t st);
+int gemm_tiles(const GemmDesc& d);
+int num_sms();
+
+}  // namespace atp

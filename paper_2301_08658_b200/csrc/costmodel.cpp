@@ -1,0 +1,247 @@
+// ATP cost model and mesh search, pure host C++ (§3.3-§3.5, §5.4).
+//
+//   Eq. 3  effective bandwidths B1', B2' from the hierarchical
+//                      communication matrix (reading G5/G6 in DESIGN.md)
+//   Eq. 4  Rabenseifner: B = d / (2(d-1)) * B'
+//   Eq. 2  T = 2Lbs (3h/(d1 B2) + h/(d2 B1) + 4h/(d1 B2) + h/(d2 B1))
+//   search argmin over all (d1, d2), d1*d2 = N; ties -> larger d1
+//
+// Every double is evaluated in the canonical order listed in DESIGN.md
+// ("Canonical evaluation order") so results are bit-identical to the oracle.
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/atp.h"
+
+namespace atp {
+void set_error(const std::string& msg);
+
+namespace {
+
+struct Spans {
+  int k1[ATP_MAX_HCM_LAYERS];
+  int k2[ATP_MAX_HCM_LAYERS];
+};
+
+// Mesh dim 2 is innermost (rank = i1*d2 + i2): it takes whole inner layers,
+// then an even divisor of the next one.  Returns false on misalignment.
+bool spans(const atp_hcm& hcm, int d2, Spans& s) {
+  int rem = d2;
+  for (int j = 0; j < hcm.n_layers; ++j) s.k2[j] = 1;
+  for (int j = hcm.n_layers - 1; j >= 0 && rem > 1; --j) {
+    const int R = hcm.ranks[j];
+    if (rem >= R) {
+      if (rem % R) return false;
+      s.k2[j] = R;
+      rem /= R;
+    } else {
+      if (R % rem) return false;
+      s.k2[j] = rem;
+      rem = 1;
+    }
+  }
+  if (rem != 1) return false;
+  for (int j = 0; j < hcm.n_layers; ++j) s.k1[j] = hcm.ranks[j] / s.k2[j];
+  return true;
+}
+
+// B'_j = min(GroupBW_j, (k_j - 1) * P2P_j) / share_j, B' = min over spanned layers.
+// Returns 0.0 for NoComm (dimension of size 1).
+bool eq3(const atp_hcm& hcm, int d1, int d2, double& b1p, double& b2p) {
+  Spans s;
+  if (!spans(hcm, d2, s)) return false;
+  bool have1 = false, have2 = false;
+  b1p = 0.0;
+  b2p = 0.0;
+  for (int j = 0; j < hcm.n_layers; ++j) {
+    long long devs = 1;  // devices inside one layer-j rank
+    for (int jj = j + 1; jj < hcm.n_layers; ++jj) devs *= hcm.ranks[jj];
+    if (s.k1[j] > 1) {
+      const double cap = static_cast<double>(s.k1[j] - 1) * hcm.p2p_gbps[j];
+      const double g = hcm.group_gbps[j];
+      const double m = cap < g ? cap : g;
+      const long long share = std::min<long long>(d2, devs);
+      const double v = m / static_cast<double>(share);
+      if (!have1 || v < b1p) b1p = v;
+      have1 = true;
+    }
+    if (s.k2[j] > 1) {
+      const double cap = static_cast<double>(s.k2[j] - 1) * hcm.p2p_gbps[j];
+      const double g = hcm.group_gbps[j];
+      const double v = (cap < g ? cap : g) / 1.0;
+      if (!have2 || v < b2p) b2p = v;
+      have2 = true;
+    }
+  }
+  if (d1 == 1) b1p = 0.0;
+  if (d2 == 1) b2p = 0.0;
+  return true;
+}
+
+double eq4(double bp, int d) {
+  if (d == 1 || bp <= 0.0) return 0.0;
+  return (static_cast<double>(d) * bp) / (2.0 * static_cast<double>(d - 1));
+}
+
+void eq2(const atp_model& m, int d1, int d2, double b1, double b2, atp_cost& c) {
+  const double h = static_cast<double>(m.h);
+  const double t1 = b2 > 0.0 ? (3.0 * h) / (static_cast<double>(d1) * (b2 * 1e9)) : 0.0;
+  const double t2 = b1 > 0.0 ? h / (static_cast<double>(d2) * (b1 * 1e9)) : 0.0;
+  const double t3 = b2 > 0.0 ? (4.0 * h) / (static_cast<double>(d1) * (b2 * 1e9)) : 0.0;
+  const double t4 = b1 > 0.0 ? h / (static_cast<double>(d2) * (b1 * 1e9)) : 0.0;
+  const double scale = 2.0 * static_cast<double>(m.L) * static_cast<double>(m.b) * static_cast<double>(m.s) *
+                       static_cast<double>(m.bytes_per_elem);
+  c.t_f[0] = scale * t1;
+  c.t_f[1] = scale * t2;
+  c.t_f[2] = scale * t3;
+  c.t_f[3] = scale * t4;
+  c.t_comm = scale * (((t1 + t2) + t3) + t4);
+}
+
+bool valid_hcm(const atp_hcm* hcm, long long* n) {
+  if (hcm == nullptr || hcm->n_layers < 1 || hcm->n_layers > ATP_MAX_HCM_LAYERS) return false;
+  long long p = 1;
+  for (int j = 0; j < hcm->n_layers; ++j) {
+    if (hcm->ranks[j] < 1 || !(hcm->p2p_gbps[j] > 0.0) || !(hcm->group_gbps[j] > 0.0)) return false;
+    p *= hcm->ranks[j];
+  }
+  *n = p;
+  return true;
+}
+
+const char* model_reject(const atp_model& m, int d1, int d2) {
+  if (m.h % d2) return "h % d2";
+  if (m.h % d1) return "h % d1";
+  if (m.heads % d1) return "heads % d1";
+  if (m.h % m.heads) return "h % heads";
+  return nullptr;
+}
+
+}  // namespace
+}  // namespace atp
+
+extern "C" {
+
+atp_status atp_effective_bandwidth(const atp_hcm* hcm, int d1, int d2, double* b1p, double* b2p) {
+  long long n = 0;
+  if (!atp::valid_hcm(hcm, &n) || d1 < 1 || d2 < 1 || b1p == nullptr || b2p == nullptr) {
+    atp::set_error("atp_effective_bandwidth: invalid HCM or arguments");
+    return ATP_ERR_INVALID;
+  }
+  if (static_cast<long long>(d1) * d2 != n) {
+    atp::set_error("atp_effective_bandwidth: d1*d2 != HCM device count");
+    return ATP_ERR_INVALID;
+  }
+  if (!atp::eq3(*hcm, d1, d2, *b1p, *b2p)) {
+    atp::set_error("atp_effective_bandwidth: mesh dim 2 does not align with the HCM layers");
+    return ATP_ERR_SHAPE;
+  }
+  return ATP_OK;
+}
+
+atp_status atp_search(const atp_hcm* hcm, const atp_model* model, int n_devices, const atp_calib* calib,
+                      atp_plan* out) {
+  long long n = 0;
+  if (!atp::valid_hcm(hcm, &n) || model == nullptr || out == nullptr) {
+    atp::set_error("atp_search: invalid HCM (layers 1..8, ranks >= 1, bandwidths > 0) or NULL argument");
+    return ATP_ERR_INVALID;
+  }
+  if (n != n_devices) {
+    atp::set_error("atp_search: product of HCM ranks != n_devices");
+    return ATP_ERR_INVALID;
+  }
+  if (model->L < 1 || model->b < 1 || model->s < 1 || model->h < 1 || model->heads < 1 || model->bytes_per_elem < 1) {
+    atp::set_error("atp_search: model fields must be positive");
+    return ATP_ERR_INVALID;
+  }
+  *out = atp_plan{};
+  std::vector<atp_cost> reps;
+  for (int d1 = n_devices; d1 >= 1; --d1) {
+    if (n_devices % d1) continue;
+    const int d2 = n_devices / d1;
+    if (atp::model_reject(*model, d1, d2)) {
+      if (out->n_rejected < ATP_MAX_PLAN) {
+        out->rejected_d1[out->n_rejected] = d1;
+        out->rejected_d2[out->n_rejected] = d2;
+        ++out->n_rejected;
+      }
+      continue;
+    }
+    atp_cost c{};
+    c.d1 = d1;
+    c.d2 = d2;
+    int cal = -1;
+    if (calib != nullptr)
+      for (int i = 0; i < calib->n && i < ATP_MAX_PLAN; ++i)
+        if (calib->d1[i] == d1 && calib->d2[i] == d2) cal = i;
+    if (cal >= 0) {
+      if ((d1 > 1 && !(calib->b1[cal] > 0.0)) || (d2 > 1 && !(calib->b2[cal] > 0.0))) {
+        atp::set_error("atp_search: calibration entry lacks a bandwidth for a dimension of size > 1");
+        return ATP_ERR_INVALID;
+      }
+      c.b1 = d1 > 1 ? calib->b1[cal] : 0.0;
+      c.b2 = d2 > 1 ? calib->b2[cal] : 0.0;
+      c.calibrated = 1;
+    } else {
+      if (!atp::eq3(*hcm, d1, d2, c.b1_prime, c.b2_prime)) {
+        if (out->n_rejected < ATP_MAX_PLAN) {
+          out->rejected_d1[out->n_rejected] = d1;
+          out->rejected_d2[out->n_rejected] = d2;
+          ++out->n_rejected;
+        }
+        continue;
+      }
+      c.b1 = atp::eq4(c.b1_prime, d1);
+      c.b2 = atp::eq4(c.b2_prime, d2);
+    }
+    atp::eq2(*model, d1, d2, c.b1, c.b2, c);
+    reps.push_back(c);
+  }
+  if (reps.empty()) {
+    atp::set_error("atp_search: no admissible mesh");
+    return ATP_ERR_EMPTY;
+  }
+  std::stable_sort(reps.begin(), reps.end(), [](const atp_cost& a, const atp_cost& b) { return a.t_comm < b.t_comm; });
+  out->n_ranked = static_cast<int>(std::min<size_t>(reps.size(), ATP_MAX_PLAN));
+  for (int i = 0; i < out->n_ranked; ++i) out->ranked[i] = reps[i];
+  out->chosen = 0;
+  return ATP_OK;
+}
+
+atp_status atp_comm_volume(int d1, int d2, int64_t T, int64_t h, int64_t F, int chunks, atp_call* calls, int cap,
+                           int* n_calls, int64_t* dim1_elems, int64_t* dim2_elems) {
+  if (d1 < 1 || d2 < 1 || T < 1 || h < 1 || F < 1 || chunks < 1 || n_calls == nullptr) {
+    atp::set_error("atp_comm_volume: invalid arguments");
+    return ATP_ERR_INVALID;
+  }
+  if (T % chunks || h % d1 || h % d2 || F % d1) {
+    atp::set_error("atp_comm_volume: T % chunks, h % d1, h % d2 and F % d1 must be 0");
+    return ATP_ERR_SHAPE;
+  }
+  const int64_t M = T / chunks;
+  // (phase, block, dim, width): the schedule order of the layer (reading G4)
+  const struct {
+    int phase, block, dim;
+    int64_t width;
+  } seq[8] = {{0, 0, 2, 3 * h / d1}, {0, 1, 1, h / d2}, {0, 2, 2, F / d1}, {0, 3, 1, h / d2},
+              {1, 3, 2, F / d1},     {1, 2, 1, h / d2}, {1, 1, 2, h / d1}, {1, 0, 1, h / d2}};
+  int cnt = 0;
+  int64_t e1 = 0, e2 = 0;
+  for (const auto& st : seq) {
+    const int p = st.dim == 1 ? d1 : d2;
+    if (p == 1) continue;
+    for (int k = 0; k < chunks; ++k) {
+      if (calls != nullptr && cnt < cap) calls[cnt] = atp_call{st.phase, st.block, st.dim, p, M * st.width};
+      ++cnt;
+      (st.dim == 1 ? e1 : e2) += M * st.width;
+    }
+  }
+  *n_calls = cnt;
+  if (dim1_elems) *dim1_elems = e1;
+  if (dim2_elems) *dim2_elems = e2;
+  return ATP_OK;
+}
+
+}  // extern "C"

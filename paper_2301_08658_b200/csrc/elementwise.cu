@@ -1,0 +1,212 @@
+// HBM-bound elementwise steps of the ATP block that cannot live in a GEMM
+// epilogue because an all-reduce sits between the GEMM and them (the GEMM
+// output is a Partial(SUM); GeLU and the residual are applied to the SUM):
+//   gelu_rows     H = GeLU(U)                      F10 (exact erf)
+//   dgelu_rows    dU = dH * GeLU'(U)   (in place)  B2
+//   add_rows      out = a + out        (in place)  residuals F7/F12/B3/B6
+//   core_fwd      ctx = Q + K + V per head         F5 (stand-in core, G20)
+//   core_bwd      dQ = dK = dV = dctx              B5
+//   colsum        db[n] = sum_t dY[t, n]  (fp32, deterministic, no workspace)
+//   group_sum     virtual-mesh all-reduce: sum of p member buffers, in
+//                 ascending coordinate order, written back to every member
+// All kernels move 16 B per thread per access (8 bf16) and use grid-stride
+// loops with a grid sized to a multiple of the SM count.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "atp_internal.h"
+#include "elementwise.h"
+
+namespace atp {
+
+namespace {
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
+         x * 0.39894228040143268f * __expf(-0.5f * x * x);
+}
+
+struct V8 {
+  float f[8];
+};
+__device__ __forceinline__ V8 ld8(const __nv_bfloat16* p) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  V8 r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    r.f[2 * i] = f.x;
+    r.f[2 * i + 1] = f.y;
+  }
+  return r;
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const V8& v) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v.f[2 * i], v.f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// Elementwise over a dense [rows, cols] matrix (cols % 8 == 0), n8 = rows*cols/8.
+__global__ void gelu_kernel(const __nv_bfloat16* __restrict__ u, __nv_bfloat16* __restrict__ h,
+                            int64_t n8) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    V8 v = ld8(u + 8 * i);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v.f[j] = gelu_f(v.f[j]);
+    st8(h + 8 * i, v);
+  }
+}
+
+__global__ void dgelu_kernel(__nv_bfloat16* __restrict__ dh, const __nv_bfloat16* __restrict__ u,
+                             int64_t n8) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    V8 g = ld8(dh + 8 * i);
+    V8 x = ld8(u + 8 * i);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g.f[j] *= gelu_grad_f(x.f[j]);
+    st8(dh + 8 * i, g);
+  }
+}
+
+__global__ void add_kernel(const __nv_bfloat16* __restrict__ a, __nv_bfloat16* __restrict__ out,
+                           int64_t n8) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    V8 x = ld8(a + 8 * i);
+    V8 y = ld8(out + 8 * i);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) y.f[j] += x.f[j];
+    st8(out + 8 * i, y);
+  }
+}
+
+// ctx[t, hd*d + j] = qkv[t, hd*3d + j] + qkv[t, hd*3d + d + j] + qkv[t, hd*3d + 2d + j]
+// One thread per 8 ctx columns; d % 8 == 0.
+__global__ void core_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ ctx,
+                                int64_t rows, int heads, int d) {
+  const int w8 = heads * d / 8;
+  const int64_t n = rows * w8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / w8;
+    const int c8 = static_cast<int>(i % w8) * 8;
+    const int hd = c8 / d, j = c8 % d;
+    const __nv_bfloat16* src = qkv + t * (int64_t)(3 * heads * d) + hd * 3 * d + j;
+    V8 q = ld8(src), k = ld8(src + d), v = ld8(src + 2 * d);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) q.f[e] = (q.f[e] + k.f[e]) + v.f[e];
+    st8(ctx + t * (int64_t)(heads * d) + c8, q);
+  }
+}
+
+__global__ void core_bwd_kernel(const __nv_bfloat16* __restrict__ dctx, __nv_bfloat16* __restrict__ dqkv,
+                                int64_t rows, int heads, int d) {
+  const int w8 = heads * d / 8;
+  const int64_t n = rows * w8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / w8;
+    const int c8 = static_cast<int>(i % w8) * 8;
+    const int hd = c8 / d, j = c8 % d;
+    uint4 v = *reinterpret_cast<const uint4*>(dctx + t * (int64_t)(heads * d) + c8);
+    __nv_bfloat16* dst = dqkv + t * (int64_t)(3 * heads * d) + hd * 3 * d + j;
+    *reinterpret_cast<uint4*>(dst) = v;
+    *reinterpret_cast<uint4*>(dst + d) = v;
+    *reinterpret_cast<uint4*>(dst + 2 * d) = v;
+  }
+}
+
+// db[c] = sum_t x[t, c]: one block per 64-column strip; warp w sums rows
+// w, w+W, ... in order (2 columns per lane), then the W warp partials are added
+// in warp order -> deterministic, no workspace.
+constexpr int kColsumWarps = 16;
+__global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                  float* __restrict__ out, int64_t rows, int cols) {
+  __shared__ float2 part[kColsumWarps][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c2 = blockIdx.x * 64 + 2 * lane;
+  float a = 0.f, b = 0.f;
+  if (c2 < cols) {
+    for (int64_t r = warp; r < rows; r += kColsumWarps) {
+      float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + r * cols + c2));
+      a += f.x;
+      b += f.y;
+    }
+  }
+  part[warp][lane] = make_float2(a, b);
+  __syncthreads();
+  if (warp == 0 && c2 < cols) {
+    float2 s = part[0][lane];
+    for (int w = 1; w < kColsumWarps; ++w) {
+      s.x += part[w][lane].x;
+      s.y += part[w][lane].y;
+    }
+    out[c2] = s.x;
+    out[c2 + 1] = s.y;
+  }
+}
+
+__global__ void group_sum_kernel(GroupSumArgs g, int64_t n8) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    V8 acc = ld8(g.buf[0] + 8 * i);
+    for (int r = 1; r < g.p; ++r) {
+      V8 v = ld8(g.buf[r] + 8 * i);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc.f[j] += v.f[j];
+    }
+    for (int r = 0; r < g.p; ++r) st8(g.buf[r] + 8 * i, acc);
+  }
+}
+
+int ew_grid(int64_t n) {
+  const int64_t per = 256;
+  int64_t blocks = (n + per - 1) / per;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  return blocks < 1 ? 1 : static_cast<int>(blocks);
+}
+
+}  // namespace
+
+cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
+  using bf = __nv_bfloat16;
+  const int64_t n = e.rows * e.cols;
+  switch (e.kind) {
+    case EW_GELU:
+      gelu_kernel<<<ew_grid(n / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, n / 8);
+      break;
+    case EW_DGELU:
+      dgelu_kernel<<<ew_grid(n / 8), 256, 0, st>>>((bf*)e.out, (const bf*)e.a, n / 8);
+      break;
+    case EW_ADD:
+      add_kernel<<<ew_grid(n / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, n / 8);
+      break;
+    case EW_CORE_FWD:
+      core_fwd_kernel<<<ew_grid(e.rows * e.cols / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, e.rows,
+                                                                    e.heads, static_cast<int>(e.cols / e.heads));
+      break;
+    case EW_CORE_BWD:
+      core_bwd_kernel<<<ew_grid(e.rows * e.cols / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, e.rows,
+                                                                    e.heads, static_cast<int>(e.cols / e.heads));
+      break;
+    case EW_COLSUM:
+      colsum_kernel<<<static_cast<int>((e.cols + 63) / 64), kColsumWarps * 32, 0, st>>>(
+          (const bf*)e.a, (float*)e.out, e.rows, static_cast<int>(e.cols));
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t group_sum_launch(const GroupSumArgs& g, int64_t n, cudaStream_t st) {
+  group_sum_kernel<<<ew_grid(n / 8), 256, 0, st>>>(g, n / 8);
+  return cudaGetLastError();
+}
+
+}  // namespace atp

@@ -1,0 +1,406 @@
+// Local shard GEMM on the 5th-generation tensor cores (sm_100a).
+//
+// C[M,N] = A[M,K] * B[N,K]^T  (bf16 operands, fp32 accumulation in TMEM)
+//
+// This is the contraction of every ATP step F3/F6/F8/F11 and of the backward
+// products dX = dY W^T and dW = X^T dY (§4.2).  The three
+// operand arrangements of the layer map onto the UMMA "major" bits, so no
+// operand is ever transposed in HBM:
+//     forward   Y  = X  W      A = X  [M,K] K-major,  B = W  [K,N] stored -> MN-major
+//     dX        dX = dY W^T    A = dY [M,N] K-major,  B = W  [K,N] stored -> K-major
+//     dW        dW = X^T dY    A = X  [T,K] stored -> MN-major, B = dY [T,N] -> MN-major
+//
+// Design (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: 128B-swizzled boxes into a STAGES-deep smem ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 2..5  epilogue: tcgen05.ld -> registers -> fused epilogue -> global
+//   TMEM holds two BN-column fp32 accumulators so the epilogue of tile i
+//   overlaps the main loop of tile i+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "atp_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace atp {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int kThreads = 192;
+constexpr uint32_t kBoxBytesMN = 64 * 64 * 2;  // one MN-major box: 64 (mn) x 64 (k)
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
+         x * 0.39894228040143268f * __expf(-0.5f * x * x);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+template <int BN, int STAGES>
+struct SmemLayout {
+  static constexpr uint32_t kABytes = BM * BK * 2;
+  static constexpr uint32_t kBBytes = BN * BK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
+  // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem slot
+  static constexpr uint32_t kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;
+};
+
+template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      int M, int N, int K, EpiParams ep) {
+  using L = SmemLayout<BN, STAGES>;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t bar0 = base + L::kBarOffset;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::kBarOffset + (2 * STAGES + 4) * 8);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x % 32;
+
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_k = (K + BK - 1) / BK;
+  const int num_tiles = num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(full_bar(s), 1);
+      ptx::mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(tfull_bar(a), 1);
+      ptx::mbar_init(tempty_bar(a), 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), TMEM_COLS);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % num_m) * BM;
+        const int n0 = (tile / num_m) * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sA = base + stage * L::kStageBytes;
+          const uint32_t sB = sA + L::kABytes;
+          const uint32_t fb = full_bar(stage);
+          ptx::mbar_arrive_expect_tx(fb, L::kStageBytes);
+          const int k0 = kb * BK;
+          if constexpr (!A_MN) {
+            ptx::tma_load_2d(sA, &tmA, fb, k0, m0);
+          } else {
+            ptx::tma_load_2d(sA, &tmA, fb, m0, k0);
+            ptx::tma_load_2d(sA + kBoxBytesMN, &tmA, fb, m0 + 64, k0);
+          }
+          if constexpr (!B_MN) {
+            ptx::tma_load_2d(sB, &tmB, fb, k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sB + j * kBoxBytesMN, &tmB, fb, n0 + 64 * j, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          ptx::mbar_wait(full_bar(stage), phase);
+          ptx::tc_fence_after();
+          const uint32_t sA = base + stage * L::kStageBytes;
+          const uint32_t sB = sA + L::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(sA + kk * 2048, kBoxBytesMN, 1024)
+                                     : ptx::smem_desc_sw128(sA + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(sB + kk * 2048, kBoxBytesMN, 1024)
+                                     : ptx::smem_desc_sw128(sB + kk * 32, 16, 1024);
+            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(empty_bar(stage));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(tfull_bar(acc));
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m0 = (tile % num_m) * BM;
+      const int n0 = (tile / num_m) * BN;
+      ptx::mbar_wait(tfull_bar(acc), acc_phase);
+      ptx::tc_fence_after();
+      const int row = m0 + 32 * q + static_cast<int>(lane);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN + 32 * c, v);
+        ptx::tmem_wait_ld();
+        const int col0 = n0 + 32 * c;
+        if (row < M && col0 < N) {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          if (ep.bias != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) f[j] += __bfloat162float(ep.bias[col0 + j]);
+          }
+          const bool full = (col0 + 32 <= N);
+          if constexpr (EPI == EPI_F32) {
+            float* dst = static_cast<float*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              if (full || col0 + 4 * g + 4 <= N)
+                reinterpret_cast<float4*>(dst)[g] = make_float4(f[4 * g], f[4 * g + 1], f[4 * g + 2], f[4 * g + 3]);
+          } else {
+            if constexpr (EPI == EPI_RESID) {
+              const __nv_bfloat16* r = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                if (full || col0 + 8 * g + 8 <= N) {
+                  uint4 rv = reinterpret_cast<const uint4*>(r)[g];
+                  const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) f[8 * g + j] += __bfloat162float(rb[j]);
+                }
+              }
+            }
+            if constexpr (EPI == EPI_BIAS_GELU) {
+              // U = acc + bias (stored, rounded once); H = GeLU(U) from the rounded U
+              __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(ep.C2) + static_cast<int64_t>(row) * ep.ldc2 + col0;
+              uint32_t hp[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float u0 = __bfloat162float(__float2bfloat16_rn(f[2 * j]));
+                const float u1 = __bfloat162float(__float2bfloat16_rn(f[2 * j + 1]));
+                hp[j] = pack_bf16(gelu_f(u0), gelu_f(u1));
+              }
+#pragma unroll
+              for (int g = 0; g < 4; ++g)
+                if (full || col0 + 8 * g + 8 <= N)
+                  reinterpret_cast<uint4*>(dh)[g] = make_uint4(hp[4 * g], hp[4 * g + 1], hp[4 * g + 2], hp[4 * g + 3]);
+            }
+            if constexpr (EPI == EPI_DGELU) {
+              // dU = dH * GeLU'(U); dH is the bf16-rounded product (as after an all-reduce)
+              const __nv_bfloat16* u = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                if (full || col0 + 8 * g + 8 <= N) {
+                  uint4 uv = reinterpret_cast<const uint4*>(u)[g];
+                  const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uv);
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    const float dh = __bfloat162float(__float2bfloat16_rn(f[8 * g + j]));
+                    f[8 * g + j] = dh * gelu_grad_f(__bfloat162float(ub[j]));
+                  }
+                }
+              }
+            }
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
+            uint32_t p[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) p[j] = pack_bf16(f[2 * j], f[2 * j + 1]);
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              if (full || col0 + 8 * g + 8 <= N)
+                reinterpret_cast<uint4*>(dst)[g] = make_uint4(p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, cols] matrix with row pitch ld
+// (elements); box = [box_rows, box_cols], 128B swizzle, OOB -> zero.
+bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+               int box_cols) {
+  if (!get_encode()) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
+cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
+  using L = SmemLayout<BN, STAGES>;
+  auto kern = gemm_sm100_kernel<BN, STAGES, EPI, A_MN, B_MN>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<grid, kThreads, L::kBytes, st>>>(d.tmA, d.tmB, d.M, d.N, d.K, d.ep);
+  return cudaGetLastError();
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN>
+cudaError_t launch_epi(const GemmDesc& d, int grid, cudaStream_t st) {
+  switch (d.epi) {
+    case EPI_BF16: return launch_t<BN, STAGES, EPI_BF16, A_MN, B_MN>(d, grid, st);
+    case EPI_F32: return launch_t<BN, STAGES, EPI_F32, A_MN, B_MN>(d, grid, st);
+    case EPI_RESID: return launch_t<BN, STAGES, EPI_RESID, A_MN, B_MN>(d, grid, st);
+    case EPI_BIAS_GELU: return launch_t<BN, STAGES, EPI_BIAS_GELU, A_MN, B_MN>(d, grid, st);
+    case EPI_DGELU: return launch_t<BN, STAGES, EPI_DGELU, A_MN, B_MN>(d, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int BN, int STAGES>
+cudaError_t launch_bn(const GemmDesc& d, int grid, cudaStream_t st) {
+  if (!d.a_mn && d.b_mn) return launch_epi<BN, STAGES, false, true>(d, grid, st);
+  if (!d.a_mn && !d.b_mn) return launch_epi<BN, STAGES, false, false>(d, grid, st);
+  if (d.a_mn && d.b_mn) return launch_epi<BN, STAGES, true, true>(d, grid, st);
+  return cudaErrorInvalidValue;  // (MN, K) is not used by the layer
+}
+
+int g_num_sms = 0;
+
+}  // namespace
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+int gemm_tiles(const GemmDesc& d) {
+  return ((d.M + BM - 1) / BM) * ((d.N + d.bn - 1) / d.bn);
+}
+
+// Validate and build the TMA descriptors of one GEMM.  Returns a message on error.
+const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
+                         bool b_mn, int M, int N, int K) {
+  if (M <= 0 || N <= 0 || K <= 0) return "gemm: M, N, K must be positive";
+  if (a_mn && !b_mn) return "gemm: operand arrangement (MN, K) unsupported";
+  if ((N % 8) != 0 || (K % 8) != 0 || (a_mn && (M % 8) != 0)) return "gemm: N, K (and M for MN-major A) must be multiples of 8";
+  if ((lda % 8) != 0 || (ldb % 8) != 0) return "gemm: leading dimensions must be multiples of 8 elements";
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return "gemm: operands must be 16-byte aligned";
+  d.M = M;
+  d.N = N;
+  d.K = K;
+  d.a_mn = a_mn;
+  d.b_mn = b_mn;
+  if (d.bn != 128 && d.bn != 256) d.bn = (N % 256 == 0 || N > 1024) ? 256 : 128;
+  bool ok;
+  if (!a_mn)
+    ok = make_tmap(&d.tmA, A, M, K, lda, BM, BK);
+  else
+    ok = make_tmap(&d.tmA, A, K, M, lda, BK, 64);
+  if (!ok) return "gemm: cuTensorMapEncodeTiled failed for A";
+  if (!b_mn)
+    ok = make_tmap(&d.tmB, B, N, K, ldb, d.bn, BK);
+  else
+    ok = make_tmap(&d.tmB, B, K, N, ldb, BK, 64);
+  if (!ok) return "gemm: cuTensorMapEncodeTiled failed for B";
+  return nullptr;
+}
+
+cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t st) {
+  int sms = d.max_ctas > 0 ? d.max_ctas : num_sms();
+  int tiles = gemm_tiles(d);
+  int grid = tiles < sms ? tiles : sms;
+  if (d.bn == 256) return launch_bn<256, 4>(d, grid, st);
+  return launch_bn<128, 6>(d, grid, st);
+}
+
+}  // namespace atp

@@ -1,0 +1,356 @@
+// Mesh lifetime and the two schedule executors.
+//
+// Distributed mesh (one process per GPU): the schedule's compute ops go
+// on the caller's stream, its all-reduces on the mesh's communication stream
+// as ncclAllReduce on the dim-1 / dim-2 communicator (grouped all-reduce,
+// §3.2; communicators from ncclCommSplit, P:161 / P:270).  Cross-stream
+// order is carried by CUDA events only; the host never synchronises.
+//
+// Virtual mesh (all d1*d2 ranks in one process on one GPU): the SAME per-rank
+// schedules run in lockstep, op index by op index, each rank on its own
+// compute and communication streams; a grouped all-reduce becomes one
+// group_sum kernel per group on the group leader's communication stream,
+// gated by events from every member (sum in ascending mesh coordinate, as the
+// oracle does).  This lets a single B200 check the whole sharded pipeline —
+// chunking, events, epilogues — for every mesh shape.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "runtime.h"
+
+namespace atp {
+
+namespace {
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void count_launch(uint64_t n) { g_launches += n; }
+uint64_t launch_count() { return g_launches.load(); }
+
+// Algorithmic cost of one op (class 0 = GEMM, 1 = elementwise, 2 = all-reduce).
+void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes) {
+  *flops = 0;
+  *bytes = 0;
+  if (op.kind == OP_GEMM) {
+    const double M = op.g.M, N = op.g.N, K = op.g.K;
+    *cls = 0;
+    *flops = 2.0 * M * N * K;
+    double out = op.g.epi == EPI_F32 ? 4.0 : 2.0;
+    double extra = (op.g.epi == EPI_RESID || op.g.epi == EPI_DGELU || op.g.epi == EPI_BIAS_GELU) ? 2.0 : 0.0;
+    *bytes = 2.0 * (M * K + N * K) + M * N * (out + extra);
+  } else if (op.kind == OP_EW) {
+    *cls = 1;
+    const double n = static_cast<double>(op.e.rows) * op.e.cols;
+    switch (op.e.kind) {
+      case EW_GELU: *bytes = 4.0 * n; break;
+      case EW_DGELU: case EW_ADD: *bytes = 6.0 * n; break;
+      case EW_CORE_FWD: case EW_CORE_BWD: *bytes = 8.0 * n; break;
+      case EW_COLSUM: *bytes = 2.0 * n + 4.0 * op.e.cols; break;
+    }
+  } else {
+    *cls = 2;
+    *bytes = p > 1 ? 2.0 * (p - 1) / p * op.ar_count * 2.0 : 0.0;
+  }
+}
+
+// Profiling: bracket an enqueue with timing events on its stream.
+static ProfRec* prof_begin(atp_mesh* m, const Op& op, cudaStream_t st) {
+  if (!m->profiling) return nullptr;
+  if (m->prof_used == m->prof.size()) {
+    ProfRec r;
+    if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return nullptr;
+    m->prof.push_back(r);
+  }
+  ProfRec* r = &m->prof[m->prof_used++];
+  const int p = op.kind == OP_AR ? (op.ar_dim == 1 ? m->d1 : m->d2) : 1;
+  op_cost(op, p, &r->cls, &r->flops, &r->bytes);
+  cudaEventRecord(r->a, st);
+  return r;
+}
+static void prof_end(ProfRec* r, cudaStream_t st) {
+  if (r) cudaEventRecord(r->b, st);
+}
+
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+
+RankView rank_view(const atp_mesh* m, int r) {
+  RankView v;
+  v.d1 = m->d1;
+  v.d2 = m->d2;
+  if (m->is_virtual) {
+    v.i1 = r / m->d2;
+    v.i2 = r % m->d2;
+  } else {
+    v.i1 = m->i1;
+    v.i2 = m->i2;
+  }
+  v.gemm_ctas = m->gemm_ctas;
+  return v;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return 3;  // ATP_ERR_CUDA
+}
+
+static int ensure_events(RankState& s, int n) {
+  while (static_cast<int>(s.ev.size()) < n) {
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaEventCreate");
+    s.ev.push_back(e);
+  }
+  return 0;
+}
+
+static cudaError_t launch_local(const Op& op, cudaStream_t st) {
+  if (op.kind == OP_GEMM) {
+    count_launch(1);
+    return gemm_launch(op.g, st);
+  }
+  count_launch(1);
+  return ew_launch(op.e, st);
+}
+
+static cudaError_t wait_all(const Op& op, RankState& s, cudaStream_t st) {
+  for (int w = 0; w < op.n_waits; ++w) {
+    cudaError_t e = cudaStreamWaitEvent(st, s.ev[op.waits[w]], 0);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
+  const int n = static_cast<int>(sch.size());
+  if (n != static_cast<int>(m->rs.size())) {
+    set_error("internal: schedule count != rank count");
+    return 1;
+  }
+  for (int r = 0; r < n; ++r) {
+    if (sch[r].ops.size() != sch[0].ops.size()) {
+      set_error("internal: rank schedules differ in length");
+      return 1;
+    }
+    int rc = ensure_events(m->rs[r], sch[r].n_events);
+    if (rc) return rc;
+  }
+  cudaError_t e = cudaEventRecord(m->ev_start, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  for (int r = 0; r < n; ++r) {
+    cudaStreamWaitEvent(m->rs[r].comm, m->ev_start, 0);
+    if (m->is_virtual) cudaStreamWaitEvent(m->rs[r].compute, m->ev_start, 0);
+  }
+
+  if (!m->is_virtual) {
+    RankState& s = m->rs[0];
+    for (const Op& op : sch[0].ops) {
+      cudaStream_t st = op.stream ? s.comm : stream;
+      if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+      ProfRec* pr = prof_begin(m, op, st);
+      if (op.kind == OP_AR) {
+        if (m->comm_enabled) {
+          ncclComm_t comm = op.ar_dim == 1 ? m->dim1 : m->dim2;
+          ncclResult_t nr = ncclAllReduce(op.ar_ptr, op.ar_ptr, static_cast<size_t>(op.ar_count), ncclBfloat16,
+                                          ncclSum, comm, st);
+          if (nr != ncclSuccess) {
+            set_error(std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+            return 4;
+          }
+        }
+      } else if ((e = launch_local(op, st)) != cudaSuccess) {
+        return cuda_fail(e, op.kind == OP_GEMM ? "gemm launch" : "elementwise launch");
+      }
+      prof_end(pr, st);
+      if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+    }
+    cudaEventRecord(s.join, s.comm);
+    cudaStreamWaitEvent(stream, s.join, 0);
+    return 0;
+  }
+
+  // ---------------------------------------------------- virtual lockstep
+  const size_t n_ops = sch[0].ops.size();
+  for (size_t i = 0; i < n_ops; ++i) {
+    const OpKind kind = sch[0].ops[i].kind;
+    for (int r = 0; r < n; ++r) {
+      if (sch[r].ops[i].kind != kind) {
+        set_error("internal: rank schedules differ in structure");
+        return 1;
+      }
+    }
+    if (kind != OP_AR) {
+      for (int r = 0; r < n; ++r) {
+        const Op& op = sch[r].ops[i];
+        RankState& s = m->rs[r];
+        cudaStream_t st = op.stream ? s.comm : s.compute;
+        if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+        ProfRec* pr = prof_begin(m, op, st);
+        if ((e = launch_local(op, st)) != cudaSuccess)
+          return cuda_fail(e, op.kind == OP_GEMM ? "gemm launch" : "elementwise launch");
+        prof_end(pr, st);
+        if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+      }
+      continue;
+    }
+    const int dim = sch[0].ops[i].ar_dim;
+    for (int r = 0; r < n; ++r) {
+      if ((e = wait_all(sch[r].ops[i], m->rs[r], m->rs[r].comm)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamWaitEvent");
+    }
+    const int ngroups = dim == 1 ? m->d2 : m->d1;
+    const int p = dim == 1 ? m->d1 : m->d2;
+    if (p > kMaxGroup) {
+      set_error("virtual mesh: group larger than 16");
+      return 1;
+    }
+    for (int g = 0; g < ngroups; ++g) {
+      int members[kMaxGroup];
+      for (int j = 0; j < p; ++j) members[j] = dim == 1 ? (j * m->d2 + g) : (g * m->d2 + j);
+      const int leader = members[0];
+      GroupSumArgs ga;
+      ga.p = p;
+      for (int j = 0; j < p; ++j) {
+        ga.buf[j] = static_cast<__nv_bfloat16*>(sch[members[j]].ops[i].ar_ptr);
+        if (j > 0) {
+          cudaEventRecord(m->rs[members[j]].arrive, m->rs[members[j]].comm);
+          cudaStreamWaitEvent(m->rs[leader].comm, m->rs[members[j]].arrive, 0);
+        }
+      }
+      ProfRec* pr = prof_begin(m, sch[leader].ops[i], m->rs[leader].comm);
+      if (m->comm_enabled) {
+        if ((e = group_sum_launch(ga, sch[leader].ops[i].ar_count, m->rs[leader].comm)) != cudaSuccess)
+          return cuda_fail(e, "group_sum launch");
+        count_launch(1);
+      }
+      prof_end(pr, m->rs[leader].comm);
+      cudaEventRecord(m->rs[leader].done, m->rs[leader].comm);
+      for (int j = 1; j < p; ++j) cudaStreamWaitEvent(m->rs[members[j]].comm, m->rs[leader].done, 0);
+    }
+    for (int r = 0; r < n; ++r) {
+      const Op& op = sch[r].ops[i];
+      if (op.record >= 0) cudaEventRecord(m->rs[r].ev[op.record], m->rs[r].comm);
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    RankState& s = m->rs[r];
+    cudaEventRecord(s.join, s.comm);
+    cudaStreamWaitEvent(stream, s.join, 0);
+    cudaEventRecord(s.join, s.compute);
+    cudaStreamWaitEvent(stream, s.join, 0);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "virtual executor");
+  return 0;
+}
+
+// ---------------------------------------------------------------- mesh lifetime
+static int make_rank_state(RankState& s, bool with_compute) {
+  int lo, hi;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaError_t e = cudaStreamCreateWithPriority(&s.comm, cudaStreamNonBlocking, hi);
+  if (e == cudaSuccess && with_compute) e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.arrive, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e, "stream/event create");
+  return 0;
+}
+
+static void free_rank_state(RankState& s) {
+  for (cudaEvent_t ev : s.ev) cudaEventDestroy(ev);
+  s.ev.clear();
+  if (s.arrive) cudaEventDestroy(s.arrive);
+  if (s.done) cudaEventDestroy(s.done);
+  if (s.join) cudaEventDestroy(s.join);
+  if (s.comm) cudaStreamDestroy(s.comm);
+  if (s.compute) cudaStreamDestroy(s.compute);
+  s = RankState();
+}
+
+int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, bool is_virtual,
+                atp_mesh** out) {
+  if (out == nullptr) {
+    set_error("atp_mesh_init: out is NULL");
+    return 1;
+  }
+  *out = nullptr;
+  if (d1 < 1 || d2 < 1) {
+    set_error("atp_mesh_init: d1 and d2 must be >= 1");
+    return 1;
+  }
+  const int n = d1 * d2;
+  if (!is_virtual && (world_rank < 0 || world_rank >= n)) {
+    set_error("atp_mesh_init: world_rank out of range");
+    return 1;
+  }
+  if (is_virtual && (d1 > kMaxGroup || d2 > kMaxGroup)) {
+    set_error("atp_vmesh_init: mesh dimensions above 16 unsupported");
+    return 1;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  atp_mesh* m = new atp_mesh();
+  m->d1 = d1;
+  m->d2 = d2;
+  m->is_virtual = is_virtual;
+  m->device = device;
+  m->rank = is_virtual ? 0 : world_rank;
+  m->i1 = m->rank / d2;
+  m->i2 = m->rank % d2;
+  m->rs.resize(is_virtual ? n : 1);
+  for (auto& s : m->rs) {
+    int rc = make_rank_state(s, is_virtual);
+    if (rc) {
+      for (auto& t : m->rs) free_rank_state(t);
+      delete m;
+      return rc;
+    }
+  }
+  cudaEventCreateWithFlags(&m->ev_start, cudaEventDisableTiming);
+  if (!is_virtual) {
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&m->world, n, id, world_rank);
+    // dim-1 group: the d1 ranks sharing i2 (color i2, ordered by i1); dim-2: sharing i1.
+    if (r == ncclSuccess) r = ncclCommSplit(m->world, m->i2, m->i1, &m->dim1, nullptr);
+    if (r == ncclSuccess) r = ncclCommSplit(m->world, m->i1, m->i2, &m->dim2, nullptr);
+    if (r != ncclSuccess) {
+      set_error(std::string("NCCL mesh init: ") + ncclGetErrorString(r));
+      if (m->dim1) ncclCommDestroy(m->dim1);
+      if (m->world) ncclCommDestroy(m->world);
+      for (auto& t : m->rs) free_rank_state(t);
+      delete m;
+      return 4;
+    }
+  }
+  *out = m;
+  return 0;
+}
+
+int mesh_destroy(atp_mesh* m) {
+  if (m == nullptr) return 0;
+  cudaSetDevice(m->device);
+  for (auto& s : m->rs) {
+    if (s.comm) cudaStreamSynchronize(s.comm);
+    if (s.compute) cudaStreamSynchronize(s.compute);
+  }
+  if (m->dim2) ncclCommDestroy(m->dim2);
+  if (m->dim1) ncclCommDestroy(m->dim1);
+  if (m->world) ncclCommDestroy(m->world);
+  for (auto& s : m->rs) free_rank_state(s);
+  for (auto& r : m->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  if (m->ev_start) cudaEventDestroy(m->ev_start);
+  delete m;
+  return 0;
+}
+
+}  // namespace atp

@@ -1,0 +1,86 @@
+// Host runtime of libatp: mesh state, the op-list schedule and its executors.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "atp_internal.h"
+#include "elementwise.h"
+
+struct atp_mesh;
+
+namespace atp {
+
+void set_error(const std::string& msg);
+
+enum OpKind : int { OP_GEMM = 0, OP_EW = 1, OP_AR = 2 };
+
+// One enqueue on one of a rank's two streams.  `waits` are schedule-local
+// event ids the op's stream waits on first; `record` is recorded after it.
+struct Op {
+  OpKind kind = OP_GEMM;
+  int stream = 0;  // 0 = compute (caller's stream), 1 = communication
+  int waits[4] = {-1, -1, -1, -1};
+  int n_waits = 0;
+  int record = -1;
+  GemmDesc g;
+  EwDesc e;
+  int ar_dim = 0;  // mesh dimension of the grouped all-reduce (1 or 2)
+  void* ar_ptr = nullptr;
+  int64_t ar_count = 0;  // bf16 elements, in place
+};
+
+struct Sched {
+  std::vector<Op> ops;
+  int n_events = 0;
+};
+
+struct RankView {
+  int d1 = 1, d2 = 1, i1 = 0, i2 = 0;
+  int gemm_ctas = 0;
+};
+
+struct RankState {
+  cudaStream_t comm = nullptr;
+  cudaStream_t compute = nullptr;  // virtual mesh only (one per virtual rank)
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t arrive = nullptr, done = nullptr, join = nullptr;
+};
+
+}  // namespace atp
+
+namespace atp {
+struct ProfRec {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int cls = 0;
+  double flops = 0, bytes = 0;
+};
+}  // namespace atp
+
+struct atp_mesh {
+  int d1 = 1, d2 = 1;
+  bool comm_enabled = true;
+  bool profiling = false;
+  std::vector<atp::ProfRec> prof;  // event pool; the first prof_used are live
+  size_t prof_used = 0;
+  bool is_virtual = false;
+  int rank = 0, i1 = 0, i2 = 0;
+  int device = 0;
+  int gemm_ctas = 0;
+  ncclComm_t world = nullptr, dim1 = nullptr, dim2 = nullptr;
+  std::vector<atp::RankState> rs;  // 1 (distributed) or d1*d2 (virtual)
+  cudaEvent_t ev_start = nullptr;
+};
+
+namespace atp {
+
+RankView rank_view(const atp_mesh* m, int r);
+// Run one schedule per rank (size 1 for a distributed mesh) on `stream`.
+int execute(atp_mesh* m, std::vector<Sched>& per_rank, cudaStream_t stream);
+void count_launch(uint64_t n);
+uint64_t launch_count();
+void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes);
+
+}  // namespace atp

@@ -1,0 +1,29 @@
+#pragma once
+#include "../../include/atp.h"
+#include "runtime.h"
+
+namespace atp {
+
+using LinearFwd = atp_linear_fwd_args;
+using LinearBwd = atp_linear_bwd_args;
+
+// Which blocks of one layer to emit into a single chunk pipeline.
+struct LayerParts {
+  const atp_attn_fwd_args* attn_fwd = nullptr;
+  const atp_mlp_fwd_args* mlp_fwd = nullptr;
+  const atp_mlp_bwd_args* mlp_bwd = nullptr;
+  const atp_attn_bwd_args* attn_bwd = nullptr;
+};
+
+int build_linear_fwd(const RankView& rv, bool colfirst, const LinearFwd& a, int64_t M, int64_t K, int64_t N,
+                     int chunks, Sched& out);
+int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int64_t M, int64_t K, int64_t N,
+                     int chunks, Sched& out);
+int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
+                int chunks, Sched& out);
+
+const char* last_error();
+int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, bool is_virtual, atp_mesh** out);
+int mesh_destroy(atp_mesh* m);
+
+}  // namespace atp

@@ -1,0 +1,166 @@
+"""Sharded ATP layer on the GPU vs the oracle, element by element per rank.
+
+Virtual meshes run every rank of DeviceMesh(d1, d2) on one B200 with the same
+schedule (chunk pipeline, events, epilogues) the distributed mesh uses; the
+grouped all-reduce is a library kernel.  Every forward activation, the input
+gradient and every weight/bias gradient of every rank is compared with the
+oracle's shard: relative Frobenius <= 2e-2 (north_star, bf16).  Ranks of one
+all-reduce group must hold bit-identical replicas."""
+import numpy as np
+import pytest
+
+from gpu_util import BWD_MAP, FWD_MAP, oracle_layer, rel, to_np
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+MESHES = [(1, 1), (2, 1), (1, 2), (4, 1), (2, 2), (1, 4), (8, 1), (4, 2), (2, 4), (1, 8)]
+
+
+def run_gpu_layer(d1, d2, T, h, F, heads, chunks, seed, backward=True):
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    mesh = atp.Mesh.virtual(d1, d2, 0)
+    try:
+        bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(d1 * d2)]
+        for b in bufs:  # poison outputs so unwritten elements show up
+            for k in ("qkv", "ctx", "y1", "u", "h", "z", "dy1", "dx", "dwqkv", "dbqkv", "dwo", "dbo",
+                      "dw1", "db1", "dw2", "db2"):
+                b[k].fill_(float("nan"))
+        atp.atp_layer_fwd_bwd(mesh, bufs, T, h, F, heads, chunks, backward)
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    return bufs
+
+
+def compare(bufs, fw, bw, d1, d2, backward=True):
+    worst = {}
+    for r, b in enumerate(bufs):
+        for k, ok in FWD_MAP.items():
+            got = to_np(b[k])
+            assert np.isfinite(got).all(), (r, k)
+            e = rel(got, fw[ok][r])
+            worst[k] = max(worst.get(k, 0), e)
+            assert e <= TOL, (d1, d2, r, k, e)
+        if backward:
+            for k, ok in BWD_MAP.items():
+                got = to_np(b[k])
+                assert np.isfinite(got).all(), (r, k)
+                e = rel(got, bw[ok][r])
+                worst[k] = max(worst.get(k, 0), e)
+                assert e <= TOL, (d1, d2, r, k, e)
+    return worst
+
+
+def check_replicas(bufs, d1, d2):
+    import torch
+    from oracle import mesh as omesh
+
+    # QKV, U, H, dU-derived grads are replicated over dim 2; Y1, Z, dY1, dX over dim 1
+    for dim, keys in ((2, ("qkv", "ctx", "u", "h", "db1", "dbqkv")),
+                      (1, ("y1", "z", "dy1", "dx", "db2", "dbo"))):
+        for grp in omesh.groups(d1, d2, dim):
+            for k in keys:
+                for r in grp[1:]:
+                    assert torch.equal(bufs[r][k], bufs[grp[0]][k]), (dim, grp, k)
+
+
+@pytest.mark.parametrize("d1,d2", MESHES)
+@pytest.mark.parametrize("chunks", [1, 2, 4])
+def test_layer_every_mesh(d1, d2, chunks):
+    T, h, F, heads, seed = 256, 256, 1024, 8, 17
+    g, sh, fw, bw, log = oracle_layer(T, h, F, heads, d1, d2, chunks, seed)
+    bufs = run_gpu_layer(d1, d2, T, h, F, heads, chunks, seed)
+    compare(bufs, fw, bw, d1, d2)
+    check_replicas(bufs, d1, d2)
+
+
+def test_cfg1_mlp_2x2():
+    """BASELINE.json configs[0]: h=64, ffn=256, tokens=32 on a 2x2 mesh."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, seed, d1, d2 = 32, 64, 256, 2, 5, 2, 2
+    g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, d1, d2, 1, seed)
+    mesh = atp.Mesh.virtual(d1, d2)
+    bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(4)]
+    # the MLP alone, fed the oracle's Y1 shards
+    for r, b in enumerate(bufs):
+        b["y1"].copy_(torch.from_numpy(fw["y1"][r]).to(torch.bfloat16))
+    atp.atp_mlp_fwd(mesh, bufs, T, h, F, 1)
+    torch.cuda.synchronize()
+    mesh.destroy()
+    for r, b in enumerate(bufs):
+        assert rel(to_np(b["z"]), fw["z"][r]) <= TOL
+
+
+@pytest.mark.parametrize("d1,d2", [(2, 2), (4, 2), (1, 1)])
+def test_ragged_chunk_and_odd_sizes(d1, d2):
+    # T/chunks = 72 rows (not a multiple of the 128-row tile), head dim 16
+    T, h, F, heads, chunks, seed = 216, 192, 320, 12, 3, 29
+    if heads % d1:
+        pytest.skip("heads % d1")
+    g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, d1, d2, chunks, seed)
+    bufs = run_gpu_layer(d1, d2, T, h, F, heads, chunks, seed)
+    compare(bufs, fw, bw, d1, d2)
+
+
+@pytest.mark.parametrize("colfirst", [True, False])
+@pytest.mark.parametrize("d1,d2", [(2, 2), (4, 2), (2, 4), (1, 1)])
+@pytest.mark.parametrize("chunks", [1, 4])
+def test_single_linear(colfirst, d1, d2, chunks):
+    """atp_linear_{colfirst,rowfirst}_{fwd,bwd} vs the oracle's sharded linear."""
+    import torch
+    import datagen
+    import paper_2301_08658_b200 as atp
+    from oracle import layer as olayer, sharding as osh
+    from oracle.sharding import R, S1
+
+    M, K, N, seed = 256, 384, 512, 3
+    X = datagen.tensor("lin_x", (M, K), seed).astype(np.float64)
+    W = datagen.tensor("lin_w", (K, N), seed).astype(np.float64) * 20
+    W = datagen.round_bf16(W.astype(np.float32)).astype(np.float64)
+    bvec = datagen.tensor("lin_b", (N,), seed).astype(np.float64)
+    dY = datagen.tensor("lin_dy", (M, N), seed).astype(np.float64)
+    xs = (olayer.ACT if colfirst else (S1, R))
+    ws = olayer.COL_W if colfirst else olayer.ROW_W
+    ys = olayer.COL_OUT if colfirst else olayer.ACT
+    Xl, Wl, dYl = osh.shard(X, xs, d1, d2), osh.shard(W, ws, d1, d2), osh.shard(dY, ys, d1, d2)
+    bl = [osh.local(bvec[None, :], ys, d1, d2, r)[0] for r in range(d1 * d2)]
+    fwd = olayer.colfirst_forward if colfirst else olayer.rowfirst_forward
+    Yl = fwd(Xl, Wl, d1, d2)
+    Yl = [y + b for y, b in zip(Yl, bl)]
+    dXl, dWl = olayer.linear_backward("col" if colfirst else "row", Xl, Wl, dYl, d1, d2)
+    mesh = atp.Mesh.virtual(d1, d2)
+    T_ = lambda a, dt=torch.bfloat16: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+    fa = [dict(x=T_(Xl[r]), w=T_(Wl[r]), bias=T_(bl[r]), y=torch.empty(Yl[r].shape, dtype=torch.bfloat16, device="cuda"))
+          for r in range(d1 * d2)]
+    atp.atp_linear_fwd(mesh, colfirst, fa, M, K, N, chunks)
+    ba = [dict(x=fa[r]["x"], w=fa[r]["w"], dy=T_(dYl[r]), dx=torch.empty(Xl[r].shape, dtype=torch.bfloat16, device="cuda"),
+               dw=torch.empty(Wl[r].shape, dtype=torch.float32, device="cuda"),
+               dbias=torch.empty(bl[r].shape, dtype=torch.float32, device="cuda")) for r in range(d1 * d2)]
+    atp.atp_linear_bwd(mesh, colfirst, ba, M, K, N, chunks)
+    torch.cuda.synchronize()
+    mesh.destroy()
+    for r in range(d1 * d2):
+        assert rel(to_np(fa[r]["y"]), Yl[r]) <= TOL
+        assert rel(to_np(ba[r]["dx"]), dXl[r]) <= TOL
+        assert rel(to_np(ba[r]["dw"]), dWl[r]) <= TOL
+        assert rel(to_np(ba[r]["dbias"]), dYl[r].sum(axis=0)) <= TOL
+
+
+def test_shape_errors_before_enqueue():
+    import paper_2301_08658_b200 as atp
+
+    mesh = atp.Mesh.virtual(2, 2)
+    try:
+        bufs = [atp.alloc_layer_rank(2, 2, r, 64, 64, 256, "cuda", 1) for r in range(4)]
+        with pytest.raises(atp.AtpError) as e:
+            atp.atp_layer_fwd_bwd(mesh, bufs, 64, 64, 256, 3, 1)  # heads % d1 != 0
+        assert e.value.status == 2
+        with pytest.raises(atp.AtpError):
+            atp.atp_layer_fwd_bwd(mesh, bufs, 64, 64, 256, 4, 3)  # T % chunks != 0
+    finally:
+        mesh.destroy()
