@@ -33,6 +33,7 @@ struct GemmDesc {
   int M = 0, N = 0, K = 0;
   bool a_mn = false, b_mn = false;
   int bn = 0;        // 128 or 256 (0 = choose)
+  int cg = 0;        // 1 = single CTA (128 x bn tile), 2 = CTA pair (256 x bn); 0 = choose
   int max_ctas = 0;  // persistent grid cap (0 = all SMs)
   int epi = EPI_BF16;
   EpiParams ep;

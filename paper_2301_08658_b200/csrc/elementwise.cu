@@ -12,6 +12,7 @@
 // All kernels move 16 B per thread per access (8 bf16) and use grid-stride
 // loops with a grid sized to a multiple of the SM count.
 #include <cuda_bf16.h>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -121,34 +122,77 @@ __global__ void core_bwd_kernel(const __nv_bfloat16* __restrict__ dctx, __nv_bfl
   }
 }
 
-// db[c] = sum_t x[t, c]: one block per 64-column strip; warp w sums rows
-// w, w+W, ... in order (2 columns per lane), then the W warp partials are added
-// in warp order -> deterministic, no workspace.
-constexpr int kColsumWarps = 16;
+// db[c] = sum_t x[t, c], deterministic and workspace-free.  A cluster of
+// kColsumSplit CTAs shares one 128-column strip: CTA s sums its contiguous
+// row range (8 warps, 4 columns per lane, rows in order per warp, warps added
+// in order), then CTA 0 adds the kColsumSplit partials in rank order through
+// distributed shared memory.
+constexpr int kColsumSplit = 8;
+constexpr int kColsumWarps = 8;
 __global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(const __nv_bfloat16* __restrict__ x,
                                                                   float* __restrict__ out, int64_t rows, int cols) {
-  __shared__ float2 part[kColsumWarps][32];
+  namespace cg = cooperative_groups;
+  __shared__ float4 part[kColsumWarps][32];
+  __shared__ float4 total[32];
+  cg::cluster_group cluster = cg::this_cluster();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int c2 = blockIdx.x * 64 + 2 * lane;
-  float a = 0.f, b = 0.f;
-  if (c2 < cols) {
-    for (int64_t r = warp; r < rows; r += kColsumWarps) {
-      float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + r * cols + c2));
-      a += f.x;
-      b += f.y;
+  const int s = static_cast<int>(cluster.block_rank());
+  const int c4 = blockIdx.x * 128 + 4 * lane;
+  const int64_t per = (rows + kColsumSplit - 1) / kColsumSplit;
+  const int64_t r0 = s * per, r1 = min(rows, r0 + per);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c4 < cols) {
+    int64_t r = r0 + warp;
+    for (; r + 3 * kColsumWarps < r1; r += 4 * kColsumWarps) {
+      uint2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const uint2*>(x + (r + u * kColsumWarps) * cols + c4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[u].x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[u].y));
+        acc.x += a.x;
+        acc.y += a.y;
+        acc.z += b.x;
+        acc.w += b.y;
+      }
+    }
+    for (; r < r1; r += kColsumWarps) {
+      const uint2 v = *reinterpret_cast<const uint2*>(x + r * cols + c4);
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+      acc.x += a.x;
+      acc.y += a.y;
+      acc.z += b.x;
+      acc.w += b.y;
     }
   }
-  part[warp][lane] = make_float2(a, b);
+  part[warp][lane] = acc;
   __syncthreads();
-  if (warp == 0 && c2 < cols) {
-    float2 s = part[0][lane];
+  if (warp == 0) {
+    float4 t = part[0][lane];
     for (int w = 1; w < kColsumWarps; ++w) {
-      s.x += part[w][lane].x;
-      s.y += part[w][lane].y;
+      t.x += part[w][lane].x;
+      t.y += part[w][lane].y;
+      t.z += part[w][lane].z;
+      t.w += part[w][lane].w;
     }
-    out[c2] = s.x;
-    out[c2 + 1] = s.y;
+    total[lane] = t;
   }
+  cluster.sync();
+  if (s == 0 && warp == 0 && c4 < cols) {
+    float4 t = total[lane];
+    for (int r = 1; r < kColsumSplit; ++r) {
+      const float4* remote = cluster.map_shared_rank(total, r);
+      const float4 u = remote[lane];
+      t.x += u.x;
+      t.y += u.y;
+      t.z += u.z;
+      t.w += u.w;
+    }
+    *reinterpret_cast<float4*>(out + c4) = t;
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
 }
 
 __global__ void group_sum_kernel(GroupSumArgs g, int64_t n8) {
@@ -194,10 +238,20 @@ cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
       core_bwd_kernel<<<ew_grid(e.rows * e.cols / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, e.rows,
                                                                     e.heads, static_cast<int>(e.cols / e.heads));
       break;
-    case EW_COLSUM:
-      colsum_kernel<<<static_cast<int>((e.cols + 63) / 64), kColsumWarps * 32, 0, st>>>(
-          (const bf*)e.a, (float*)e.out, e.rows, static_cast<int>(e.cols));
-      break;
+    case EW_COLSUM: {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>((e.cols + 127) / 128), kColsumSplit);
+      cfg.blockDim = dim3(kColsumWarps * 32);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 1;
+      attr[0].val.clusterDim.y = kColsumSplit;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, colsum_kernel, (const bf*)e.a, (float*)e.out, e.rows, static_cast<int>(e.cols));
+    }
     default:
       return cudaErrorInvalidValue;
   }

@@ -13,7 +13,8 @@
 // Design (persistent, warp-specialised, one CTA per SM):
 //   warp 0      TMA producer: 128B-swizzled boxes into a STAGES-deep smem ring
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
-//   warps 2..5  epilogue: tcgen05.ld -> registers -> fused epilogue -> global
+//   warps 2..9  epilogue: tcgen05.ld -> registers -> fused epilogue -> global
+//               (two warps per TMEM lane quadrant, each draining half the columns)
 //   TMEM holds two BN-column fp32 accumulators so the epilogue of tile i
 //   overlaps the main loop of tile i+1.
 #include <cuda.h>
@@ -23,6 +24,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "atp_internal.h"
@@ -34,7 +36,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                 // 2 per SM sub-partition: hides epilogue latency
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer warp + MMA warp + epilogue warps
 constexpr uint32_t kBoxBytesMN = 64 * 64 * 2;  // one MN-major box: 64 (mn) x 64 (k)
 
 __device__ __forceinline__ float gelu_f(float x) {
@@ -50,22 +53,113 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
-template <int BN, int STAGES>
+template <int CG, int BN, int STAGES>
 struct SmemLayout {
-  static constexpr uint32_t kABytes = BM * BK * 2;
-  static constexpr uint32_t kBBytes = BN * BK * 2;
+  static constexpr uint32_t kABytes = BM * BK * 2;             // this CTA's 128 rows of A
+  static constexpr uint32_t kBBytes = (BN / CG) * BK * 2;      // this CTA's share of B
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem slot
   static constexpr uint32_t kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;
 };
 
-template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
+// Tile order: groups of kGroupM M-tiles sweep all N-tiles, so the ~148 tiles in
+// flight share a few A row-blocks and B column-blocks in L2.
+constexpr int kGroupM = 16;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mt, int& nt) {
+  const int per_group = kGroupM * num_n;
+  const int g = tile / per_group;
+  const int first = g * kGroupM;
+  const int gm = min(kGroupM, num_m - first);
+  const int r = tile - g * per_group;
+  mt = first + r % gm;
+  nt = r / gm;
+}
+
+// One 32-column slice of one accumulator row: fused epilogue + 16-byte stores.
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(float (&f)[32], int row, int col0, int M, int N, const EpiParams& ep) {
+  if (row >= M || col0 >= N) return;
+  if (ep.bias != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < N) f[j] += __bfloat162float(ep.bias[col0 + j]);
+  }
+  const bool full = (col0 + 32 <= N);
+  if constexpr (EPI == EPI_F32) {
+    float* dst = static_cast<float*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (full || col0 + 4 * g + 4 <= N)
+        reinterpret_cast<float4*>(dst)[g] = make_float4(f[4 * g], f[4 * g + 1], f[4 * g + 2], f[4 * g + 3]);
+  } else {
+    if constexpr (EPI == EPI_RESID) {
+      const __nv_bfloat16* r = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (full || col0 + 8 * g + 8 <= N) {
+          uint4 rv = reinterpret_cast<const uint4*>(r)[g];
+          const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) f[8 * g + j] += __bfloat162float(rb[j]);
+        }
+      }
+    }
+    if constexpr (EPI == EPI_BIAS_GELU) {
+      // U = acc + bias (stored, rounded once); H = GeLU(U) from the rounded U
+      __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(ep.C2) + static_cast<int64_t>(row) * ep.ldc2 + col0;
+      uint32_t hp[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float u0 = __bfloat162float(__float2bfloat16_rn(f[2 * j]));
+        const float u1 = __bfloat162float(__float2bfloat16_rn(f[2 * j + 1]));
+        hp[j] = pack_bf16(gelu_f(u0), gelu_f(u1));
+      }
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (full || col0 + 8 * g + 8 <= N)
+          reinterpret_cast<uint4*>(dh)[g] = make_uint4(hp[4 * g], hp[4 * g + 1], hp[4 * g + 2], hp[4 * g + 3]);
+    }
+    if constexpr (EPI == EPI_DGELU) {
+      // dU = dH * GeLU'(U); dH is the bf16-rounded product (as after an all-reduce)
+      const __nv_bfloat16* u = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (full || col0 + 8 * g + 8 <= N) {
+          uint4 uv = reinterpret_cast<const uint4*>(u)[g];
+          const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float dh = __bfloat162float(__float2bfloat16_rn(f[8 * g + j]));
+            f[8 * g + j] = dh * gelu_grad_f(__bfloat162float(ub[j]));
+          }
+        }
+      }
+    }
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
+    uint32_t p[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) p[j] = pack_bf16(f[2 * j], f[2 * j + 1]);
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if (full || col0 + 8 * g + 8 <= N)
+        reinterpret_cast<uint4*>(dst)[g] = make_uint4(p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
+  }
+}
+
+// CG = 1: one CTA per 128 x BN tile (cta_group::1).
+// CG = 2: a CTA pair (cluster of 2) per 256 x BN tile (cta_group::2): each CTA
+//         loads its 128 rows of A and BN/2 rows of B, the leader CTA issues
+//         M=256 MMAs that read both CTAs' smem, each CTA's TMEM holds its 128
+//         accumulator rows; smem stage bytes and L2->SM traffic per FLOP drop
+//         by a third.
+template <int CG, int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       int M, int N, int K, EpiParams ep) {
-  using L = SmemLayout<BN, STAGES>;
+  using L = SmemLayout<CG, BN, STAGES>;
   constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr int BNC = BN / CG;  // B rows loaded by this CTA
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -79,11 +173,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
+  const uint32_t cta_rank = CG == 2 ? ptx::cluster_ctarank() : 0;
+  const bool leader = cta_rank == 0;
 
-  const int num_m = (M + BM - 1) / BM;
+  const int num_m = (M + BM * CG - 1) / (BM * CG);
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
   const int num_tiles = num_m * num_n;
+  const int unit = blockIdx.x / CG;      // tile-processing unit (CTA or CTA pair)
+  const int n_units = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -94,45 +192,63 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(tfull_bar(a), 1);
-      ptx::mbar_init(tempty_bar(a), 4);
+      ptx::mbar_init(tempty_bar(a), kEpiWarps * CG);
     }
     ptx::fence_barrier_init();
   }
   if (warp == 1) {
-    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), TMEM_COLS);
-    ptx::tmem_relinquish();
+    if constexpr (CG == 2) {
+      ptx::tmem_alloc_cg2(ptx::smem_u32(tmem_slot), TMEM_COLS);
+      ptx::tmem_relinquish_cg2();
+    } else {
+      ptx::tmem_alloc(ptx::smem_u32(tmem_slot), TMEM_COLS);
+      ptx::tmem_relinquish();
+    }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    ptx::cluster_sync();
+  } else {
+    __syncthreads();
+  }
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------ TMA producer
+      // ------------------------------------------------ TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % num_m) * BM;
-        const int n0 = (tile / num_m) * BN;
+      for (int tile = unit; tile < num_tiles; tile += n_units) {
+        int mt, nt;
+        tile_coords(tile, num_m, num_n, mt, nt);
+        const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
+        const int nb = nt * BN + BNC * static_cast<int>(cta_rank);
         for (int kb = 0; kb < num_k; ++kb) {
           ptx::mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sA = base + stage * L::kStageBytes;
           const uint32_t sB = sA + L::kABytes;
           const uint32_t fb = full_bar(stage);
-          ptx::mbar_arrive_expect_tx(fb, L::kStageBytes);
+          if (leader) ptx::mbar_arrive_expect_tx(fb, L::kStageBytes * CG);
           const int k0 = kb * BK;
+          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1) {
+            if constexpr (CG == 2) {
+              ptx::tma_load_2d_cg2(dst, tm, fb, c0, c1);
+            } else {
+              ptx::tma_load_2d(dst, tm, fb, c0, c1);
+            }
+          };
           if constexpr (!A_MN) {
-            ptx::tma_load_2d(sA, &tmA, fb, k0, m0);
+            load(sA, &tmA, k0, m0);
           } else {
-            ptx::tma_load_2d(sA, &tmA, fb, m0, k0);
-            ptx::tma_load_2d(sA + kBoxBytesMN, &tmA, fb, m0 + 64, k0);
+            load(sA, &tmA, m0, k0);
+            load(sA + kBoxBytesMN, &tmA, m0 + 64, k0);
           }
           if constexpr (!B_MN) {
-            ptx::tma_load_2d(sB, &tmB, fb, k0, n0);
+            load(sB, &tmB, k0, nb);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sB + j * kBoxBytesMN, &tmB, fb, n0 + 64 * j, k0);
+            for (int j = 0; j < BNC / 64; ++j) load(sB + j * kBoxBytesMN, &tmB, nb + 64 * j, k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -142,14 +258,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    if (lane == 0 && leader) {
+      // ------------------------------------------------ MMA issuer (leader CTA only)
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM * CG, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < num_tiles; tile += n_units) {
         ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -164,15 +280,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : ptx::smem_desc_sw128(sA + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::smem_desc_sw128(sB + kk * 2048, kBoxBytesMN, 1024)
                                      : ptx::smem_desc_sw128(sB + kk * 32, 16, 1024);
-            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            if constexpr (CG == 2) {
+              ptx::mma_bf16_ss_cg2(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            } else {
+              ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            }
           }
-          ptx::mma_commit(empty_bar(stage));
+          if constexpr (CG == 2) {
+            ptx::mma_commit_cg2_mc(empty_bar(stage), 0x3);
+          } else {
+            ptx::mma_commit(empty_bar(stage));
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(tfull_bar(acc));
+        if constexpr (CG == 2) {
+          ptx::mma_commit_cg2_mc(tfull_bar(acc), 0x3);
+        } else {
+          ptx::mma_commit(tfull_bar(acc));
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -180,96 +308,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue warps 2..5
+    // ------------------------------------------------ epilogue warps 2..9 (both CTAs)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) / 4;  // which half of the BN columns this warp drains
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile % num_m) * BM;
-      const int n0 = (tile / num_m) * BN;
+    for (int tile = unit; tile < num_tiles; tile += n_units) {
+      int mt, nt;
+      tile_coords(tile, num_m, num_n, mt, nt);
+      const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
+      const int n0 = nt * BN;
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
       ptx::tc_fence_after();
       const int row = m0 + 32 * q + static_cast<int>(lane);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN + 32 * c, v);
         ptx::tmem_wait_ld();
-        const int col0 = n0 + 32 * c;
-        if (row < M && col0 < N) {
-          float f[32];
+        float f[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-          if (ep.bias != nullptr) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) f[j] += __bfloat162float(ep.bias[col0 + j]);
-          }
-          const bool full = (col0 + 32 <= N);
-          if constexpr (EPI == EPI_F32) {
-            float* dst = static_cast<float*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
-#pragma unroll
-            for (int g = 0; g < 8; ++g)
-              if (full || col0 + 4 * g + 4 <= N)
-                reinterpret_cast<float4*>(dst)[g] = make_float4(f[4 * g], f[4 * g + 1], f[4 * g + 2], f[4 * g + 3]);
-          } else {
-            if constexpr (EPI == EPI_RESID) {
-              const __nv_bfloat16* r = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                if (full || col0 + 8 * g + 8 <= N) {
-                  uint4 rv = reinterpret_cast<const uint4*>(r)[g];
-                  const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) f[8 * g + j] += __bfloat162float(rb[j]);
-                }
-              }
-            }
-            if constexpr (EPI == EPI_BIAS_GELU) {
-              // U = acc + bias (stored, rounded once); H = GeLU(U) from the rounded U
-              __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(ep.C2) + static_cast<int64_t>(row) * ep.ldc2 + col0;
-              uint32_t hp[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const float u0 = __bfloat162float(__float2bfloat16_rn(f[2 * j]));
-                const float u1 = __bfloat162float(__float2bfloat16_rn(f[2 * j + 1]));
-                hp[j] = pack_bf16(gelu_f(u0), gelu_f(u1));
-              }
-#pragma unroll
-              for (int g = 0; g < 4; ++g)
-                if (full || col0 + 8 * g + 8 <= N)
-                  reinterpret_cast<uint4*>(dh)[g] = make_uint4(hp[4 * g], hp[4 * g + 1], hp[4 * g + 2], hp[4 * g + 3]);
-            }
-            if constexpr (EPI == EPI_DGELU) {
-              // dU = dH * GeLU'(U); dH is the bf16-rounded product (as after an all-reduce)
-              const __nv_bfloat16* u = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                if (full || col0 + 8 * g + 8 <= N) {
-                  uint4 uv = reinterpret_cast<const uint4*>(u)[g];
-                  const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uv);
-#pragma unroll
-                  for (int j = 0; j < 8; ++j) {
-                    const float dh = __bfloat162float(__float2bfloat16_rn(f[8 * g + j]));
-                    f[8 * g + j] = dh * gelu_grad_f(__bfloat162float(ub[j]));
-                  }
-                }
-              }
-            }
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
-            uint32_t p[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) p[j] = pack_bf16(f[2 * j], f[2 * j + 1]);
-#pragma unroll
-            for (int g = 0; g < 4; ++g)
-              if (full || col0 + 8 * g + 8 <= N)
-                reinterpret_cast<uint4*>(dst)[g] = make_uint4(p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
-          }
-        }
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        epilogue_chunk<EPI>(f, row, n0 + 32 * c, M, N, ep);
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(tempty_bar(acc));
+      if (lane == 0) {
+        if constexpr (CG == 2) {
+          ptx::mbar_arrive_cluster(ptx::mapa_shared(tempty_bar(acc), 0));
+        } else {
+          ptx::mbar_arrive(tempty_bar(acc));
+        }
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -278,10 +348,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    ptx::cluster_sync();
+  } else {
+    __syncthreads();
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    if constexpr (CG == 2) {
+      ptx::tmem_dealloc_cg2(tmem_base, TMEM_COLS);
+    } else {
+      ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
   }
 }
 
@@ -315,41 +393,61 @@ bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int6
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
+template <int CG, int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
-  using L = SmemLayout<BN, STAGES>;
-  auto kern = gemm_sm100_kernel<BN, STAGES, EPI, A_MN, B_MN>;
+  using L = SmemLayout<CG, BN, STAGES>;
+  auto kern = gemm_sm100_kernel<CG, BN, STAGES, EPI, A_MN, B_MN>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<grid, kThreads, L::kBytes, st>>>(d.tmA, d.tmB, d.M, d.N, d.K, d.ep);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep);
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN>
+template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>
 cudaError_t launch_epi(const GemmDesc& d, int grid, cudaStream_t st) {
   switch (d.epi) {
-    case EPI_BF16: return launch_t<BN, STAGES, EPI_BF16, A_MN, B_MN>(d, grid, st);
-    case EPI_F32: return launch_t<BN, STAGES, EPI_F32, A_MN, B_MN>(d, grid, st);
-    case EPI_RESID: return launch_t<BN, STAGES, EPI_RESID, A_MN, B_MN>(d, grid, st);
-    case EPI_BIAS_GELU: return launch_t<BN, STAGES, EPI_BIAS_GELU, A_MN, B_MN>(d, grid, st);
-    case EPI_DGELU: return launch_t<BN, STAGES, EPI_DGELU, A_MN, B_MN>(d, grid, st);
+    case EPI_BF16: return launch_t<CG, BN, STAGES, EPI_BF16, A_MN, B_MN>(d, grid, st);
+    case EPI_F32: return launch_t<CG, BN, STAGES, EPI_F32, A_MN, B_MN>(d, grid, st);
+    case EPI_RESID: return launch_t<CG, BN, STAGES, EPI_RESID, A_MN, B_MN>(d, grid, st);
+    case EPI_BIAS_GELU: return launch_t<CG, BN, STAGES, EPI_BIAS_GELU, A_MN, B_MN>(d, grid, st);
+    case EPI_DGELU: return launch_t<CG, BN, STAGES, EPI_DGELU, A_MN, B_MN>(d, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 
-template <int BN, int STAGES>
+template <int CG, int BN, int STAGES>
 cudaError_t launch_bn(const GemmDesc& d, int grid, cudaStream_t st) {
-  if (!d.a_mn && d.b_mn) return launch_epi<BN, STAGES, false, true>(d, grid, st);
-  if (!d.a_mn && !d.b_mn) return launch_epi<BN, STAGES, false, false>(d, grid, st);
-  if (d.a_mn && d.b_mn) return launch_epi<BN, STAGES, true, true>(d, grid, st);
+  if (!d.a_mn && d.b_mn) return launch_epi<CG, BN, STAGES, false, true>(d, grid, st);
+  if (!d.a_mn && !d.b_mn) return launch_epi<CG, BN, STAGES, false, false>(d, grid, st);
+  if (d.a_mn && d.b_mn) return launch_epi<CG, BN, STAGES, true, true>(d, grid, st);
   return cudaErrorInvalidValue;  // (MN, K) is not used by the layer
 }
 
 int g_num_sms = 0;
+
+// ATP_GEMM_MODE=1 forces single-CTA tiles (A/B comparison of the two kernels).
+int gemm_mode() {
+  static int mode = [] {
+    const char* e = getenv("ATP_GEMM_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  return mode;
+}
 
 }  // namespace
 
@@ -364,7 +462,7 @@ int num_sms() {
 }
 
 int gemm_tiles(const GemmDesc& d) {
-  return ((d.M + BM - 1) / BM) * ((d.N + d.bn - 1) / d.bn);
+  return ((d.M + BM * d.cg - 1) / (BM * d.cg)) * ((d.N + d.bn - 1) / d.bn);
 }
 
 // Validate and build the TMA descriptors of one GEMM.  Returns a message on error.
@@ -381,6 +479,9 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
   d.a_mn = a_mn;
   d.b_mn = b_mn;
   if (d.bn != 128 && d.bn != 256) d.bn = (N % 256 == 0 || N > 1024) ? 256 : 128;
+  // CTA pairs for big tiles (M >= 256 and a full 256-wide N tile), single CTAs otherwise
+  if (d.cg != 1 && d.cg != 2) d.cg = (d.bn == 256 && M >= 256 && gemm_mode() != 1) ? 2 : 1;
+  if (d.cg == 2 && d.bn != 256) d.cg = 1;
   bool ok;
   if (!a_mn)
     ok = make_tmap(&d.tmA, A, M, K, lda, BM, BK);
@@ -388,7 +489,7 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
     ok = make_tmap(&d.tmA, A, K, M, lda, BK, 64);
   if (!ok) return "gemm: cuTensorMapEncodeTiled failed for A";
   if (!b_mn)
-    ok = make_tmap(&d.tmB, B, N, K, ldb, d.bn, BK);
+    ok = make_tmap(&d.tmB, B, N, K, ldb, d.bn / d.cg, BK);
   else
     ok = make_tmap(&d.tmB, B, K, N, ldb, BK, 64);
   if (!ok) return "gemm: cuTensorMapEncodeTiled failed for B";
@@ -397,10 +498,12 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t st) {
   int sms = d.max_ctas > 0 ? d.max_ctas : num_sms();
-  int tiles = gemm_tiles(d);
-  int grid = tiles < sms ? tiles : sms;
-  if (d.bn == 256) return launch_bn<256, 4>(d, grid, st);
-  return launch_bn<128, 6>(d, grid, st);
+  const int units = sms / d.cg > 0 ? sms / d.cg : 1;
+  const int tiles = gemm_tiles(d);
+  const int grid = (tiles < units ? tiles : units) * d.cg;
+  if (d.cg == 2) return launch_bn<2, 256, 6>(d, grid, st);
+  if (d.bn == 256) return launch_bn<1, 256, 4>(d, grid, st);
+  return launch_bn<1, 128, 6>(d, grid, st);
 }
 
 }  // namespace atp

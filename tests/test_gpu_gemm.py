@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [
     (128, 128, 64), (256, 256, 128), (200, 136, 72), (1024, 768, 640), (384, 1280, 2560),
-    (2048, 1536, 512), (136, 2056, 1024), (8, 8, 8),
+    (2048, 1536, 512), (136, 2056, 1024), (8, 8, 8), (520, 1032, 200), (264, 256, 64),
 ]
 
 
