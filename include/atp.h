@@ -76,6 +76,11 @@ atp_status atp_mesh_init(int d1, int d2, int world_rank, const uint8_t uid[128],
                          atp_mesh** out);
 /* All d1*d2 ranks of a mesh in this process on `cuda_device` (see header). */
 atp_status atp_vmesh_init(int d1, int d2, int cuda_device, atp_mesh** out);
+/* Dry-run handle for ONE rank `rank` of DeviceMesh(d1, d2) on `cuda_device`
+ * without communicators: every all-reduce of its schedule is elided (results
+ * are therefore not the mesh's results).  Used to measure, on one GPU, the
+ * compute part of a rank's step for a mesh that needs d1*d2 GPUs. */
+atp_status atp_mesh_init_local(int d1, int d2, int rank, int cuda_device, atp_mesh** out);
 atp_status atp_mesh_destroy(atp_mesh* mesh);
 /* Coordinates of a distributed mesh's rank (virtual mesh: ATP_ERR_INVALID). */
 atp_status atp_mesh_coords(const atp_mesh* mesh, int* i1, int* i2);

@@ -101,6 +101,7 @@ SIGNATURES = {
     "atp_get_unique_id": (C.c_int, [C.c_char_p]),
     "atp_mesh_init": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(vp)]),
     "atp_vmesh_init": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "atp_mesh_init_local": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "atp_mesh_destroy": (C.c_int, [vp]),
     "atp_mesh_coords": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "atp_mesh_dims": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),

@@ -49,6 +49,13 @@ class Mesh:
         return cls(h, d1, d2, True)
 
     @classmethod
+    def local(cls, d1: int, d2: int, rank: int, device: int = 0) -> "Mesh":
+        """Dry-run handle of one rank (collectives elided) for single-GPU measurement."""
+        h = C.c_void_p()
+        check(lib().atp_mesh_init_local(d1, d2, rank, device, C.byref(h)))
+        return cls(h, d1, d2, False, rank)
+
+    @classmethod
     def distributed(cls, d1: int, d2: int, rank: int, uid: bytes, device: int) -> "Mesh":
         h = C.c_void_p()
         check(lib().atp_mesh_init(d1, d2, rank, uid, device, C.byref(h)))

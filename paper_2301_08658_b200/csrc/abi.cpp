@@ -68,6 +68,10 @@ atp_status atp_mesh_init(int d1, int d2, int world_rank, const uint8_t uid[128],
   return static_cast<atp_status>(atp::mesh_create(d1, d2, world_rank, uid, cuda_device, false, out));
 }
 
+atp_status atp_mesh_init_local(int d1, int d2, int rank, int cuda_device, atp_mesh** out) {
+  return static_cast<atp_status>(atp::mesh_create(d1, d2, rank, nullptr, cuda_device, false, out));
+}
+
 atp_status atp_vmesh_init(int d1, int d2, int cuda_device, atp_mesh** out) {
   return static_cast<atp_status>(atp::mesh_create(d1, d2, 0, nullptr, cuda_device, true, out));
 }
@@ -116,6 +120,7 @@ atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas) {
 // ---------------------------------------------------------------- measurement hooks
 atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled) {
   if (mesh == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_set_comm_enabled: NULL mesh");
+  if (mesh->local_only && enabled) return fail(ATP_ERR_INVALID, "atp_mesh_set_comm_enabled: local mesh has no communicators");
   mesh->comm_enabled = enabled != 0;
   return ATP_OK;
 }
@@ -165,7 +170,7 @@ atp_status atp_gemm(const void* A, int64_t lda, int a_mn, const void* B, int64_t
   d.epi = out_f32 ? atp::EPI_F32 : atp::EPI_BF16;
   d.ep.C = C;
   d.ep.ldc = ldc;
-  d.ep.bias = static_cast<const __nv_bfloat16*>(bias);
+  d.ep.bias = bias;
   const char* m = atp::gemm_prepare(d, A, lda, a_mn != 0, B, ldb, b_mn != 0, (int)M, (int)N, (int)K);
   if (m) return fail(ATP_ERR_SHAPE, m);
   atp::count_launch(1);
@@ -181,8 +186,10 @@ static atp_status linear_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, in
   if (s) return s;
   if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "linear: only ATP_BF16");
   const int din = colfirst ? mesh->d2 : mesh->d1, dout = colfirst ? mesh->d1 : mesh->d2;
-  if (chunks < 1 || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) || !w8(N / dout))
-    return fail(ATP_ERR_SHAPE, "linear fwd: need M % chunks == 0, K % d_in == 0, N % d_out == 0, local widths % 8 == 0");
+  if (chunks < 1 || chunks > atp::kMaxChunks || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) ||
+      !w8(N / dout))
+    return fail(ATP_ERR_SHAPE,
+                "linear fwd: need 1 <= chunks <= 16, M % chunks == 0, K % d_in == 0, N % d_out == 0, widths % 8 == 0");
   for (int r = 0; r < n_ranks(mesh); ++r)
     if (!args[r].x || !args[r].w || !args[r].y) return fail(ATP_ERR_INVALID, "linear fwd: NULL buffer");
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
@@ -196,8 +203,10 @@ static atp_status linear_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, in
   if (s) return s;
   if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "linear: only ATP_BF16");
   const int din = colfirst ? mesh->d2 : mesh->d1, dout = colfirst ? mesh->d1 : mesh->d2;
-  if (chunks < 1 || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) || !w8(N / dout) || M % 8)
-    return fail(ATP_ERR_SHAPE, "linear bwd: need M % chunks == 0, M % 8 == 0, K % d_in, N % d_out, local widths % 8 == 0");
+  if (chunks < 1 || chunks > atp::kMaxChunks || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) ||
+      !w8(N / dout) || M % 8)
+    return fail(ATP_ERR_SHAPE,
+                "linear bwd: need 1 <= chunks <= 16, M % chunks == 0, M % 8 == 0, K % d_in, N % d_out, widths % 8 == 0");
   for (int r = 0; r < n_ranks(mesh); ++r)
     if (!args[r].x || !args[r].w || !args[r].dy || !args[r].dx) return fail(ATP_ERR_INVALID, "linear bwd: NULL buffer");
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
@@ -225,8 +234,10 @@ atp_status atp_linear_rowfirst_bwd(atp_mesh* mesh, const atp_linear_bwd_args* ar
 // ---------------------------------------------------------------- composites
 static atp_status check_layer_shapes(const atp_mesh* m, int64_t T, int64_t h, int64_t F, int64_t heads, int chunks,
                                      bool attn, bool mlp) {
-  if (chunks < 1 || T < 1 || h < 1 || T % chunks || (T / chunks) % 8 || h % m->d2 || !w8(h / m->d2))
-    return fail(ATP_ERR_SHAPE, "layer: need T % chunks == 0, (T/chunks) % 8 == 0, h % d2 == 0, (h/d2) % 8 == 0");
+  if (chunks < 1 || chunks > atp::kMaxChunks || T < 1 || h < 1 || T % chunks || (T / chunks) % 8 || h % m->d2 ||
+      !w8(h / m->d2))
+    return fail(ATP_ERR_SHAPE,
+                "layer: need 1 <= chunks <= 16, T % chunks == 0, (T/chunks) % 8 == 0, h % d2 == 0, (h/d2) % 8 == 0");
   if (mlp && (F < 1 || F % m->d1 || !w8(F / m->d1)))
     return fail(ATP_ERR_SHAPE, "mlp: need F % d1 == 0 and (F/d1) % 8 == 0");
   if (attn && (heads < 1 || heads % m->d1 || h % heads || (h / heads) % 8 || !w8(h / m->d1)))
@@ -335,7 +346,7 @@ atp_status atp_probe_allreduce(atp_mesh* mesh, int dim, size_t msg_bytes, int it
                                double* algbw_gbps, double* seconds) {
   if (mesh == nullptr || buf == nullptr || iters < 1 || msg_bytes < 2 || (dim != 1 && dim != 2))
     return fail(ATP_ERR_INVALID, "atp_probe_allreduce: bad arguments");
-  if (mesh->is_virtual) return fail(ATP_ERR_INVALID, "atp_probe_allreduce: needs a distributed mesh");
+  if (mesh->is_virtual || mesh->local_only) return fail(ATP_ERR_INVALID, "atp_probe_allreduce: needs a distributed mesh");
   const int p = dim == 1 ? mesh->d1 : mesh->d2;
   if (busbw_gbps) *busbw_gbps = 0.0;
   if (algbw_gbps) *algbw_gbps = 0.0;

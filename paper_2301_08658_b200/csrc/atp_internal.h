@@ -20,8 +20,8 @@ enum EpiKind : int {
 struct EpiParams {
   void* C = nullptr;
   int64_t ldc = 0;
-  const __nv_bfloat16* bias = nullptr;
-  const __nv_bfloat16* aux = nullptr;
+  const void* bias = nullptr;  // [N] bf16, or nullptr
+  const void* aux = nullptr;   // residual (EPI_RESID) or saved U (EPI_DGELU), bf16
   int64_t ldaux = 0;
   void* C2 = nullptr;
   int64_t ldc2 = 0;
@@ -37,6 +37,11 @@ struct GemmDesc {
   int max_ctas = 0;  // persistent grid cap (0 = all SMs)
   int epi = EPI_BF16;
   EpiParams ep;
+  // Chunk signalling (schedule.cpp "signalled stages"): tiles run chunk by
+  // chunk (sig_rows rows each) and every CTA-tile of chunk k adds 1 to sig[k]
+  // once its output is globally visible.  nullptr = no signalling.
+  uint32_t* sig = nullptr;
+  int sig_rows = 0;
 };
 
 // C[M,N] = A[M,K] * B[N,K]^T.
@@ -45,6 +50,8 @@ struct GemmDesc {
 const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, const void* B,
                          int64_t ldb, bool b_mn, int M, int N, int K);
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t st);
+// Tile plan gemm_prepare will use for an M x N output: N tile (128/256) and CTA group (1/2).
+void gemm_plan_tile(int M, int N, int* bn, int* cg);
 int gemm_tiles(const GemmDesc& d);
 int num_sms();
 

@@ -63,16 +63,21 @@ struct SmemLayout {
   static constexpr uint32_t kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;
 };
 
-// Tile order: groups of kGroupM M-tiles sweep all N-tiles, so the ~148 tiles in
-// flight share a few A row-blocks and B column-blocks in L2.
+// Tile order: chunk by chunk (mt_chunk M-tiles per chunk; = all M-tiles when
+// not signalling), and inside a chunk groups of kGroupM M-tiles sweep all
+// N-tiles, so the ~148 tiles in flight share a few A row-blocks and B
+// column-blocks in L2.
 constexpr int kGroupM = 16;
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mt, int& nt) {
+__device__ __forceinline__ void tile_coords(int tile, int mt_chunk, int num_n, int& mt, int& nt, int& chunk) {
+  const int per_chunk = mt_chunk * num_n;
+  chunk = tile / per_chunk;
+  const int r0 = tile - chunk * per_chunk;
   const int per_group = kGroupM * num_n;
-  const int g = tile / per_group;
+  const int g = r0 / per_group;
   const int first = g * kGroupM;
-  const int gm = min(kGroupM, num_m - first);
-  const int r = tile - g * per_group;
-  mt = first + r % gm;
+  const int gm = min(kGroupM, mt_chunk - first);
+  const int r = r0 - g * per_group;
+  mt = chunk * mt_chunk + first + r % gm;
   nt = r / gm;
 }
 
@@ -83,7 +88,7 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int row, int col0
   if (ep.bias != nullptr) {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (col0 + j < N) f[j] += __bfloat162float(ep.bias[col0 + j]);
+      if (col0 + j < N) f[j] += __bfloat162float(static_cast<const __nv_bfloat16*>(ep.bias)[col0 + j]);
   }
   const bool full = (col0 + 32 <= N);
   if constexpr (EPI == EPI_F32) {
@@ -94,7 +99,7 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int row, int col0
         reinterpret_cast<float4*>(dst)[g] = make_float4(f[4 * g], f[4 * g + 1], f[4 * g + 2], f[4 * g + 3]);
   } else {
     if constexpr (EPI == EPI_RESID) {
-      const __nv_bfloat16* r = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
+      const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(ep.aux) + static_cast<int64_t>(row) * ep.ldaux + col0;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         if (full || col0 + 8 * g + 8 <= N) {
@@ -122,7 +127,7 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int row, int col0
     }
     if constexpr (EPI == EPI_DGELU) {
       // dU = dH * GeLU'(U); dH is the bf16-rounded product (as after an all-reduce)
-      const __nv_bfloat16* u = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
+      const __nv_bfloat16* u = static_cast<const __nv_bfloat16*>(ep.aux) + static_cast<int64_t>(row) * ep.ldaux + col0;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         if (full || col0 + 8 * g + 8 <= N) {
@@ -156,7 +161,7 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int row, int col0
 template <int CG, int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      int M, int N, int K, EpiParams ep) {
+                      int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows) {
   using L = SmemLayout<CG, BN, STAGES>;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr int BNC = BN / CG;  // B rows loaded by this CTA
@@ -180,6 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
   const int num_tiles = num_m * num_n;
+  const int mt_chunk = sig != nullptr ? sig_rows / (BM * CG) : num_m;  // M-tiles per chunk
   const int unit = blockIdx.x / CG;      // tile-processing unit (CTA or CTA pair)
   const int n_units = gridDim.x / CG;
 
@@ -220,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = unit; tile < num_tiles; tile += n_units) {
-        int mt, nt;
-        tile_coords(tile, num_m, num_n, mt, nt);
+        int mt, nt, chunk;
+        tile_coords(tile, mt_chunk, num_n, mt, nt, chunk);
         const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
         const int nb = nt * BN + BNC * static_cast<int>(cta_rank);
         for (int kb = 0; kb < num_k; ++kb) {
@@ -314,8 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = unit; tile < num_tiles; tile += n_units) {
-      int mt, nt;
-      tile_coords(tile, num_m, num_n, mt, nt);
+      int mt, nt, chunk;
+      tile_coords(tile, mt_chunk, num_n, mt, nt, chunk);
       const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
       const int n0 = nt * BN;
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
@@ -338,6 +344,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive_cluster(ptx::mapa_shared(tempty_bar(acc), 0));
         } else {
           ptx::mbar_arrive(tempty_bar(acc));
+        }
+      }
+      if (sig != nullptr) {
+        // all epilogue warps of this CTA have issued their stores of this tile;
+        // make them visible (system scope: NCCL peers read them) and count the tile.
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (warp == 2 && lane == 0) {
+          __threadfence_system();
+          atomicAdd(sig + chunk, 1u);
         }
       }
       if (++acc == 2) {
@@ -415,7 +430,7 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep);
+  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows);
 }
 
 template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>
@@ -461,6 +476,13 @@ int num_sms() {
   return g_num_sms;
 }
 
+// N tile 256 when N is a multiple of 256 or large, else 128; CTA pairs for big
+// tiles (M >= 256 and a 256-wide N tile), single CTAs otherwise.
+void gemm_plan_tile(int M, int N, int* bn, int* cg) {
+  *bn = (N % 256 == 0 || N > 1024) ? 256 : 128;
+  *cg = (*bn == 256 && M >= 256 && gemm_mode() != 1) ? 2 : 1;
+}
+
 int gemm_tiles(const GemmDesc& d) {
   return ((d.M + BM * d.cg - 1) / (BM * d.cg)) * ((d.N + d.bn - 1) / d.bn);
 }
@@ -478,8 +500,7 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
   d.K = K;
   d.a_mn = a_mn;
   d.b_mn = b_mn;
-  if (d.bn != 128 && d.bn != 256) d.bn = (N % 256 == 0 || N > 1024) ? 256 : 128;
-  // CTA pairs for big tiles (M >= 256 and a full 256-wide N tile), single CTAs otherwise
+  if (d.bn != 128 && d.bn != 256) gemm_plan_tile(M, N, &d.bn, &d.cg);
   if (d.cg != 1 && d.cg != 2) d.cg = (d.bn == 256 && M >= 256 && gemm_mode() != 1) ? 2 : 1;
   if (d.cg == 2 && d.bn != 256) d.cg = 1;
   bool ok;

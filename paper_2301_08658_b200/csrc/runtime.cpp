@@ -13,10 +13,14 @@
 // gated by events from every member (sum in ascending mesh coordinate, as the
 // oracle does).  This lets a single B200 check the whole sharded pipeline —
 // chunking, events, epilogues — for every mesh shape.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -31,6 +35,27 @@ std::atomic<uint64_t> g_launches{0};
 }  // namespace
 
 void count_launch(uint64_t n) { g_launches += n; }
+
+// cuStreamWaitValue32 from the driver (no link-time libcuda dependency).
+static PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
+static std::once_flag g_wait32_once;
+bool stream_wait_available() {
+  std::call_once(g_wait32_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fn);
+  });
+  return g_wait32 != nullptr;
+}
+
+static cudaError_t wait_sig(RankState& s, const Op& op, cudaStream_t st) {
+  s.sig_total[op.sig_slot] += op.sig_inc;
+  CUresult r = g_wait32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(s.sig_buf + op.sig_slot),
+                        s.sig_total[op.sig_slot], CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
 uint64_t launch_count() { return g_launches.load(); }
 
 // Algorithmic cost of one op (class 0 = GEMM, 1 = elementwise, 2 = all-reduce).
@@ -92,6 +117,8 @@ RankView rank_view(const atp_mesh* m, int r) {
     v.i2 = m->i2;
   }
   v.gemm_ctas = m->gemm_ctas;
+  v.sig_buf = m->rs[m->is_virtual ? r : 0].sig_buf;
+  v.signalled = m->signalled && stream_wait_available();
   return v;
 }
 
@@ -153,6 +180,11 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
     for (const Op& op : sch[0].ops) {
       cudaStream_t st = op.stream ? s.comm : stream;
       if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+      if (op.kind == OP_WAITSIG) {
+        if ((e = wait_sig(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWaitValue32");
+        if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+        continue;
+      }
       ProfRec* pr = prof_begin(m, op, st);
       if (op.kind == OP_AR) {
         if (m->comm_enabled) {
@@ -191,6 +223,11 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
         RankState& s = m->rs[r];
         cudaStream_t st = op.stream ? s.comm : s.compute;
         if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+        if (op.kind == OP_WAITSIG) {
+          if ((e = wait_sig(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWaitValue32");
+          if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+          continue;
+        }
         ProfRec* pr = prof_begin(m, op, st);
         if ((e = launch_local(op, st)) != cudaSuccess)
           return cuda_fail(e, op.kind == OP_GEMM ? "gemm launch" : "elementwise launch");
@@ -258,7 +295,11 @@ static int make_rank_state(RankState& s, bool with_compute) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.arrive, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming);
-  if (e != cudaSuccess) return cuda_fail(e, "stream/event create");
+  if (e == cudaSuccess) e = cudaMalloc(&s.sig_buf, kSigSlots * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(s.sig_buf, 0, kSigSlots * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "stream/event/counter create");
+  s.sig_total.assign(kSigSlots, 0u);
   return 0;
 }
 
@@ -270,6 +311,7 @@ static void free_rank_state(RankState& s) {
   if (s.join) cudaEventDestroy(s.join);
   if (s.comm) cudaStreamDestroy(s.comm);
   if (s.compute) cudaStreamDestroy(s.compute);
+  if (s.sig_buf) cudaFree(s.sig_buf);
   s = RankState();
 }
 
@@ -301,6 +343,10 @@ int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, 
   m->is_virtual = is_virtual;
   m->device = device;
   m->rank = is_virtual ? 0 : world_rank;
+  {
+    const char* e = getenv("ATP_SIGNALLED");
+    m->signalled = !(e && e[0] == '0');
+  }
   m->i1 = m->rank / d2;
   m->i2 = m->rank % d2;
   m->rs.resize(is_virtual ? n : 1);
@@ -313,7 +359,10 @@ int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, 
     }
   }
   cudaEventCreateWithFlags(&m->ev_start, cudaEventDisableTiming);
-  if (!is_virtual) {
+  if (!is_virtual && uid == nullptr) {
+    m->comm_enabled = false;  // local dry-run rank: no communicators, collectives elided
+    m->local_only = true;
+  } else if (!is_virtual) {
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&m->world, n, id, world_rank);

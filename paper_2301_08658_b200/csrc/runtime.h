@@ -15,14 +15,17 @@ namespace atp {
 
 void set_error(const std::string& msg);
 
-enum OpKind : int { OP_GEMM = 0, OP_EW = 1, OP_AR = 2 };
+enum OpKind : int { OP_GEMM = 0, OP_EW = 1, OP_AR = 2, OP_WAITSIG = 3 };
+
+constexpr int kSigSlots = 4096;  // per-rank chunk-completion counters
+constexpr int kMaxChunks = 16;   // chunk count limit (bounds the waits of one op)
 
 // One enqueue on one of a rank's two streams.  `waits` are schedule-local
 // event ids the op's stream waits on first; `record` is recorded after it.
 struct Op {
   OpKind kind = OP_GEMM;
   int stream = 0;  // 0 = compute (caller's stream), 1 = communication
-  int waits[4] = {-1, -1, -1, -1};
+  int waits[kMaxChunks] = {};
   int n_waits = 0;
   int record = -1;
   GemmDesc g;
@@ -30,6 +33,10 @@ struct Op {
   int ar_dim = 0;  // mesh dimension of the grouped all-reduce (1 or 2)
   void* ar_ptr = nullptr;
   int64_t ar_count = 0;  // bf16 elements, in place
+  // OP_WAITSIG: the stream waits until counter `sig_slot` has grown by
+  // `sig_inc` since the previous wait on that slot (cyclic >=).
+  int sig_slot = 0;
+  uint32_t sig_inc = 0;
 };
 
 struct Sched {
@@ -40,6 +47,8 @@ struct Sched {
 struct RankView {
   int d1 = 1, d2 = 1, i1 = 0, i2 = 0;
   int gemm_ctas = 0;
+  uint32_t* sig_buf = nullptr;  // this rank's chunk-completion counters (device)
+  bool signalled = true;        // use signalled stages when possible
 };
 
 struct RankState {
@@ -47,6 +56,8 @@ struct RankState {
   cudaStream_t compute = nullptr;  // virtual mesh only (one per virtual rank)
   std::vector<cudaEvent_t> ev;
   cudaEvent_t arrive = nullptr, done = nullptr, join = nullptr;
+  uint32_t* sig_buf = nullptr;       // device counters [kSigSlots]
+  std::vector<uint32_t> sig_total;   // host mirror of the values the counters reach
 };
 
 }  // namespace atp
@@ -62,6 +73,8 @@ struct ProfRec {
 struct atp_mesh {
   int d1 = 1, d2 = 1;
   bool comm_enabled = true;
+  bool local_only = false;  // atp_mesh_init_local: no communicators
+  bool signalled = true;    // signalled stages (ATP_SIGNALLED=0 disables, for A/B runs)
   bool profiling = false;
   std::vector<atp::ProfRec> prof;  // event pool; the first prof_used are live
   size_t prof_used = 0;
@@ -82,5 +95,6 @@ int execute(atp_mesh* m, std::vector<Sched>& per_rank, cudaStream_t stream);
 void count_launch(uint64_t n);
 uint64_t launch_count();
 void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes);
+bool stream_wait_available();
 
 }  // namespace atp

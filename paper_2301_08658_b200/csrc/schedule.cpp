@@ -1,26 +1,40 @@
 // Schedule builders: the per-rank op lists of the ATP linears and blocks.
 //
-// Chunk pipeline (§4.1 Fig. 7; reading G14): the rows of
-// every activation are cut into `c` chunks; each linear ("stage") is emitted
-// breadth-first over the chunks — GEMM(k), all-reduce(k) — on two streams, and
-// chunk k of stage s+1 waits only for the all-reduce of chunk k of stage s.
-// Host enqueue order is the op order below, i.e. each all-reduce is submitted
-// before the GEMM it should overlap (the reason for the paper's
-// CUDA_DEVICE_MAX_CONNECTIONS=1).
+// Chunk-based overlapping (§4.1 Fig. 7; reading G14): the
+// token rows are cut into `c` chunks and the all-reduce of chunk k overlaps the
+// computation of the later chunks.  A "stage" is one linear (GEMM + grouped
+// all-reduce).  Three ways to emit a stage:
 //
-// Backward (§4.2): per linear, the dX GEMMs are chunked and each
-// chunk's all-reduce overlaps the next chunk; the dW GEMM runs once over all
-// T rows right after that linear's dX chunks, overlapping their all-reduces
-// (dW feeds no collective, so chunking it would only add fp32 read-modify-write
-// traffic).
+//  * no communication (the reducing mesh dimension has size 1): one GEMM over
+//    all T rows with the following elementwise step fused into its epilogue;
+//
+//  * SIGNALLED (default when the chunk rows are a multiple of the tile rows):
+//    ONE persistent GEMM over all T rows whose tiles run chunk by chunk; each
+//    CTA-tile bumps a per-chunk counter once its output is globally visible.
+//    The communication stream waits for chunk k's counter (cuStreamWaitValue32),
+//    all-reduces chunk k and applies chunk k's post-all-reduce elementwise step
+//    (GeLU / residual / core / dGeLU).  So chunk k's all-reduce overlaps the
+//    GEMM's later chunks without cutting the GEMM into c small launches that
+//    cannot fill 148 SMs; the next stage's GEMM starts once the last chunk is
+//    reduced.  B200-native replacement for the paper's per-chunk kernel calls;
+//
+//  * PER-CHUNK fallback: c GEMM launches (breadth-first over chunks) on the
+//    compute stream with event hand-off to the communication stream; chunk k
+//    of stage s+1 waits only on chunk k's all-reduce of stage s.
+//
+// Backward (§4.2): the dX GEMM is chunked (signalled) and each
+// linear's dW GEMM over all T rows is enqueued right after it, before the
+// communication ops, so it runs while the dX chunks are all-reduced (dW feeds
+// no collective; chunking it would only add fp32 read-modify-write traffic).
+//
+// Host enqueue order = op order below: every all-reduce is submitted before
+// the compute that should overlap it, and every wait refers to an op submitted
+// earlier, which keeps the order valid for CUDA_DEVICE_MAX_CONNECTIONS=1
+// (P:345).
 //
 // Bias placement (reading G16): a bias is added exactly once per reduction
-// group — fused into the GEMM epilogue of the coordinate-0 rank before the
-// all-reduce, or unconditionally when the reducing dimension has size 1.
-// Elementwise steps that follow an all-reduce (GeLU, dGeLU, residual, core)
-// are separate HBM-bound kernels; when the reducing dimension has size 1 they
-// are fused into the GEMM epilogue instead (EPI_RESID / EPI_BIAS_GELU /
-// EPI_DGELU).
+// group — in the GEMM epilogue of the coordinate-0 rank before the all-reduce,
+// or unconditionally when the reducing dimension has size 1.
 #include <string>
 #include <vector>
 
@@ -38,14 +52,17 @@ inline const char* cptr(const void* p, int64_t off_elems) {
 }
 inline char* mptr(void* p, int64_t off_elems) { return static_cast<char*>(p) + off_elems * 2; }
 
+using EwList = std::vector<EwDesc>;
+
 struct Builder {
   Sched s;
   RankView rv;
   std::string err;
   int chunks = 1;
   int64_t T = 0, Mc = 0;
-  std::vector<int> pend;                // per chunk: event the next stage's chunk must wait on
-  std::vector<std::vector<EwDesc>> def;  // per chunk: deferred prologue ops
+  int next_slot = 0;
+  std::vector<int> pend;    // per chunk: event the next compute op of that chunk must wait on
+  std::vector<EwList> def;  // per chunk: deferred elementwise ops (per-chunk mode)
 
   Builder(const RankView& v, int64_t rows, int c) : rv(v), chunks(c), T(rows), Mc(rows / c) {
     pend.assign(c, -1);
@@ -61,10 +78,13 @@ struct Builder {
     return o;
   }
   static void add_wait(Op& o, int e) {
-    if (e >= 0) o.waits[o.n_waits++] = e;
+    if (e < 0) return;
+    for (int i = 0; i < o.n_waits; ++i)
+      if (o.waits[i] == e) return;
+    o.waits[o.n_waits++] = e;
   }
-  // Emit chunk k's pending wait + deferred prologue ops on the compute stream.
-  // Returns the wait that is still unconsumed (if no prologue op carried it).
+  // Chunk k's pending wait + deferred ops on the compute stream; returns the
+  // wait still unconsumed (no deferred op carried it).
   int prologue(int k) {
     int w = pend[k];
     pend[k] = -1;
@@ -77,10 +97,20 @@ struct Builder {
     def[k].clear();
     return w;
   }
-  bool gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn, int64_t M, int64_t N,
-            int64_t K, int epi, const EpiParams& ep, int wait, int record, int bn = 0) {
+  // Every chunk's prologue; returns the distinct unconsumed waits.
+  std::vector<int> prologue_all() {
+    std::vector<int> w;
+    for (int k = 0; k < chunks; ++k) {
+      int e = prologue(k);
+      bool seen = false;
+      for (int x : w) seen |= (x == e);
+      if (e >= 0 && !seen) w.push_back(e);
+    }
+    return w;
+  }
+  Op* gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn, int64_t M, int64_t N,
+           int64_t K, int epi, const EpiParams& ep, const std::vector<int>& waits, int record) {
     Op& o = push(OP_GEMM, 0);
-    o.g.bn = bn;
     o.g.max_ctas = rv.gemm_ctas;
     o.g.epi = epi;
     o.g.ep = ep;
@@ -88,11 +118,11 @@ struct Builder {
                                  static_cast<int>(K));
     if (m) {
       err = m;
-      return false;
+      return nullptr;
     }
-    add_wait(o, wait);
+    for (int w : waits) add_wait(o, w);
     o.record = record;
-    return true;
+    return &o;
   }
   void allreduce(int dim, void* ptr, int64_t count, int wait, int record) {
     Op& o = push(OP_AR, 1);
@@ -102,83 +132,93 @@ struct Builder {
     add_wait(o, wait);
     o.record = record;
   }
-  void ew_now(const EwDesc& e, int wait = -1) {
-    Op& o = push(OP_EW, 0);
+  void ew(const EwDesc& e, int stream, int wait = -1) {
+    Op& o = push(OP_EW, stream);
     o.e = e;
     add_wait(o, wait);
   }
   int dim_size(int dim) const { return dim == 1 ? rv.d1 : rv.d2; }
   bool coord0(int dim) const { return (dim == 1 ? rv.i1 : rv.i2) == 0; }
 
-  // One forward linear stage over all chunks: out_k = in_k W (+bias), then the
-  // grouped all-reduce over `dim` (skipped when that dimension has size 1).
-  // `fused` = epilogue to use when no all-reduce follows.  `after_ar(k)` =
-  // deferred elementwise ops of chunk k once the sum is available.
-  template <class AfterAR, class FusedEp>
-  bool fwd_stage(int dim, const void* in, int64_t in_w, const void* w, int64_t out_w, const void* bias, void* out,
-                 int fused_epi, FusedEp fused_ep, AfterAR after_ar) {
+  // One linear stage.  out[T, out_w] = in[T, in_w] * W (+bias), B given as
+  // W^T-free storage (b_mn) — i.e. forward: W stored [in_w, out_w]; backward
+  // dX: W stored [out_w(x_w), in_w(dy_w)] read K-major.  `after_ar(k, rows0,
+  // nrows)` returns the elementwise ops that must follow the all-reduce of the
+  // given row range; `fused(ep)` configures the epilogue used when no
+  // all-reduce follows (epi kind `fused_epi`); `extra()` emits compute-stream
+  // work (the dW GEMMs) that should overlap this stage's communication.
+  template <class AfterAR, class Fused, class Extra>
+  bool stage(int dim, const void* in, int64_t in_w, const void* w, int64_t ldw, bool b_mn, int64_t out_w, const void* bias,
+             void* out, int fused_epi, Fused fused, AfterAR after_ar, Extra extra) {
     const bool comm = dim_size(dim) > 1;
+    if (!comm) {
+      // ---- no all-reduce: one full-T GEMM, elementwise step fused into its epilogue
+      std::vector<int> waits = prologue_all();
+      EpiParams ep;
+      ep.C = out;
+      ep.ldc = out_w;
+      ep.bias = bias;
+      int epi = fused_epi;
+      fused(ep, 0, T);
+      if (!gemm(in, in_w, false, w, ldw, b_mn, T, out_w, in_w, epi, ep, waits, -1)) return false;
+      if (!extra()) return false;
+      return true;
+    }
+    const void* bias_here = coord0(dim) ? bias : nullptr;
+    int bn = 0, cg = 0;
+    gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
+    if (rv.signalled && rv.sig_buf != nullptr && chunks > 1 && Mc % (128 * cg) == 0 &&
+        next_slot + chunks <= kSigSlots) {
+      // ---- signalled stage: one GEMM over all T rows, per-chunk counters
+      std::vector<int> waits = prologue_all();
+      EpiParams ep;
+      ep.C = out;
+      ep.ldc = out_w;
+      ep.bias = bias_here;
+      Op* g = gemm(in, in_w, false, w, ldw, b_mn, T, out_w, in_w, EPI_BF16, ep, waits, -1);
+      if (!g) return false;
+      const int slot0 = next_slot;
+      next_slot += chunks;
+      g->g.sig = rv.sig_buf + slot0;
+      g->g.sig_rows = static_cast<int>(Mc);
+      const uint32_t per_chunk = static_cast<uint32_t>((Mc / 128) * ((out_w + g->g.bn - 1) / g->g.bn));
+      if (!extra()) return false;
+      for (int k = 0; k < chunks; ++k) {
+        Op& wsig = push(OP_WAITSIG, 1);
+        wsig.sig_slot = slot0 + k;
+        wsig.sig_inc = per_chunk;
+        allreduce(dim, mptr(out, k * Mc * out_w), Mc * out_w, -1, -1);
+        for (const EwDesc& e : after_ar(k, k * Mc, Mc)) ew(e, 1);
+      }
+      const int last = ev();
+      s.ops.back().record = last;
+      for (int k = 0; k < chunks; ++k) pend[k] = last;
+      return true;
+    }
+    // ---- per-chunk stage: c GEMM launches, event hand-off per chunk
     for (int k = 0; k < chunks; ++k) {
       const int wait = prologue(k);
       EpiParams ep;
-      int epi = EPI_BF16;
       ep.C = mptr(out, k * Mc * out_w);
       ep.ldc = out_w;
-      if (comm) {
-        ep.bias = coord0(dim) ? static_cast<const bf16*>(bias) : nullptr;
-      } else {
-        ep.bias = static_cast<const bf16*>(bias);
-        epi = fused_epi;
-        fused_ep(k, ep);
-      }
-      const int e = comm ? ev() : -1;
-      if (!gemm(cptr(in, k * Mc * in_w), in_w, false, w, out_w, true, Mc, out_w, in_w, epi, ep, wait, e))
+      ep.bias = bias_here;
+      const int e = ev();
+      if (!gemm(cptr(in, k * Mc * in_w), in_w, false, w, ldw, b_mn, Mc, out_w, in_w, EPI_BF16, ep, {wait}, e))
         return false;
-      if (comm) {
-        const int r = ev();
-        allreduce(dim, ep.C, Mc * out_w, e, r);
-        pend[k] = r;
-        after_ar(k);
-      }
+      const int r = ev();
+      allreduce(dim, ep.C, Mc * out_w, e, r);
+      pend[k] = r;
+      for (const EwDesc& d : after_ar(k, k * Mc, Mc)) def[k].push_back(d);
     }
-    return true;
+    return extra();
   }
 
-  // One backward linear stage: dx_k = dy_k W^T then all-reduce over `dim`
-  // (the conjugate dimension); dW = X^T dY over all T rows afterwards.
-  template <class AfterAR, class FusedEp>
-  bool bwd_stage(int dim, const void* dy, int64_t dy_w, const void* w, int64_t x_w, void* dx, int fused_epi,
-                 FusedEp fused_ep, AfterAR after_ar) {
-    const bool comm = dim_size(dim) > 1;
-    for (int k = 0; k < chunks; ++k) {
-      const int wait = prologue(k);
-      EpiParams ep;
-      int epi = EPI_BF16;
-      ep.C = mptr(dx, k * Mc * x_w);
-      ep.ldc = x_w;
-      if (!comm) {
-        epi = fused_epi;
-        fused_ep(k, ep);
-      }
-      const int e = comm ? ev() : -1;
-      // dx_k [Mc, x_w] = dy_k [Mc, dy_w] * W[x_w, dy_w]^T: A K-major, B = W stored [x_w, dy_w] K-major
-      if (!gemm(cptr(dy, k * Mc * dy_w), dy_w, false, w, dy_w, false, Mc, x_w, dy_w, epi, ep, wait, e))
-        return false;
-      if (comm) {
-        const int r = ev();
-        allreduce(dim, ep.C, Mc * x_w, e, r);
-        pend[k] = r;
-        after_ar(k);
-      }
-    }
-    return true;
-  }
   // dW[x_w, dy_w] (fp32) = X[T, x_w]^T dY[T, dy_w]  (both MN-major), + dbias = colsum(dY)
   bool dw(const void* x, int64_t x_w, const void* dy, int64_t dy_w, float* dwp, float* dbias) {
     EpiParams ep;
     ep.C = dwp;
     ep.ldc = dy_w;
-    if (dwp != nullptr && !gemm(x, x_w, true, dy, dy_w, true, x_w, dy_w, T, EPI_F32, ep, -1, -1)) return false;
+    if (dwp != nullptr && !gemm(x, x_w, true, dy, dy_w, true, x_w, dy_w, T, EPI_F32, ep, {}, -1)) return false;
     if (dbias != nullptr) {
       EwDesc e;
       e.kind = EW_COLSUM;
@@ -186,17 +226,15 @@ struct Builder {
       e.a = dy;
       e.rows = T;
       e.cols = dy_w;
-      ew_now(e);
+      ew(e, 0);
     }
     return true;
   }
-  void flush() {
-    for (int k = 0; k < chunks; ++k) {
-      int w = prologue(k);
-      (void)w;  // a trailing all-reduce with no consumer is joined by the executor
-    }
-  }
-  static EwDesc ew(int kind, void* out, const void* a, int64_t rows, int64_t cols, int heads = 1) {
+  // Remaining deferred work; a trailing all-reduce with no consumer is joined
+  // by the executor.
+  void flush() { prologue_all(); }
+
+  static EwDesc ewd(int kind, void* out, const void* a, int64_t rows, int64_t cols, int heads = 1) {
     EwDesc e;
     e.kind = kind;
     e.out = out;
@@ -208,8 +246,9 @@ struct Builder {
   }
 };
 
-auto no_fuse = [](int, EpiParams&) {};
-auto no_after = [](int) {};
+auto no_fuse = [](EpiParams&, int64_t, int64_t) {};
+auto no_after = [](int, int64_t, int64_t) { return EwList{}; };
+auto no_extra = []() { return true; };
 
 }  // namespace
 
@@ -220,7 +259,7 @@ int build_linear_fwd(const RankView& rv, bool colfirst, const LinearFwd& a, int6
   const int dim = colfirst ? 2 : 1;
   const int64_t in_w = colfirst ? K / rv.d2 : K / rv.d1;
   const int64_t out_w = colfirst ? N / rv.d1 : N / rv.d2;
-  if (!b.fwd_stage(dim, a.x, in_w, a.w, out_w, a.bias, a.y, EPI_BF16, no_fuse, no_after)) {
+  if (!b.stage(dim, a.x, in_w, a.w, out_w, true, out_w, a.bias, a.y, EPI_BF16, no_fuse, no_after, no_extra)) {
     set_error(b.err);
     return 2;
   }
@@ -235,8 +274,9 @@ int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int6
   const int dim = colfirst ? 1 : 2;  // conjugate dimension ("f3 ... on the second dimension in backward")
   const int64_t x_w = colfirst ? K / rv.d2 : K / rv.d1;
   const int64_t dy_w = colfirst ? N / rv.d1 : N / rv.d2;
-  if (!b.bwd_stage(dim, a.dy, dy_w, a.w, x_w, a.dx, EPI_BF16, no_fuse, no_after) ||
-      !b.dw(a.x, x_w, a.dy, dy_w, a.dw, a.dbias)) {
+  // dx [M, x_w] = dy [M, dy_w] * W[x_w, dy_w]^T: B = W stored [x_w, dy_w], K-major
+  if (!b.stage(dim, a.dy, dy_w, a.w, dy_w, false, x_w, nullptr, a.dx, EPI_BF16, no_fuse, no_after,
+               [&]() { return b.dw(a.x, x_w, a.dy, dy_w, a.dw, a.dbias); })) {
     set_error(b.err);
     return 2;
   }
@@ -249,109 +289,119 @@ int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int6
 int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
                 int chunks, Sched& out) {
   Builder b(rv, T, chunks);
-  const int64_t Mc = T / chunks;
-  const int64_t hc = h / rv.d2;       // activation column block
-  const int64_t h1 = h / rv.d1;       // ctx width / Out input
-  const int64_t q1 = 3 * h / rv.d1;   // local QKV width
-  const int64_t F1 = F / rv.d1;       // local FFN width
-  const int64_t hl = heads / rv.d1;   // local heads
-  const int d1 = rv.d1, d2 = rv.d2;
-  auto rowsof = [&](const void* base, int k, int64_t w) { return cptr(base, k * Mc * w); };
-  auto mrowsof = [&](void* base, int k, int64_t w) { return mptr(base, k * Mc * w); };
+  const int64_t hc = h / rv.d2;      // activation column block
+  const int64_t h1 = h / rv.d1;      // ctx width / Out input
+  const int64_t q1 = 3 * h / rv.d1;  // local QKV width
+  const int64_t F1 = F / rv.d1;      // local FFN width
+  const int hl = static_cast<int>(heads / rv.d1);  // local heads
+  auto rows = [](const void* base, int64_t r0, int64_t w) { return cptr(base, r0 * w); };
+  auto mrows = [](void* base, int64_t r0, int64_t w) { return mptr(base, r0 * w); };
+  auto aux = [](const void* p) { return static_cast<const void*>(p); };
   auto fail = [&]() {
     set_error(b.err);
     return 2;
   };
+  using E = Builder;
 
   if (p.attn_fwd) {
     const atp_attn_fwd_args& a = *p.attn_fwd;
-    // F3/F4: QKV column-first, all-reduce on dim 2 (f1); F5 core deferred
-    if (!b.fwd_stage(2, a.x, hc, a.wqkv, q1, a.bqkv, a.qkv, EPI_BF16, no_fuse, no_after)) return fail();
-    for (int k = 0; k < chunks; ++k)
-      b.def[k].push_back(Builder::ew(EW_CORE_FWD, mrowsof(a.ctx, k, h1), rowsof(a.qkv, k, q1), Mc, h1, (int)hl));
+    // F3/F4: QKV column-first, all-reduce on dim 2 (f1); F5 core after the sum
+    if (!b.stage(2, a.x, hc, a.wqkv, q1, true, q1, a.bqkv, a.qkv, EPI_BF16, no_fuse,
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_CORE_FWD, mrows(a.ctx, r0, h1), rows(a.qkv, r0, q1), n, h1, hl)};
+                 },
+                 [&]() {
+                   if (rv.d2 == 1) b.ew(E::ewd(EW_CORE_FWD, a.ctx, a.qkv, T, h1, hl), 0);
+                   return true;
+                 }))
+      return fail();
     // F6/F7: Out row-first, all-reduce on dim 1 (f2), residual Y1 = X + .
-    if (!b.fwd_stage(
-            1, a.ctx, h1, a.wo, hc, a.bo, a.y, EPI_RESID,
-            [&](int k, EpiParams& ep) {
-              ep.aux = static_cast<const bf16*>(static_cast<const void*>(rowsof(a.x, k, hc)));
-              ep.ldaux = hc;
-            },
-            [&](int k) { b.def[k].push_back(Builder::ew(EW_ADD, mrowsof(a.y, k, hc), rowsof(a.x, k, hc), Mc, hc)); }))
+    if (!b.stage(1, a.ctx, h1, a.wo, hc, true, hc, a.bo, a.y, EPI_RESID,
+                 [&](EpiParams& ep, int64_t, int64_t) {
+                   ep.aux = aux(a.x);
+                   ep.ldaux = hc;
+                 },
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_ADD, mrows(a.y, r0, hc), rows(a.x, r0, hc), n, hc)};
+                 },
+                 no_extra))
       return fail();
   }
   if (p.mlp_fwd) {
     const atp_mlp_fwd_args& a = *p.mlp_fwd;
     // F8/F9/F10: FC1 column-first, all-reduce on dim 2 (f3), U saved, H = GeLU(U)
-    if (!b.fwd_stage(
-            2, a.x, hc, a.w1, F1, a.b1, a.u, EPI_BIAS_GELU,
-            [&](int k, EpiParams& ep) {
-              ep.C2 = mrowsof(a.h_act, k, F1);
-              ep.ldc2 = F1;
-            },
-            [&](int k) {
-              b.def[k].push_back(Builder::ew(EW_GELU, mrowsof(a.h_act, k, F1), rowsof(a.u, k, F1), Mc, F1));
-            }))
+    if (!b.stage(2, a.x, hc, a.w1, F1, true, F1, a.b1, a.u, EPI_BIAS_GELU,
+                 [&](EpiParams& ep, int64_t, int64_t) {
+                   ep.C2 = a.h_act;
+                   ep.ldc2 = F1;
+                 },
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_GELU, mrows(a.h_act, r0, F1), rows(a.u, r0, F1), n, F1)};
+                 },
+                 no_extra))
       return fail();
     // F11/F12: FC2 row-first, all-reduce on dim 1 (f4), Z = X + .
-    if (!b.fwd_stage(
-            1, a.h_act, F1, a.w2, hc, a.b2, a.z, EPI_RESID,
-            [&](int k, EpiParams& ep) {
-              ep.aux = static_cast<const bf16*>(static_cast<const void*>(rowsof(a.x, k, hc)));
-              ep.ldaux = hc;
-            },
-            [&](int k) { b.def[k].push_back(Builder::ew(EW_ADD, mrowsof(a.z, k, hc), rowsof(a.x, k, hc), Mc, hc)); }))
+    if (!b.stage(1, a.h_act, F1, a.w2, hc, true, hc, a.b2, a.z, EPI_RESID,
+                 [&](EpiParams& ep, int64_t, int64_t) {
+                   ep.aux = aux(a.x);
+                   ep.ldaux = hc;
+                 },
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_ADD, mrows(a.z, r0, hc), rows(a.x, r0, hc), n, hc)};
+                 },
+                 no_extra))
       return fail();
   }
   if (p.mlp_bwd) {
     const atp_mlp_bwd_args& a = *p.mlp_bwd;
-    // B1: dH = dZ W2^T, all-reduce on dim 2 (conjugate of f4); dU = dH * GeLU'(U)
-    if (!b.bwd_stage(
-            2, a.dz, hc, a.w2, F1, a.ws_dh, EPI_DGELU,
-            [&](int k, EpiParams& ep) {
-              ep.aux = static_cast<const bf16*>(static_cast<const void*>(rowsof(a.u, k, F1)));
-              ep.ldaux = F1;
-            },
-            [&](int k) {
-              b.def[k].push_back(Builder::ew(EW_DGELU, mrowsof(a.ws_dh, k, F1), rowsof(a.u, k, F1), Mc, F1));
-            }))
+    // B1: dH = dZ W2^T, all-reduce on dim 2 (conjugate of f4); dU = dH * GeLU'(U); || dW2, db2
+    if (!b.stage(2, a.dz, hc, a.w2, hc, false, F1, nullptr, a.ws_dh, EPI_DGELU,
+                 [&](EpiParams& ep, int64_t, int64_t) {
+                   ep.aux = aux(a.u);
+                   ep.ldaux = F1;
+                 },
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_DGELU, mrows(a.ws_dh, r0, F1), rows(a.u, r0, F1), n, F1)};
+                 },
+                 [&]() { return b.dw(a.h_act, F1, a.dz, hc, a.dw2, a.db2); }))
       return fail();
-    if (!b.dw(a.h_act, F1, a.dz, hc, a.dw2, a.db2)) return fail();
-    // B3: dX1 = dU W1^T, all-reduce on dim 1 (conjugate of f3); dX1 += dZ (residual)
-    if (!b.bwd_stage(
-            1, a.ws_dh, F1, a.w1, hc, a.dx, EPI_RESID,
-            [&](int k, EpiParams& ep) {
-              ep.aux = static_cast<const bf16*>(static_cast<const void*>(rowsof(a.dz, k, hc)));
-              ep.ldaux = hc;
-            },
-            [&](int k) { b.def[k].push_back(Builder::ew(EW_ADD, mrowsof(a.dx, k, hc), rowsof(a.dz, k, hc), Mc, hc)); }))
+    // B3: dX1 = dU W1^T, all-reduce on dim 1 (conjugate of f3); dX1 += dZ; || dW1, db1
+    if (!b.stage(1, a.ws_dh, F1, a.w1, F1, false, hc, nullptr, a.dx, EPI_RESID,
+                 [&](EpiParams& ep, int64_t, int64_t) {
+                   ep.aux = aux(a.dz);
+                   ep.ldaux = hc;
+                 },
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_ADD, mrows(a.dx, r0, hc), rows(a.dz, r0, hc), n, hc)};
+                 },
+                 [&]() { return b.dw(a.x, hc, a.ws_dh, F1, a.dw1, a.db1); }))
       return fail();
-    // dW1 needs every chunk's dU, which the B3 prologues completed
-    if (!b.dw(a.x, hc, a.ws_dh, F1, a.dw1, a.db1)) return fail();
   }
   if (p.attn_bwd) {
     const atp_attn_bwd_args& a = *p.attn_bwd;
-    // dbo / dWo need the complete dY: flush its deferred residuals first
-    // (they are the prologue of B4's chunks anyway, emitted in chunk order)
-    // B4: dctx = dY Wo^T, all-reduce on dim 2 (conjugate of f2); dQKV = expand(dctx)
-    if (!b.bwd_stage(2, a.dy, hc, a.wo, h1, a.ws_dctx, EPI_BF16, no_fuse, no_after)) return fail();
-    for (int k = 0; k < chunks; ++k)
-      b.def[k].push_back(
-          Builder::ew(EW_CORE_BWD, mrowsof(a.ws_dqkv, k, q1), rowsof(a.ws_dctx, k, h1), Mc, h1, (int)hl));
-    if (!b.dw(a.ctx, h1, a.dy, hc, a.dwo, a.dbo)) return fail();
-    // B6: dX = dQKV Wqkv^T, all-reduce on dim 1 (conjugate of f1); dX += dY (residual)
-    if (!b.bwd_stage(
-            1, a.ws_dqkv, q1, a.wqkv, hc, a.dx, EPI_RESID,
-            [&](int k, EpiParams& ep) {
-              ep.aux = static_cast<const bf16*>(static_cast<const void*>(rowsof(a.dy, k, hc)));
-              ep.ldaux = hc;
-            },
-            [&](int k) { b.def[k].push_back(Builder::ew(EW_ADD, mrowsof(a.dx, k, hc), rowsof(a.dy, k, hc), Mc, hc)); }))
+    // B4/B5: dctx = dY Wo^T, all-reduce on dim 2 (conjugate of f2); dQKV = expand(dctx); || dWo, dbo
+    if (!b.stage(2, a.dy, hc, a.wo, hc, false, h1, nullptr, a.ws_dctx, EPI_BF16, no_fuse,
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_CORE_BWD, mrows(a.ws_dqkv, r0, q1), rows(a.ws_dctx, r0, h1), n, h1, hl)};
+                 },
+                 [&]() {
+                   if (rv.d2 == 1) b.ew(E::ewd(EW_CORE_BWD, a.ws_dqkv, a.ws_dctx, T, h1, hl), 0);
+                   return b.dw(a.ctx, h1, a.dy, hc, a.dwo, a.dbo);
+                 }))
       return fail();
-    if (!b.dw(a.x, hc, a.ws_dqkv, q1, a.dwqkv, a.dbqkv)) return fail();
+    // B6: dX = dQKV Wqkv^T, all-reduce on dim 1 (conjugate of f1); dX += dY; || dWqkv, dbqkv
+    if (!b.stage(1, a.ws_dqkv, q1, a.wqkv, q1, false, hc, nullptr, a.dx, EPI_RESID,
+                 [&](EpiParams& ep, int64_t, int64_t) {
+                   ep.aux = aux(a.dy);
+                   ep.ldaux = hc;
+                 },
+                 [&](int, int64_t r0, int64_t n) {
+                   return EwList{E::ewd(EW_ADD, mrows(a.dx, r0, hc), rows(a.dy, r0, hc), n, hc)};
+                 },
+                 [&]() { return b.dw(a.x, hc, a.ws_dqkv, q1, a.dwqkv, a.dbqkv); }))
+      return fail();
   }
   b.flush();
-  (void)d1;
-  (void)d2;
   out = std::move(b.s);
   return 0;
 }

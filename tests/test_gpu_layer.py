@@ -77,6 +77,23 @@ def test_layer_every_mesh(d1, d2, chunks):
     check_replicas(bufs, d1, d2)
 
 
+@pytest.mark.parametrize("d1,d2", [(2, 2), (4, 2), (2, 4), (8, 1), (1, 8)])
+def test_layer_signalled_stages(d1, d2):
+    """T/chunks = 256 rows: every communicating stage runs as ONE GEMM with
+    per-chunk completion counters gating the all-reduces (signalled stages)."""
+    T, h, F, heads, chunks, seed = 1024, 512, 2048, 8, 4, 23
+    g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, d1, d2, chunks, seed)
+    bufs = run_gpu_layer(d1, d2, T, h, F, heads, chunks, seed)
+    compare(bufs, fw, bw, d1, d2)
+    check_replicas(bufs, d1, d2)
+    # a second call reuses the counters (cumulative targets) and must agree bit for bit
+    bufs2 = run_gpu_layer(d1, d2, T, h, F, heads, chunks, seed)
+    import torch
+    for b1, b2 in zip(bufs, bufs2):
+        for k in ("z", "dx", "dw1", "dwqkv"):
+            assert torch.equal(b1[k], b2[k]), k
+
+
 def test_cfg1_mlp_2x2():
     """BASELINE.json configs[0]: h=64, ffn=256, tokens=32 on a 2x2 mesh."""
     import torch
