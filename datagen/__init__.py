@@ -121,8 +121,9 @@ def _to_i64(v: int) -> int:
 
 
 def torch_block(name: str, shape_global, row0: int, nrows: int, col0: int, ncols: int,
-                device, seed: int = BASE_SEED, scale: float | None = None):
-    """bf16 torch tensor equal to ``tensor(name, shape_global)[row0:row0+nrows, col0:col0+ncols]``."""
+                device, seed: int = BASE_SEED, scale: float | None = None, bf16: bool = True):
+    """Torch tensor equal to ``tensor(name, shape_global, bf16=bf16)[row0:row0+nrows, col0:col0+ncols]``
+    (bf16 dtype when ``bf16``, else the unrounded float32 values)."""
     import torch
 
     tid = TENSOR_IDS[name]
@@ -132,7 +133,7 @@ def torch_block(name: str, shape_global, row0: int, nrows: int, col0: int, ncols
     else:
         n_cols = shape_global[1]
     key = _to_i64(seed ^ (tid << 40))
-    out = torch.empty((nrows, ncols), dtype=torch.bfloat16, device=device)
+    out = torch.empty((nrows, ncols), dtype=torch.bfloat16 if bf16 else torch.float32, device=device)
     step = max(1, (1 << 24) // max(ncols, 1))
     c = torch.arange(col0, col0 + ncols, device=device, dtype=torch.int64).view(1, -1)
     for r0 in range(0, nrows, step):
@@ -145,7 +146,7 @@ def torch_block(name: str, shape_global, row0: int, nrows: int, col0: int, ncols
         z = z ^ _lsr(z, 31)
         u = _lsr(z, 40).to(torch.float64) / float(1 << 24)
         v = (sc * (2.0 * u - 1.0)).to(torch.float32)
-        out[r0:r0 + rr] = v.to(torch.bfloat16)  # torch's f32->bf16 cast is RNE
+        out[r0:r0 + rr] = v.to(torch.bfloat16) if bf16 else v  # torch's f32->bf16 cast is RNE
     return out
 
 

@@ -54,7 +54,12 @@ typedef enum {
   ATP_ERR_UNSUPPORTED = 6  /* feature not built / not available              */
 } atp_status;
 
-typedef enum { ATP_BF16 = 0 } atp_dtype;
+/* ATP_BF16: the product path (bf16 storage, tcgen05 GEMMs, fp32 accumulation,
+ * bf16 all-reduce).  ATP_FP32: check mode — every activation, weight, bias and
+ * workspace buffer is fp32, GEMMs are CUDA-core fp32 FMA, all-reduces fp32;
+ * same schedule, so the sharded pipeline can be checked against the fp64
+ * oracle at <= 1e-4 (north_star). */
+typedef enum { ATP_BF16 = 0, ATP_FP32 = 1 } atp_dtype;
 
 typedef struct atp_mesh atp_mesh; /* opaque */
 

@@ -15,6 +15,7 @@ ATP_OK, ATP_ERR_INVALID, ATP_ERR_SHAPE, ATP_ERR_CUDA, ATP_ERR_NCCL, ATP_ERR_EMPT
 STATUS_NAMES = ["ATP_OK", "ATP_ERR_INVALID", "ATP_ERR_SHAPE", "ATP_ERR_CUDA", "ATP_ERR_NCCL", "ATP_ERR_EMPTY",
                 "ATP_ERR_UNSUPPORTED"]
 ATP_BF16 = 0
+ATP_FP32 = 1
 ATP_CORE_SUM_QKV = 0
 ATP_MAX_HCM_LAYERS = 8
 ATP_MAX_PLAN = 64

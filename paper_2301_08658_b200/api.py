@@ -118,7 +118,7 @@ def atp_linear_fwd(mesh: Mesh, colfirst: bool, per_rank: list[dict], M: int, K: 
     a = _arr(_abi.LinearFwdArgs, [_abi.LinearFwdArgs(d["x"].data_ptr(), d["w"].data_ptr(), _ptr(d.get("bias")),
                                                      d["y"].data_ptr()) for d in per_rank])
     f = lib().atp_linear_colfirst_fwd if colfirst else lib().atp_linear_rowfirst_fwd
-    check(f(mesh.handle, a, M, K, N, chunks, _abi.ATP_BF16, _stream(stream)))
+    check(f(mesh.handle, a, M, K, N, chunks, _dt(per_rank[0]["x"]), _stream(stream)))
 
 
 def atp_linear_bwd(mesh: Mesh, colfirst: bool, per_rank: list[dict], M: int, K: int, N: int, chunks: int = 1,
@@ -128,7 +128,7 @@ def atp_linear_bwd(mesh: Mesh, colfirst: bool, per_rank: list[dict], M: int, K: 
                                                      d["dx"].data_ptr(), _ptr(d.get("dw")), _ptr(d.get("dbias")))
                                   for d in per_rank])
     f = lib().atp_linear_colfirst_bwd if colfirst else lib().atp_linear_rowfirst_bwd
-    check(f(mesh.handle, a, M, K, N, chunks, _abi.ATP_BF16, _stream(stream)))
+    check(f(mesh.handle, a, M, K, N, chunks, _dt(per_rank[0]["x"]), _stream(stream)))
 
 
 # ------------------------------------------------------------------ layer buffers
@@ -154,23 +154,30 @@ def _attn_bwd(b):
                             _ptr(b["dwo"]), _ptr(b["dbo"]), b["ws_dctx"].data_ptr(), b["ws_dqkv"].data_ptr())
 
 
+def _dt(t) -> int:
+    import torch
+
+    return _abi.ATP_FP32 if t.dtype == torch.float32 else _abi.ATP_BF16
+
+
 def alloc_layer_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, device, seed: int, with_bias: bool = True,
-                     inputs: bool = True) -> dict:
+                     inputs: bool = True, fp32: bool = False) -> dict:
     """Allocate one rank's layer buffers; fill inputs/weights from the seeded
-    counter-based generator (datagen) directly on the device."""
+    counter-based generator (datagen) directly on the device.  fp32=True:
+    the ATP_FP32 check mode (fp32 storage, unrounded fp32 inputs)."""
     import torch
     import datagen
 
     w = layout.local_widths(d1, d2, h, F)
     hc, h1, q1, F1 = w["hc"], w["h1"], w["q1"], w["F1"]
-    bf, f32 = torch.bfloat16, torch.float32
+    bf, f32 = (torch.float32 if fp32 else torch.bfloat16), torch.float32
     box = layout.shard_boxes(d1, d2, rank, T, h, F)
     shapes = datagen.layer_shapes(T, h, F)
     b = {}
     for name in ("x", "dz", "wqkv", "wo", "w1", "w2") + (("bqkv", "bo", "b1", "b2") if with_bias else ()):
         r0, nr, c0, nc = box[name]
         if inputs:
-            t = datagen.torch_block(name, shapes[name], r0, nr, c0, nc, device, seed=seed)
+            t = datagen.torch_block(name, shapes[name], r0, nr, c0, nc, device, seed=seed, bf16=not fp32)
         else:
             t = torch.empty((nr, nc), dtype=bf, device=device)
         b[name] = t.reshape(-1) if name.startswith("b") else t
@@ -184,24 +191,24 @@ def alloc_layer_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, device
 
 def atp_attn_proj_fwd(mesh, bufs, T, h, heads, chunks=1, stream=None):
     a = _arr(_abi.AttnFwdArgs, [_attn_fwd(b) for b in bufs])
-    check(lib().atp_attn_proj_fwd(mesh.handle, a, T, h, heads, chunks, _abi.ATP_CORE_SUM_QKV, _abi.ATP_BF16,
+    check(lib().atp_attn_proj_fwd(mesh.handle, a, T, h, heads, chunks, _abi.ATP_CORE_SUM_QKV, _dt(bufs[0]["x"]),
                                   _stream(stream)))
 
 
 def atp_attn_proj_bwd(mesh, bufs, T, h, heads, chunks=1, stream=None):
     a = _arr(_abi.AttnBwdArgs, [_attn_bwd(b) for b in bufs])
-    check(lib().atp_attn_proj_bwd(mesh.handle, a, T, h, heads, chunks, _abi.ATP_CORE_SUM_QKV, _abi.ATP_BF16,
+    check(lib().atp_attn_proj_bwd(mesh.handle, a, T, h, heads, chunks, _abi.ATP_CORE_SUM_QKV, _dt(bufs[0]["x"]),
                                   _stream(stream)))
 
 
 def atp_mlp_fwd(mesh, bufs, T, h, F, chunks=1, stream=None):
     a = _arr(_abi.MlpFwdArgs, [_mlp_fwd(b) for b in bufs])
-    check(lib().atp_mlp_fwd(mesh.handle, a, T, h, F, chunks, _abi.ATP_BF16, _stream(stream)))
+    check(lib().atp_mlp_fwd(mesh.handle, a, T, h, F, chunks, _dt(bufs[0]["y1"]), _stream(stream)))
 
 
 def atp_mlp_bwd(mesh, bufs, T, h, F, chunks=1, stream=None):
     a = _arr(_abi.MlpBwdArgs, [_mlp_bwd(b) for b in bufs])
-    check(lib().atp_mlp_bwd(mesh.handle, a, T, h, F, chunks, _abi.ATP_BF16, _stream(stream)))
+    check(lib().atp_mlp_bwd(mesh.handle, a, T, h, F, chunks, _dt(bufs[0]["y1"]), _stream(stream)))
 
 
 class LayerCall:
@@ -212,11 +219,12 @@ class LayerCall:
         self.args = _arr(_abi.LayerArgs, [_abi.LayerArgs(_attn_fwd(b), _mlp_fwd(b), _mlp_bwd(b), _attn_bwd(b))
                                           for b in bufs])
         self.dims = (T, h, F, heads, chunks, int(backward))
+        self.dtype = _dt(bufs[0]["x"])
         self._f = lib().atp_layer_fwd_bwd
 
     def __call__(self, stream=None):
         T, h, F, heads, chunks, bwd = self.dims
-        check(self._f(self.mesh.handle, self.args, T, h, F, heads, chunks, bwd, _abi.ATP_BF16, _stream(stream)))
+        check(self._f(self.mesh.handle, self.args, T, h, F, heads, chunks, bwd, self.dtype, _stream(stream)))
 
 
 def atp_layer_fwd_bwd(mesh, bufs, T, h, F, heads, chunks=1, backward=True, stream=None):

@@ -184,7 +184,7 @@ static atp_status linear_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, in
                              int chunks, atp_dtype dtype, void* stream, bool colfirst) {
   atp_status s = check_mesh(mesh, args);
   if (s) return s;
-  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "linear: only ATP_BF16");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "linear: dtype must be ATP_BF16 or ATP_FP32");
   const int din = colfirst ? mesh->d2 : mesh->d1, dout = colfirst ? mesh->d1 : mesh->d2;
   if (chunks < 1 || chunks > atp::kMaxChunks || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) ||
       !w8(N / dout))
@@ -193,7 +193,7 @@ static atp_status linear_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, in
   for (int r = 0; r < n_ranks(mesh); ++r)
     if (!args[r].x || !args[r].w || !args[r].y) return fail(ATP_ERR_INVALID, "linear fwd: NULL buffer");
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
-    return atp::build_linear_fwd(rv, colfirst, args[r], M, K, N, chunks, out);
+    return atp::build_linear_fwd(rv, colfirst, args[r], M, K, N, chunks, dtype, out);
   });
 }
 
@@ -201,7 +201,7 @@ static atp_status linear_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, in
                              int chunks, atp_dtype dtype, void* stream, bool colfirst) {
   atp_status s = check_mesh(mesh, args);
   if (s) return s;
-  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "linear: only ATP_BF16");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "linear: dtype must be ATP_BF16 or ATP_FP32");
   const int din = colfirst ? mesh->d2 : mesh->d1, dout = colfirst ? mesh->d1 : mesh->d2;
   if (chunks < 1 || chunks > atp::kMaxChunks || M < 1 || M % chunks || K % din || N % dout || !w8(K / din) ||
       !w8(N / dout) || M % 8)
@@ -210,7 +210,7 @@ static atp_status linear_bwd(atp_mesh* mesh, const atp_linear_bwd_args* args, in
   for (int r = 0; r < n_ranks(mesh); ++r)
     if (!args[r].x || !args[r].w || !args[r].dy || !args[r].dx) return fail(ATP_ERR_INVALID, "linear bwd: NULL buffer");
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
-    return atp::build_linear_bwd(rv, colfirst, args[r], M, K, N, chunks, out);
+    return atp::build_linear_bwd(rv, colfirst, args[r], M, K, N, chunks, dtype, out);
   });
 }
 
@@ -249,7 +249,7 @@ atp_status atp_mlp_fwd(atp_mesh* mesh, const atp_mlp_fwd_args* args, int64_t T, 
                        atp_dtype dtype, void* stream) {
   atp_status s = check_mesh(mesh, args);
   if (s) return s;
-  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "mlp: only ATP_BF16");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "mlp: dtype must be ATP_BF16 or ATP_FP32");
   if ((s = check_layer_shapes(mesh, T, h, F, 1, chunks, false, true))) return s;
   for (int r = 0; r < n_ranks(mesh); ++r) {
     const auto& a = args[r];
@@ -258,7 +258,7 @@ atp_status atp_mlp_fwd(atp_mesh* mesh, const atp_mlp_fwd_args* args, int64_t T, 
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
     atp::LayerParts p;
     p.mlp_fwd = &args[r];
-    return atp::build_layer(rv, p, T, h, F, 1, chunks, out);
+    return atp::build_layer(rv, p, T, h, F, 1, chunks, dtype, out);
   });
 }
 
@@ -266,7 +266,7 @@ atp_status atp_mlp_bwd(atp_mesh* mesh, const atp_mlp_bwd_args* args, int64_t T, 
                        atp_dtype dtype, void* stream) {
   atp_status s = check_mesh(mesh, args);
   if (s) return s;
-  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "mlp: only ATP_BF16");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "mlp: dtype must be ATP_BF16 or ATP_FP32");
   if ((s = check_layer_shapes(mesh, T, h, F, 1, chunks, false, true))) return s;
   for (int r = 0; r < n_ranks(mesh); ++r) {
     const auto& a = args[r];
@@ -276,7 +276,7 @@ atp_status atp_mlp_bwd(atp_mesh* mesh, const atp_mlp_bwd_args* args, int64_t T, 
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
     atp::LayerParts p;
     p.mlp_bwd = &args[r];
-    return atp::build_layer(rv, p, T, h, F, 1, chunks, out);
+    return atp::build_layer(rv, p, T, h, F, 1, chunks, dtype, out);
   });
 }
 
@@ -284,7 +284,7 @@ atp_status atp_attn_proj_fwd(atp_mesh* mesh, const atp_attn_fwd_args* args, int6
                              int chunks, atp_core core, atp_dtype dtype, void* stream) {
   atp_status s = check_mesh(mesh, args);
   if (s) return s;
-  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_BF16");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "attn: dtype must be ATP_BF16 or ATP_FP32");
   if (core != ATP_CORE_SUM_QKV) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_CORE_SUM_QKV");
   if ((s = check_layer_shapes(mesh, T, h, 8, heads, chunks, true, false))) return s;
   for (int r = 0; r < n_ranks(mesh); ++r) {
@@ -294,7 +294,7 @@ atp_status atp_attn_proj_fwd(atp_mesh* mesh, const atp_attn_fwd_args* args, int6
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
     atp::LayerParts p;
     p.attn_fwd = &args[r];
-    return atp::build_layer(rv, p, T, h, 8, heads, chunks, out);
+    return atp::build_layer(rv, p, T, h, 8, heads, chunks, dtype, out);
   });
 }
 
@@ -302,7 +302,7 @@ atp_status atp_attn_proj_bwd(atp_mesh* mesh, const atp_attn_bwd_args* args, int6
                              int chunks, atp_core core, atp_dtype dtype, void* stream) {
   atp_status s = check_mesh(mesh, args);
   if (s) return s;
-  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_BF16");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "attn: dtype must be ATP_BF16 or ATP_FP32");
   if (core != ATP_CORE_SUM_QKV) return fail(ATP_ERR_UNSUPPORTED, "attn: only ATP_CORE_SUM_QKV");
   if ((s = check_layer_shapes(mesh, T, h, 8, heads, chunks, true, false))) return s;
   for (int r = 0; r < n_ranks(mesh); ++r) {
@@ -313,7 +313,7 @@ atp_status atp_attn_proj_bwd(atp_mesh* mesh, const atp_attn_bwd_args* args, int6
   return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
     atp::LayerParts p;
     p.attn_bwd = &args[r];
-    return atp::build_layer(rv, p, T, h, 8, heads, chunks, out);
+    return atp::build_layer(rv, p, T, h, 8, heads, chunks, dtype, out);
   });
 }
 
@@ -321,7 +321,7 @@ atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t
                              int64_t heads, int chunks, int do_backward, atp_dtype dtype, void* stream) {
   atp_status s = check_mesh(mesh, args);
   if (s) return s;
-  if (dtype != ATP_BF16) return fail(ATP_ERR_UNSUPPORTED, "layer: only ATP_BF16");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "layer: dtype must be ATP_BF16 or ATP_FP32");
   if ((s = check_layer_shapes(mesh, T, h, F, heads, chunks, true, true))) return s;
   for (int r = 0; r < n_ranks(mesh); ++r) {
     const auto& a = args[r];
@@ -337,7 +337,7 @@ atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t
       p.mlp_bwd = &args[r].mlp_b;
       p.attn_bwd = &args[r].attn_b;
     }
-    return atp::build_layer(rv, p, T, h, F, heads, chunks, out);
+    return atp::build_layer(rv, p, T, h, F, heads, chunks, dtype, out);
   });
 }
 

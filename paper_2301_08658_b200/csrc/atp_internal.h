@@ -42,6 +42,11 @@ struct GemmDesc {
   // once its output is globally visible.  nullptr = no signalling.
   uint32_t* sig = nullptr;
   int sig_rows = 0;
+  // fp32 check mode (gemm_f32.cu): dtype 1, raw operands instead of TMA maps
+  int dtype = 0;
+  const void* A = nullptr;
+  const void* B = nullptr;
+  int64_t lda = 0, ldb = 0;
 };
 
 // C[M,N] = A[M,K] * B[N,K]^T.
@@ -50,6 +55,9 @@ struct GemmDesc {
 const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, const void* B,
                          int64_t ldb, bool b_mn, int M, int N, int K);
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t st);
+const char* gemm_prepare_f32(GemmDesc& d, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
+                             bool b_mn, int M, int N, int K);
+cudaError_t gemm_launch_f32(const GemmDesc& d, cudaStream_t st);
 // Tile plan gemm_prepare will use for an M x N output: N tile (128/256) and CTA group (1/2).
 void gemm_plan_tile(int M, int N, int* bn, int* cg);
 int gemm_tiles(const GemmDesc& d);

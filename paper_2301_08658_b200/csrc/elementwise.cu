@@ -35,6 +35,18 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
 struct V8 {
   float f[8];
 };
+__device__ __forceinline__ V8 ld8(const float* p) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0];
+  const float4 b = reinterpret_cast<const float4*>(p)[1];
+  V8 r;
+  r.f[0] = a.x; r.f[1] = a.y; r.f[2] = a.z; r.f[3] = a.w;
+  r.f[4] = b.x; r.f[5] = b.y; r.f[6] = b.z; r.f[7] = b.w;
+  return r;
+}
+__device__ __forceinline__ void st8(float* p, const V8& v) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v.f[0], v.f[1], v.f[2], v.f[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v.f[4], v.f[5], v.f[6], v.f[7]);
+}
 __device__ __forceinline__ V8 ld8(const __nv_bfloat16* p) {
   uint4 u = *reinterpret_cast<const uint4*>(p);
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -56,8 +68,8 @@ __device__ __forceinline__ void st8(__nv_bfloat16* p, const V8& v) {
 }
 
 // Elementwise over a dense [rows, cols] matrix (cols % 8 == 0), n8 = rows*cols/8.
-__global__ void gelu_kernel(const __nv_bfloat16* __restrict__ u, __nv_bfloat16* __restrict__ h,
-                            int64_t n8) {
+template <class T>
+__global__ void gelu_kernel(const T* __restrict__ u, T* __restrict__ h, int64_t n8) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     V8 v = ld8(u + 8 * i);
 #pragma unroll
@@ -66,8 +78,8 @@ __global__ void gelu_kernel(const __nv_bfloat16* __restrict__ u, __nv_bfloat16* 
   }
 }
 
-__global__ void dgelu_kernel(__nv_bfloat16* __restrict__ dh, const __nv_bfloat16* __restrict__ u,
-                             int64_t n8) {
+template <class T>
+__global__ void dgelu_kernel(T* __restrict__ dh, const T* __restrict__ u, int64_t n8) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     V8 g = ld8(dh + 8 * i);
     V8 x = ld8(u + 8 * i);
@@ -77,8 +89,8 @@ __global__ void dgelu_kernel(__nv_bfloat16* __restrict__ dh, const __nv_bfloat16
   }
 }
 
-__global__ void add_kernel(const __nv_bfloat16* __restrict__ a, __nv_bfloat16* __restrict__ out,
-                           int64_t n8) {
+template <class T>
+__global__ void add_kernel(const T* __restrict__ a, T* __restrict__ out, int64_t n8) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     V8 x = ld8(a + 8 * i);
     V8 y = ld8(out + 8 * i);
@@ -90,15 +102,15 @@ __global__ void add_kernel(const __nv_bfloat16* __restrict__ a, __nv_bfloat16* _
 
 // ctx[t, hd*d + j] = qkv[t, hd*3d + j] + qkv[t, hd*3d + d + j] + qkv[t, hd*3d + 2d + j]
 // One thread per 8 ctx columns; d % 8 == 0.
-__global__ void core_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ ctx,
-                                int64_t rows, int heads, int d) {
+template <class T>
+__global__ void core_fwd_kernel(const T* __restrict__ qkv, T* __restrict__ ctx, int64_t rows, int heads, int d) {
   const int w8 = heads * d / 8;
   const int64_t n = rows * w8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / w8;
     const int c8 = static_cast<int>(i % w8) * 8;
     const int hd = c8 / d, j = c8 % d;
-    const __nv_bfloat16* src = qkv + t * (int64_t)(3 * heads * d) + hd * 3 * d + j;
+    const T* src = qkv + t * (int64_t)(3 * heads * d) + hd * 3 * d + j;
     V8 q = ld8(src), k = ld8(src + d), v = ld8(src + 2 * d);
 #pragma unroll
     for (int e = 0; e < 8; ++e) q.f[e] = (q.f[e] + k.f[e]) + v.f[e];
@@ -106,19 +118,19 @@ __global__ void core_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bflo
   }
 }
 
-__global__ void core_bwd_kernel(const __nv_bfloat16* __restrict__ dctx, __nv_bfloat16* __restrict__ dqkv,
-                                int64_t rows, int heads, int d) {
+template <class T>
+__global__ void core_bwd_kernel(const T* __restrict__ dctx, T* __restrict__ dqkv, int64_t rows, int heads, int d) {
   const int w8 = heads * d / 8;
   const int64_t n = rows * w8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / w8;
     const int c8 = static_cast<int>(i % w8) * 8;
     const int hd = c8 / d, j = c8 % d;
-    uint4 v = *reinterpret_cast<const uint4*>(dctx + t * (int64_t)(heads * d) + c8);
-    __nv_bfloat16* dst = dqkv + t * (int64_t)(3 * heads * d) + hd * 3 * d + j;
-    *reinterpret_cast<uint4*>(dst) = v;
-    *reinterpret_cast<uint4*>(dst + d) = v;
-    *reinterpret_cast<uint4*>(dst + 2 * d) = v;
+    const V8 v = ld8(dctx + t * (int64_t)(heads * d) + c8);
+    T* dst = dqkv + t * (int64_t)(3 * heads * d) + hd * 3 * d + j;
+    st8(dst, v);
+    st8(dst + d, v);
+    st8(dst + 2 * d, v);
   }
 }
 
@@ -129,8 +141,17 @@ __global__ void core_bwd_kernel(const __nv_bfloat16* __restrict__ dctx, __nv_bfl
 // distributed shared memory.
 constexpr int kColsumSplit = 8;
 constexpr int kColsumWarps = 8;
-__global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(const __nv_bfloat16* __restrict__ x,
-                                                                  float* __restrict__ out, int64_t rows, int cols) {
+__device__ __forceinline__ float4 ld4f(const __nv_bfloat16* p) {
+  const uint2 v = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float4 ld4f(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+template <class T>
+__global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(const T* __restrict__ x, float* __restrict__ out,
+                                                                  int64_t rows, int cols) {
   namespace cg = cooperative_groups;
   __shared__ float4 part[kColsumWarps][32];
   __shared__ float4 total[32];
@@ -144,27 +165,23 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(const __nv_bf
   if (c4 < cols) {
     int64_t r = r0 + warp;
     for (; r + 3 * kColsumWarps < r1; r += 4 * kColsumWarps) {
-      uint2 v[4];
+      float4 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const uint2*>(x + (r + u * kColsumWarps) * cols + c4);
+      for (int u = 0; u < 4; ++u) v[u] = ld4f(x + (r + u * kColsumWarps) * cols + c4);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[u].x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[u].y));
-        acc.x += a.x;
-        acc.y += a.y;
-        acc.z += b.x;
-        acc.w += b.y;
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
       }
     }
     for (; r < r1; r += kColsumWarps) {
-      const uint2 v = *reinterpret_cast<const uint2*>(x + r * cols + c4);
-      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
-      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
-      acc.x += a.x;
-      acc.y += a.y;
-      acc.z += b.x;
-      acc.w += b.y;
+      const float4 v = ld4f(x + r * cols + c4);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
     }
   }
   part[warp][lane] = acc;
@@ -195,15 +212,16 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(const __nv_bf
   cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
 }
 
+template <class T>
 __global__ void group_sum_kernel(GroupSumArgs g, int64_t n8) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    V8 acc = ld8(g.buf[0] + 8 * i);
+    V8 acc = ld8(static_cast<const T*>(g.buf[0]) + 8 * i);
     for (int r = 1; r < g.p; ++r) {
-      V8 v = ld8(g.buf[r] + 8 * i);
+      V8 v = ld8(static_cast<const T*>(g.buf[r]) + 8 * i);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc.f[j] += v.f[j];
     }
-    for (int r = 0; r < g.p; ++r) st8(g.buf[r] + 8 * i, acc);
+    for (int r = 0; r < g.p; ++r) st8(static_cast<T*>(g.buf[r]) + 8 * i, acc);
   }
 }
 
@@ -217,26 +235,26 @@ int ew_grid(int64_t n) {
 
 }  // namespace
 
-cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
-  using bf = __nv_bfloat16;
+template <class T>
+cudaError_t ew_launch_t(const EwDesc& e, cudaStream_t st) {
   const int64_t n = e.rows * e.cols;
   switch (e.kind) {
     case EW_GELU:
-      gelu_kernel<<<ew_grid(n / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, n / 8);
+      gelu_kernel<T><<<ew_grid(n / 8), 256, 0, st>>>((const T*)e.a, (T*)e.out, n / 8);
       break;
     case EW_DGELU:
-      dgelu_kernel<<<ew_grid(n / 8), 256, 0, st>>>((bf*)e.out, (const bf*)e.a, n / 8);
+      dgelu_kernel<T><<<ew_grid(n / 8), 256, 0, st>>>((T*)e.out, (const T*)e.a, n / 8);
       break;
     case EW_ADD:
-      add_kernel<<<ew_grid(n / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, n / 8);
+      add_kernel<T><<<ew_grid(n / 8), 256, 0, st>>>((const T*)e.a, (T*)e.out, n / 8);
       break;
     case EW_CORE_FWD:
-      core_fwd_kernel<<<ew_grid(e.rows * e.cols / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, e.rows,
-                                                                    e.heads, static_cast<int>(e.cols / e.heads));
+      core_fwd_kernel<T><<<ew_grid(n / 8), 256, 0, st>>>((const T*)e.a, (T*)e.out, e.rows, e.heads,
+                                                         static_cast<int>(e.cols / e.heads));
       break;
     case EW_CORE_BWD:
-      core_bwd_kernel<<<ew_grid(e.rows * e.cols / 8), 256, 0, st>>>((const bf*)e.a, (bf*)e.out, e.rows,
-                                                                    e.heads, static_cast<int>(e.cols / e.heads));
+      core_bwd_kernel<T><<<ew_grid(n / 8), 256, 0, st>>>((const T*)e.a, (T*)e.out, e.rows, e.heads,
+                                                         static_cast<int>(e.cols / e.heads));
       break;
     case EW_COLSUM: {
       cudaLaunchConfig_t cfg = {};
@@ -250,7 +268,7 @@ cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      return cudaLaunchKernelEx(&cfg, colsum_kernel, (const bf*)e.a, (float*)e.out, e.rows, static_cast<int>(e.cols));
+      return cudaLaunchKernelEx(&cfg, colsum_kernel<T>, (const T*)e.a, (float*)e.out, e.rows, static_cast<int>(e.cols));
     }
     default:
       return cudaErrorInvalidValue;
@@ -258,8 +276,15 @@ cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t group_sum_launch(const GroupSumArgs& g, int64_t n, cudaStream_t st) {
-  group_sum_kernel<<<ew_grid(n / 8), 256, 0, st>>>(g, n / 8);
+cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
+  return e.dtype == 1 ? ew_launch_t<float>(e, st) : ew_launch_t<__nv_bfloat16>(e, st);
+}
+
+cudaError_t group_sum_launch(const GroupSumArgs& g, int64_t n, int dtype, cudaStream_t st) {
+  if (dtype == 1)
+    group_sum_kernel<float><<<ew_grid(n / 8), 256, 0, st>>>(g, n / 8);
+  else
+    group_sum_kernel<__nv_bfloat16><<<ew_grid(n / 8), 256, 0, st>>>(g, n / 8);
   return cudaGetLastError();
 }
 

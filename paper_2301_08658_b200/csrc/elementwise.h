@@ -21,15 +21,16 @@ struct EwDesc {
   const void* a = nullptr;
   int64_t rows = 0, cols = 0;  // cols: width of `out` (core_fwd) / of `a` (core_bwd, colsum)
   int heads = 1;
+  int dtype = 0;  // 0 = bf16, 1 = fp32 (check mode)
 };
 
 constexpr int kMaxGroup = 16;
 struct GroupSumArgs {
-  __nv_bfloat16* buf[kMaxGroup];
+  void* buf[kMaxGroup];
   int p = 0;
 };
 
 cudaError_t ew_launch(const EwDesc& e, cudaStream_t st);
-cudaError_t group_sum_launch(const GroupSumArgs& g, int64_t n, cudaStream_t st);
+cudaError_t group_sum_launch(const GroupSumArgs& g, int64_t n, int dtype, cudaStream_t st);
 
 }  // namespace atp

@@ -518,6 +518,7 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
 }
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t st) {
+  if (d.dtype == 1) return gemm_launch_f32(d, st);
   int sms = d.max_ctas > 0 ? d.max_ctas : num_sms();
   const int units = sms / d.cg > 0 ? sms / d.cg : 1;
   const int tiles = gemm_tiles(d);

@@ -80,7 +80,7 @@ void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes) {
     }
   } else {
     *cls = 2;
-    *bytes = p > 1 ? 2.0 * (p - 1) / p * op.ar_count * 2.0 : 0.0;
+    *bytes = p > 1 ? 2.0 * (p - 1) / p * op.ar_count * (op.ar_dtype == 1 ? 4.0 : 2.0) : 0.0;
   }
 }
 
@@ -189,8 +189,8 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
       if (op.kind == OP_AR) {
         if (m->comm_enabled) {
           ncclComm_t comm = op.ar_dim == 1 ? m->dim1 : m->dim2;
-          ncclResult_t nr = ncclAllReduce(op.ar_ptr, op.ar_ptr, static_cast<size_t>(op.ar_count), ncclBfloat16,
-                                          ncclSum, comm, st);
+          ncclResult_t nr = ncclAllReduce(op.ar_ptr, op.ar_ptr, static_cast<size_t>(op.ar_count),
+                                          op.ar_dtype == 1 ? ncclFloat32 : ncclBfloat16, ncclSum, comm, st);
           if (nr != ncclSuccess) {
             set_error(std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
             return 4;
@@ -254,7 +254,7 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
       GroupSumArgs ga;
       ga.p = p;
       for (int j = 0; j < p; ++j) {
-        ga.buf[j] = static_cast<__nv_bfloat16*>(sch[members[j]].ops[i].ar_ptr);
+        ga.buf[j] = sch[members[j]].ops[i].ar_ptr;
         if (j > 0) {
           cudaEventRecord(m->rs[members[j]].arrive, m->rs[members[j]].comm);
           cudaStreamWaitEvent(m->rs[leader].comm, m->rs[members[j]].arrive, 0);
@@ -262,7 +262,8 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
       }
       ProfRec* pr = prof_begin(m, sch[leader].ops[i], m->rs[leader].comm);
       if (m->comm_enabled) {
-        if ((e = group_sum_launch(ga, sch[leader].ops[i].ar_count, m->rs[leader].comm)) != cudaSuccess)
+        if ((e = group_sum_launch(ga, sch[leader].ops[i].ar_count, sch[leader].ops[i].ar_dtype,
+                                  m->rs[leader].comm)) != cudaSuccess)
           return cuda_fail(e, "group_sum launch");
         count_launch(1);
       }

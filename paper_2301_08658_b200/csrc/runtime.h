@@ -32,7 +32,8 @@ struct Op {
   EwDesc e;
   int ar_dim = 0;  // mesh dimension of the grouped all-reduce (1 or 2)
   void* ar_ptr = nullptr;
-  int64_t ar_count = 0;  // bf16 elements, in place
+  int64_t ar_count = 0;  // elements, in place
+  int ar_dtype = 0;      // 0 = bf16, 1 = fp32
   // OP_WAITSIG: the stream waits until counter `sig_slot` has grown by
   // `sig_inc` since the previous wait on that slot (cyclic >=).
   int sig_slot = 0;

@@ -47,10 +47,12 @@ namespace {
 
 using bf16 = __nv_bfloat16;
 
+// element size of the schedule being built (2 = bf16, 4 = fp32 check mode)
+thread_local int g_esz = 2;
 inline const char* cptr(const void* p, int64_t off_elems) {
-  return static_cast<const char*>(p) + off_elems * 2;
+  return static_cast<const char*>(p) + off_elems * g_esz;
 }
-inline char* mptr(void* p, int64_t off_elems) { return static_cast<char*>(p) + off_elems * 2; }
+inline char* mptr(void* p, int64_t off_elems) { return static_cast<char*>(p) + off_elems * g_esz; }
 
 using EwList = std::vector<EwDesc>;
 
@@ -64,9 +66,12 @@ struct Builder {
   std::vector<int> pend;    // per chunk: event the next compute op of that chunk must wait on
   std::vector<EwList> def;  // per chunk: deferred elementwise ops (per-chunk mode)
 
-  Builder(const RankView& v, int64_t rows, int c) : rv(v), chunks(c), T(rows), Mc(rows / c) {
+  int dtype = 0;  // 0 = bf16, 1 = fp32 check mode
+
+  Builder(const RankView& v, int64_t rows, int c, int dt) : rv(v), chunks(c), T(rows), Mc(rows / c), dtype(dt) {
     pend.assign(c, -1);
     def.assign(c, {});
+    g_esz = dt == 1 ? 4 : 2;
   }
   int ev() { return s.n_events++; }
 
@@ -91,6 +96,7 @@ struct Builder {
     for (const EwDesc& e : def[k]) {
       Op& o = push(OP_EW, 0);
       o.e = e;
+      o.e.dtype = dtype;
       add_wait(o, w);
       w = -1;
     }
@@ -114,8 +120,10 @@ struct Builder {
     o.g.max_ctas = rv.gemm_ctas;
     o.g.epi = epi;
     o.g.ep = ep;
-    const char* m = gemm_prepare(o.g, A, lda, a_mn, B, ldb, b_mn, static_cast<int>(M), static_cast<int>(N),
-                                 static_cast<int>(K));
+    const char* m = dtype == 1 ? gemm_prepare_f32(o.g, A, lda, a_mn, B, ldb, b_mn, static_cast<int>(M),
+                                                  static_cast<int>(N), static_cast<int>(K))
+                               : gemm_prepare(o.g, A, lda, a_mn, B, ldb, b_mn, static_cast<int>(M),
+                                              static_cast<int>(N), static_cast<int>(K));
     if (m) {
       err = m;
       return nullptr;
@@ -129,12 +137,14 @@ struct Builder {
     o.ar_dim = dim;
     o.ar_ptr = ptr;
     o.ar_count = count;
+    o.ar_dtype = dtype;
     add_wait(o, wait);
     o.record = record;
   }
   void ew(const EwDesc& e, int stream, int wait = -1) {
     Op& o = push(OP_EW, stream);
     o.e = e;
+    o.e.dtype = dtype;
     add_wait(o, wait);
   }
   int dim_size(int dim) const { return dim == 1 ? rv.d1 : rv.d2; }
@@ -165,8 +175,8 @@ struct Builder {
       return true;
     }
     const void* bias_here = coord0(dim) ? bias : nullptr;
-    int bn = 0, cg = 0;
-    gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
+    int bn = 128, cg = 1;  // fp32 check mode: 128 x 128 tiles
+    if (dtype == 0) gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
     if (rv.signalled && rv.sig_buf != nullptr && chunks > 1 && Mc % (128 * cg) == 0 &&
         next_slot + chunks <= kSigSlots) {
       // ---- signalled stage: one GEMM over all T rows, per-chunk counters
@@ -254,8 +264,8 @@ auto no_extra = []() { return true; };
 
 // ---------------------------------------------------------------- linears
 int build_linear_fwd(const RankView& rv, bool colfirst, const LinearFwd& a, int64_t M, int64_t K, int64_t N,
-                     int chunks, Sched& out) {
-  Builder b(rv, M, chunks);
+                     int chunks, int dtype, Sched& out) {
+  Builder b(rv, M, chunks, dtype);
   const int dim = colfirst ? 2 : 1;
   const int64_t in_w = colfirst ? K / rv.d2 : K / rv.d1;
   const int64_t out_w = colfirst ? N / rv.d1 : N / rv.d2;
@@ -269,8 +279,8 @@ int build_linear_fwd(const RankView& rv, bool colfirst, const LinearFwd& a, int6
 }
 
 int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int64_t M, int64_t K, int64_t N,
-                     int chunks, Sched& out) {
-  Builder b(rv, M, chunks);
+                     int chunks, int dtype, Sched& out) {
+  Builder b(rv, M, chunks, dtype);
   const int dim = colfirst ? 1 : 2;  // conjugate dimension ("f3 ... on the second dimension in backward")
   const int64_t x_w = colfirst ? K / rv.d2 : K / rv.d1;
   const int64_t dy_w = colfirst ? N / rv.d1 : N / rv.d2;
@@ -287,8 +297,8 @@ int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int6
 
 // ---------------------------------------------------------------- layer blocks
 int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
-                int chunks, Sched& out) {
-  Builder b(rv, T, chunks);
+                int chunks, int dtype, Sched& out) {
+  Builder b(rv, T, chunks, dtype);
   const int64_t hc = h / rv.d2;      // activation column block
   const int64_t h1 = h / rv.d1;      // ctx width / Out input
   const int64_t q1 = 3 * h / rv.d1;  // local QKV width

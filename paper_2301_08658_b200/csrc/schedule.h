@@ -15,12 +15,13 @@ struct LayerParts {
   const atp_attn_bwd_args* attn_bwd = nullptr;
 };
 
+// dtype: 0 = bf16 (tcgen05 path), 1 = fp32 check mode
 int build_linear_fwd(const RankView& rv, bool colfirst, const LinearFwd& a, int64_t M, int64_t K, int64_t N,
-                     int chunks, Sched& out);
+                     int chunks, int dtype, Sched& out);
 int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int64_t M, int64_t K, int64_t N,
-                     int chunks, Sched& out);
+                     int chunks, int dtype, Sched& out);
 int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
-                int chunks, Sched& out);
+                int chunks, int dtype, Sched& out);
 
 const char* last_error();
 int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, bool is_virtual, atp_mesh** out);

@@ -24,6 +24,13 @@ def oracle_layer(T, h, F, heads, d1, d2, chunks, seed):
     return g, sh, fw, bw, log
 
 
+def oracle_layer_fp32(T, h, F, heads, d1, d2, chunks, seed):
+    """Oracle on unrounded fp32 inputs (the ATP_FP32 check mode's values)."""
+    g = {k: v.astype(np.float64) for k, v in datagen.layer_globals(T, h, F, seed=seed, bf16=False).items()}
+    sh, fw, bw, log = olayer.run_layer(g, d1, d2, heads, chunks)
+    return g, sh, fw, bw, log
+
+
 # GPU buffer name -> oracle (dict, key)
 FWD_MAP = {"qkv": "qkv", "ctx": "ctx", "y1": "y1", "u": "u", "h": "h", "z": "z"}
 BWD_MAP = {"dy1": "dy1", "dx": "dx", "dwqkv": "dwqkv", "dbqkv": "dbqkv", "dwo": "dwo", "dbo": "dbo",
