@@ -1,0 +1,90 @@
+"""Full-size parity in the launch configuration bench.py times.
+
+* DeviceMesh(1,1), h=4096, a=32, F=16384, T=8192 (BASELINE configs[1] shapes),
+  through a distributed NCCL mesh of one rank and LayerCall exactly as bench.py
+  runs it: EVERY output (all activations, dX, all weight and bias gradients)
+  against the oracle's dense layer evaluated with float32 BLAS (the oracle code
+  is dtype-agnostic; float32 adds ~1e-6, far below the 2e-2 bar).
+* cfg 4 per-rank shapes on a virtual DeviceMesh(4,2) with 4 chunks (the
+  searched 8-GPU mesh; signalled stages): sampled token rows of the forward
+  output and of dX against the oracle evaluated row by row (the layer has no
+  cross-token op, so a row needs only its own input rows), plus a property that
+  holds at any size for a weight gradient: dW2 = H^T dZ  ==>  dW2 @ 1 = H^T (dZ 1)
+  evaluated with the GPU's own saved H.
+"""
+import numpy as np
+import pytest
+
+import datagen
+from oracle import layer as olayer
+
+from gpu_util import rel, to_np
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _globals32(T, h, F, seed, rows=None):
+    out = {}
+    for k, s in datagen.layer_shapes(T, h, F).items():
+        r = rows if (k in ("x", "dz") and rows is not None) else None
+        out[k] = datagen.tensor(k, s, seed=seed, rows=r).astype(np.float32)
+    return out
+
+
+def test_fullsize_mesh11_every_output():
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, seed = 8192, 4096, 16384, 32, 2301
+    uid = atp.atp_get_unique_id()
+    mesh = atp.Mesh.distributed(1, 1, 0, uid, 0)
+    try:
+        bufs = atp.alloc_layer_rank(1, 1, 0, T, h, F, "cuda", seed)
+        atp.LayerCall(mesh, [bufs], T, h, F, heads, 1, True)()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    g = _globals32(T, h, F, seed)
+    c = olayer.dense_forward(g, heads)
+    d = olayer.dense_backward(g, c, g["dz"], heads)
+    pairs = {"qkv": c["qkv"], "ctx": c["ctx"], "y1": c["y1"], "u": c["u"], "h": c["h"], "z": c["z"],
+             "dy1": d["dy1"], "dx": d["dx"], "dwqkv": d["dwqkv"], "dbqkv": d["dbqkv"], "dwo": d["dwo"],
+             "dbo": d["dbo"], "dw1": d["dw1"], "db1": d["db1"], "dw2": d["dw2"], "db2": d["db2"]}
+    for k, ref in pairs.items():
+        e = rel(to_np(bufs[k]), ref)
+        assert e <= TOL, (k, e)
+
+
+def test_fullsize_cfg4_mesh42_sampled_rows():
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, seed, d1, d2, chunks = 8192, 5120, 20480, 40, 2301, 4, 2, 4
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(d1 * d2)]
+        atp.LayerCall(mesh, bufs, T, h, F, heads, chunks, True)()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(T, 24, replace=False))
+    rows = np.concatenate([rows, [0, T // chunks - 1, T // chunks, T - 1]])  # chunk edges
+    g = _globals32(T, h, F, seed, rows=rows)
+    c = olayer.dense_forward(g, heads)
+    d = olayer.dense_backward(g, c, g["dz"], heads)
+    hc = h // d2
+    for r in range(d1 * d2):
+        i2 = r % d2
+        cols = slice(i2 * hc, (i2 + 1) * hc)
+        rr = torch.as_tensor(rows, device="cuda")
+        assert rel(to_np(bufs[r]["z"][rr]), c["z"][:, cols]) <= TOL
+        assert rel(to_np(bufs[r]["y1"][rr]), c["y1"][:, cols]) <= TOL
+        assert rel(to_np(bufs[r]["dx"][rr]), d["dx"][:, cols]) <= TOL
+    # any-size property of a weight gradient: dW2 @ 1 == H^T (dZ @ 1), per rank
+    for r in range(d1 * d2):
+        b = bufs[r]
+        lhs = b["dw2"].double().sum(dim=1)
+        rhs = b["h"].double().t() @ b["dz"].double().sum(dim=1)
+        assert rel(lhs.cpu().numpy(), rhs.cpu().numpy()) <= TOL
