@@ -40,12 +40,32 @@ constexpr int kEpiWarps = 8;                 // 2 per SM sub-partition: hides ep
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer warp + MMA warp + epilogue warps
 constexpr uint32_t kBoxBytesMN = 64 * 64 * 2;  // one MN-major box: 64 (mn) x 64 (k)
 
+// Exact-erf GeLU (reading G15) for the bf16 epilogues.  erf via Abramowitz &
+// Stegun 7.1.26 (|error| <= 1.5e-7, fp32 level; the output is rounded to bf16,
+// 2^-9 relative): erf(z) = 1 - t(a1 + t(a2 + t(a3 + t(a4 + t a5)))) e^{-z^2},
+// t = 1/(1 + p z), z >= 0.  With z = |x|/sqrt(2), e^{-z^2} = e^{-x^2/2} is also
+// phi(x)*sqrt(2 pi), so GeLU'(x) = Phi(x) + x phi(x) reuses it.
+struct ErfExp {
+  float erf_abs;  // erf(|x|/sqrt 2)
+  float e;        // exp(-x^2/2)
+};
+__device__ __forceinline__ ErfExp erf_as(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.0f));
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
+  const float e = exp2f(-0.72134752044448170f * x * x);  // exp(-x^2/2) = 2^(-x^2 / (2 ln 2))
+  return {1.0f - poly * e, e};
+}
 __device__ __forceinline__ float gelu_f(float x) {
-  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+  const ErfExp r = erf_as(x);
+  const float erf = copysignf(r.erf_abs, x);
+  return 0.5f * x * (1.0f + erf);
 }
 __device__ __forceinline__ float gelu_grad_f(float x) {
-  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
-         x * 0.39894228040143268f * __expf(-0.5f * x * x);
+  const ErfExp r = erf_as(x);
+  const float erf = copysignf(r.erf_abs, x);
+  return fmaf(0.5f, 1.0f + erf, x * 0.39894228040143268f * r.e);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -81,72 +101,101 @@ __device__ __forceinline__ void tile_coords(int tile, int mt_chunk, int num_n, i
   nt = r / gm;
 }
 
-// One 32-column slice of one accumulator row: fused epilogue + 16-byte stores.
+// Epilogue slice width: the GeLU / dGeLU / residual epilogues (extra inputs, ~20 FP ops per element)
+// so they drain TMEM in 16-column slices to stay within the 168-register budget
+// of 320 threads without spilling; the light epilogues use 32-column slices.
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(float (&f)[32], int row, int col0, int M, int N, const EpiParams& ep) {
-  if (row >= M || col0 >= N) return;
-  if (ep.bias != nullptr) {
+__host__ __device__ constexpr int slice_width() {
+  return (EPI == EPI_BIAS_GELU || EPI == EPI_DGELU || EPI == EPI_RESID) ? 16 : 32;
+}
+template <int EPI>
+__host__ __device__ constexpr bool uses_bias() {
+  return EPI != EPI_DGELU;
+}
+
+// Side inputs of one slice (bias, residual / saved U), fetched as 16-byte
+// vectors one slice ahead of their use.
+template <int W>
+struct Side {
+  uint4 bias[W / 8];
+  uint4 aux[W / 8];
+};
+
+template <int EPI, int W>
+__device__ __forceinline__ void load_side(Side<W>& sd, int row, int col0, int M, int N, const EpiParams& ep) {
+  const bool in = row < M && col0 < N;
+  const bool full = col0 + W <= N;
+  if (uses_bias<EPI>() && ep.bias != nullptr) {
+    const uint4* b = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.bias) + col0);
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (col0 + j < N) f[j] += __bfloat162float(static_cast<const __nv_bfloat16*>(ep.bias)[col0 + j]);
+    for (int g = 0; g < W / 8; ++g)
+      sd.bias[g] = (in && (full || col0 + 8 * g + 8 <= N)) ? b[g] : make_uint4(0, 0, 0, 0);
   }
-  const bool full = (col0 + 32 <= N);
+  if constexpr (EPI == EPI_RESID || EPI == EPI_DGELU) {
+    const uint4* a = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.aux) +
+                                                    static_cast<int64_t>(row) * ep.ldaux + col0);
+#pragma unroll
+    for (int g = 0; g < W / 8; ++g)
+      sd.aux[g] = (in && (full || col0 + 8 * g + 8 <= N)) ? a[g] : make_uint4(0, 0, 0, 0);
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ float bf16_at(const uint4 (&v)[NV], int j) {
+  const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(&v[j / 8]);
+  return __bfloat162float(p[j % 8]);
+}
+
+// One W-column slice of one accumulator row: fused epilogue + 16-byte stores.
+template <int EPI, int W>
+__device__ __forceinline__ void epilogue_chunk(float (&f)[W], const Side<W>& sd, int row, int col0, int M, int N,
+                                               const EpiParams& ep) {
+  if (row >= M || col0 >= N) return;
+  if (uses_bias<EPI>() && ep.bias != nullptr) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) f[j] += bf16_at(sd.bias, j);
+  }
+  const bool full = (col0 + W <= N);
   if constexpr (EPI == EPI_F32) {
     float* dst = static_cast<float*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
 #pragma unroll
-    for (int g = 0; g < 8; ++g)
+    for (int g = 0; g < W / 4; ++g)
       if (full || col0 + 4 * g + 4 <= N)
         reinterpret_cast<float4*>(dst)[g] = make_float4(f[4 * g], f[4 * g + 1], f[4 * g + 2], f[4 * g + 3]);
   } else {
     if constexpr (EPI == EPI_RESID) {
-      const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(ep.aux) + static_cast<int64_t>(row) * ep.ldaux + col0;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        if (full || col0 + 8 * g + 8 <= N) {
-          uint4 rv = reinterpret_cast<const uint4*>(r)[g];
-          const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) f[8 * g + j] += __bfloat162float(rb[j]);
-        }
-      }
+      for (int j = 0; j < W; ++j) f[j] += bf16_at(sd.aux, j);
     }
     if constexpr (EPI == EPI_BIAS_GELU) {
       // U = acc + bias (stored, rounded once); H = GeLU(U) from the rounded U
       __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(ep.C2) + static_cast<int64_t>(row) * ep.ldc2 + col0;
-      uint32_t hp[16];
+      uint32_t hp[W / 2];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < W / 2; ++j) {
         const float u0 = __bfloat162float(__float2bfloat16_rn(f[2 * j]));
         const float u1 = __bfloat162float(__float2bfloat16_rn(f[2 * j + 1]));
         hp[j] = pack_bf16(gelu_f(u0), gelu_f(u1));
       }
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
+      for (int g = 0; g < W / 8; ++g)
         if (full || col0 + 8 * g + 8 <= N)
           reinterpret_cast<uint4*>(dh)[g] = make_uint4(hp[4 * g], hp[4 * g + 1], hp[4 * g + 2], hp[4 * g + 3]);
     }
     if constexpr (EPI == EPI_DGELU) {
       // dU = dH * GeLU'(U); dH is the bf16-rounded product (as after an all-reduce)
-      const __nv_bfloat16* u = static_cast<const __nv_bfloat16*>(ep.aux) + static_cast<int64_t>(row) * ep.ldaux + col0;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        if (full || col0 + 8 * g + 8 <= N) {
-          uint4 uv = reinterpret_cast<const uint4*>(u)[g];
-          const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uv);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float dh = __bfloat162float(__float2bfloat16_rn(f[8 * g + j]));
-            f[8 * g + j] = dh * gelu_grad_f(__bfloat162float(ub[j]));
-          }
-        }
+      for (int j = 0; j < W; ++j) {
+        const float dh = __bfloat162float(__float2bfloat16_rn(f[j]));
+        f[j] = dh * gelu_grad_f(bf16_at(sd.aux, j));
       }
     }
     __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
-    uint32_t p[16];
+    uint32_t p[W / 2];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) p[j] = pack_bf16(f[2 * j], f[2 * j + 1]);
+    for (int j = 0; j < W / 2; ++j) p[j] = pack_bf16(f[2 * j], f[2 * j + 1]);
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int g = 0; g < W / 8; ++g)
       if (full || col0 + 8 * g + 8 <= N)
         reinterpret_cast<uint4*>(dst)[g] = make_uint4(p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
   }
@@ -327,15 +376,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
       ptx::tc_fence_after();
       const int row = m0 + 32 * q + static_cast<int>(lane);
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
+      constexpr int W = slice_width<EPI>();
+      const int c_begin = half * (BN / 2 / W), c_end = (half + 1) * (BN / 2 / W);
+      // software pipeline: the TMEM slice and side inputs of slice c+1 are in
+      // flight while slice c is converted and stored
+      uint32_t v[W];
+      Side<W> sd;
+      ptx::tmem_ld_slice<W>(tbase + W * c_begin, v);
+      load_side<EPI, W>(sd, row, n0 + W * c_begin, M, N, ep);
 #pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN + 32 * c, v);
+      for (int c = c_begin; c < c_end; ++c) {
         ptx::tmem_wait_ld();
-        float f[32];
+        float f[W];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-        epilogue_chunk<EPI>(f, row, n0 + 32 * c, M, N, ep);
+        for (int j = 0; j < W; ++j) f[j] = __uint_as_float(v[j]);
+        const Side<W> cur = sd;
+        if (c + 1 < c_end) {
+          ptx::tmem_ld_slice<W>(tbase + W * (c + 1), v);
+          load_side<EPI, W>(sd, row, n0 + W * (c + 1), M, N, ep);
+        }
+        epilogue_chunk<EPI, W>(f, cur, row, n0 + W * c, M, N, ep);
       }
       ptx::tc_fence_before();
       __syncwarp();
