@@ -29,7 +29,13 @@ import sys
 import threading
 import time
 
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "1")  # P:345, set before CUDA init
+# P:345 sets CUDA_DEVICE_MAX_CONNECTIONS=1 so that, in ONE hardware work queue, a
+# communication kernel enqueued before the next GEMM is launched first.  This
+# library's schedule instead gives the communication stream its own queue (high
+# priority, gated by device-side chunk counters) and caps the GEMM CTAs; with a
+# single queue the dW GEMM queued behind the dX GEMM would block the chunk
+# all-reduces (head-of-line), so the default connection count is kept
+# (DESIGN.md §6-7).  An explicit setting in the environment is respected.
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -48,7 +54,9 @@ def parse():
     p.add_argument("--ffn", type=int, default=0, help="default 4*hidden")
     p.add_argument("--batch", type=int, default=4)
     p.add_argument("--seq", type=int, default=2048)
-    p.add_argument("--mesh", default="", help="d1xd2; default: atp_search on a single-layer NVSwitch HCM")
+    p.add_argument("--mesh", default="", help="d1xd2; default: atp_search (uniform NVSwitch HCM, or --probe)")
+    p.add_argument("--probe", action="store_true",
+                   help="N>1: measure the HCM + per-mesh calibration with atp_probe_hcm and search on that")
     p.add_argument("--chunks", type=int, default=0, help="default 1 at N=1, 4 otherwise")
     p.add_argument("--gemm-ctas", type=int, default=-1, help="GEMM CTA cap (default: all SMs at N=1, SMs-16 else)")
     p.add_argument("--seed", type=int, default=2301)
@@ -176,6 +184,20 @@ def cpu_baseline(h: int, F: int, heads: int, seed: int, target_s: float) -> dict
                       f"DeviceMesh(1,1), {t:.1f} s", "seconds": t, "tokens": T_s}
 
 
+def _quiet(fn):
+    """Run fn with fd 1 redirected to stderr (NCCL prints its version banner on
+    stdout at communicator init; stdout carries only the JSON line)."""
+    sys.stdout.flush()
+    saved_fd = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        return fn()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved_fd, 1)
+        os.close(saved_fd)
+
+
 def emit(obj: dict) -> None:
     print(json.dumps(obj), flush=True)
 
@@ -249,32 +271,45 @@ def main() -> None:
     T = a.batch * a.seq
     chunks = a.chunks or (1 if world == 1 else 4)
 
-    # ---- mesh: explicit, or ATP's search on the single-layer NVSwitch HCM
+    # ---- mesh: explicit, or ATP's search (§3.5) on the single-layer NVSwitch HCM
+    # (P:488, 900 GB/s per direction), or with --probe on the HCM measured by
+    # atp_probe_hcm (S1) plus the per-mesh calibration.
     plan = None
-    if a.mesh:
-        d1, d2 = (int(v) for v in a.mesh.lower().split("x"))
-    elif world == 1:
-        d1, d2 = 1, 1
-    else:
-        plan = atp.atp_search([atp.HcmLayer(world, 900.0, 900.0)], 1, a.batch, a.seq, h, heads, 2)
-        d1, d2 = plan["chosen"]
-    assert d1 * d2 == world
-
+    mesh_source = "flag" if a.mesh else ("N=1" if world == 1 else "")
     uid = atp.atp_get_unique_id() if rank == 0 else bytes(128)
     if world > 1:
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    # NCCL prints its version banner on stdout at init: keep stdout for the JSON line only
-    sys.stdout.flush()
-    saved_fd = os.dup(1)
-    os.dup2(2, 1)
-    try:
-        mesh = atp.Mesh.distributed(d1, d2, rank, uid, local_rank)
-    finally:
-        sys.stdout.flush()
-        os.dup2(saved_fd, 1)
-        os.close(saved_fd)
+    if a.mesh:
+        d1, d2 = (int(v) for v in a.mesh.lower().split("x"))
+    elif world == 1:
+        d1, d2 = 1, 1
+    else:
+        layers, calib = [atp.HcmLayer(world, 900.0, 900.0)], None
+        mesh_source = "atp_search(uniform 900 GB/s HCM)"
+        if a.probe:
+            try:
+                pm = _quiet(lambda: atp.Mesh.distributed(world, 1, rank, uid, local_rank))
+                scratch = torch.empty((64 << 20) + 64, dtype=torch.bfloat16, device=dev)
+                chunk_bytes = 2 * (T // chunks) * (4 * h // max(1, world // 2))
+                layers, _, calib = atp.atp_probe_hcm(pm, scratch, msg_bytes=(64 << 20, max(1 << 20, chunk_bytes)),
+                                                    calib_bytes=max(1 << 20, chunk_bytes), iters=5)
+                pm.destroy()
+                del scratch
+                mesh_source = "atp_search(probed HCM + calibration)"
+            except Exception as e:  # noqa: BLE001
+                print(f"probe failed, using the uniform HCM: {e}", file=sys.stderr)
+            # fresh unique id for the layer mesh
+            uid = atp.atp_get_unique_id() if rank == 0 else bytes(128)
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        plan = atp.atp_search(layers, 1, a.batch, a.seq, h, heads, 2, calibration=calib)
+        d1, d2 = plan["chosen"]
+    assert d1 * d2 == world
+
+    mesh = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, uid, local_rank))
     ctas = a.gemm_ctas if a.gemm_ctas >= 0 else (0 if world == 1 else 132)
     mesh.set_gemm_ctas(ctas)
 
@@ -428,14 +463,15 @@ def main() -> None:
                                    f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}",
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
-                       "mesh_source": "flag" if a.mesh else ("N=1" if world == 1 else "atp_search(uniform 900 GB/s HCM)"),
+                       "mesh_source": mesh_source,
                        "l2": "working set > 126 MB L2 (weights+activations ~1-2 GB), no flush"},
             "tflops_per_gpu": per_gpu, "exposed_comm_ms": exposed, "ms_per_step_comm_disabled": ms_nocomm,
             "flops_per_step": fl, "clocks": clocks, "gpu_launches": launches,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
         }
         if plan is not None:
-            out["search"] = {"chosen": plan["chosen"], "ranked": [(r["d1"], r["d2"], r["t_comm"]) for r in plan["ranked"]]}
+            out["search"] = {"chosen": plan["chosen"], "ranked": [(r["d1"], r["d2"], r["t_comm"], r["calibrated"])
+                                                                   for r in plan["ranked"]]}
         emit(out)
     if world > 1:
         dist.destroy_process_group()

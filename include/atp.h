@@ -329,6 +329,24 @@ atp_status atp_comm_volume(int d1, int d2, int64_t T, int64_t h, int64_t F, int 
 atp_status atp_probe_allreduce(atp_mesh* mesh, int dim, size_t msg_bytes, int iters, void* buf,
                                double* busbw_gbps, double* algbw_gbps, double* seconds);
 
+/* Full probe (S1 of SURVEY §8(a)) on a distributed mesh spanning all N ranks
+ * (any d1 x d2 = N; collective call on every rank):
+ *   - group bandwidth: busBW of the N-rank all-reduce (GroupBW of the
+ *     single-layer HCM of an NVSwitch node);
+ *   - P2P: busBW of concurrent 2-rank all-reduces, all pairs covered by a
+ *     round-robin schedule of N-1 rounds (pairs of one round run together);
+ *     reported as the minimum over pairs (p2p_min) and the full matrix
+ *     (p2p_matrix[N*N], GB/s, diagonal 0; may be NULL);
+ *   - calibration: for every mesh (d1', d2') of N, all dim-1 groups
+ *     then all dim-2 groups all-reduce `calib_bytes` per rank concurrently;
+ *     B_k = algorithm bandwidth (bytes / time, GB/s), NoComm dims report 0.
+ * Messages: bus bandwidth is the max over sizes in msg_bytes[0..n_msgs).
+ * hcm_out receives ONE layer {N, p2p_min, group}.  `scratch` is a device
+ * buffer of at least max(msg_bytes, calib_bytes) bytes.
+ * Errors: ATP_ERR_INVALID (virtual/local mesh, bad sizes), ATP_ERR_NCCL. */
+atp_status atp_probe_hcm(atp_mesh* world, const size_t* msg_bytes, int n_msgs, size_t calib_bytes, int iters,
+                         void* scratch, atp_hcm* hcm_out, double* p2p_matrix, atp_calib* calib_out);
+
 #ifdef __cplusplus
 }
 #endif

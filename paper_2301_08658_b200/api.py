@@ -297,3 +297,19 @@ def atp_probe_allreduce(mesh: Mesh, dim: int, buf, msg_bytes: int, iters: int = 
     check(lib().atp_probe_allreduce(mesh.handle, dim, msg_bytes, iters, buf.data_ptr(), C.byref(bus),
                                     C.byref(alg), C.byref(sec)))
     return {"busbw_gbps": bus.value, "algbw_gbps": alg.value, "seconds": sec.value}
+
+
+def atp_probe_hcm(mesh: Mesh, scratch, msg_bytes=(64 << 20, 256 << 20), calib_bytes=16 << 20, iters: int = 10):
+    """S1 probe on a distributed mesh of all ranks (collective).  Returns
+    (hcm layers, p2p matrix [N][N] GB/s, calibration {(d1, d2): (B1, B2)})."""
+    n = mesh.d1 * mesh.d2
+    sizes = (C.c_size_t * len(msg_bytes))(*msg_bytes)
+    H = _abi.Hcm()
+    pm = (C.c_double * (n * n))()
+    cal = _abi.Calib()
+    check(lib().atp_probe_hcm(mesh.handle, sizes, len(msg_bytes), calib_bytes, iters, scratch.data_ptr(),
+                              C.byref(H), pm, C.byref(cal)))
+    layers = [HcmLayer(H.ranks[j], H.p2p_gbps[j], H.group_gbps[j]) for j in range(H.n_layers)]
+    matrix = [[pm[i * n + j] for j in range(n)] for i in range(n)]
+    calib = {(cal.d1[k], cal.d2[k]): (cal.b1[k] or None, cal.b2[k] or None) for k in range(cal.n)}
+    return layers, matrix, calib

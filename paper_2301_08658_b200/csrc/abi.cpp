@@ -379,3 +379,142 @@ atp_status atp_probe_allreduce(atp_mesh* mesh, int dim, size_t msg_bytes, int it
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- HCM probe
+namespace {
+
+// Time `iters` in-place all-reduces of `bytes` on `comm` (every rank of the
+// parent communicator calls this together); returns seconds per all-reduce.
+double time_allreduce(ncclComm_t comm, void* buf, size_t bytes, int iters, cudaStream_t st, ncclResult_t* err) {
+  const size_t count = bytes / 2;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  *err = ncclAllReduce(buf, buf, count, ncclBfloat16, ncclSum, comm, st);  // warm-up
+  cudaEventRecord(a, st);
+  for (int i = 0; i < iters && *err == ncclSuccess; ++i) *err = ncclAllReduce(buf, buf, count, ncclBfloat16, ncclSum, comm, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return (ms * 1e-3) / iters;
+}
+
+}  // namespace
+
+extern "C" atp_status atp_probe_hcm(atp_mesh* world, const size_t* msg_bytes, int n_msgs, size_t calib_bytes,
+                                    int iters, void* scratch, atp_hcm* hcm_out, double* p2p_matrix,
+                                    atp_calib* calib_out) {
+  if (world == nullptr || world->is_virtual || world->local_only || msg_bytes == nullptr || n_msgs < 1 ||
+      iters < 1 || scratch == nullptr || hcm_out == nullptr || calib_bytes < 2)
+    return fail(ATP_ERR_INVALID, "atp_probe_hcm: needs a distributed mesh, message sizes, scratch and outputs");
+  cudaSetDevice(world->device);
+  const int N = world->d1 * world->d2;
+  const int me = world->rank;
+  cudaStream_t st = world->rs[0].comm;
+  ncclResult_t r = ncclSuccess;
+  auto nccl_fail = [&](const char* what) { return fail(ATP_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r)); };
+  auto busbw = [&](ncclComm_t c, int p, size_t bytes) {
+    const double t = time_allreduce(c, scratch, bytes, iters, st, &r);
+    return p > 1 ? (static_cast<double>(bytes) / t) * 2.0 * (p - 1) / p / 1e9 : 0.0;
+  };
+  // group bandwidth: N-rank all-reduce on the world communicator
+  double group = 0.0;
+  for (int i = 0; i < n_msgs && N > 1; ++i) {
+    const double b = busbw(world->world, N, msg_bytes[i]);
+    if (r != ncclSuccess) return nccl_fail("probe group");
+    group = b > group ? b : group;
+  }
+  // P2P: round-robin tournament (circle method) over N (or N+1 with a bye) slots
+  const int slots = N + (N & 1);
+  std::vector<double> pm(static_cast<size_t>(N) * N, 0.0);
+  for (int round = 0; round < slots - 1 && N > 1; ++round) {
+    // slot -> rank: slot 0 fixed, others rotate
+    auto rank_at = [&](int slot) { return slot == 0 ? 0 : 1 + ((slot - 1 + round) % (slots - 1)); };
+    int partner = -1, color = -1;
+    for (int k = 0; k < slots / 2; ++k) {
+      const int a = rank_at(k), b = rank_at(slots - 1 - k);
+      if (a == me && b < N) partner = b, color = k;
+      if (b == me && a < N) partner = a, color = k;
+    }
+    ncclComm_t pc = nullptr;
+    r = ncclCommSplit(world->world, partner >= 0 ? color : NCCL_SPLIT_NOCOLOR, me, &pc, nullptr);
+    if (r != ncclSuccess) return nccl_fail("probe pair split");
+    if (pc != nullptr) {
+      double best = 0.0;
+      for (int i = 0; i < n_msgs; ++i) {
+        const double b = busbw(pc, 2, msg_bytes[i]);
+        if (r != ncclSuccess) return nccl_fail("probe pair");
+        best = b > best ? b : best;
+      }
+      pm[static_cast<size_t>(me) * N + partner] = best;
+      ncclCommDestroy(pc);
+    }
+  }
+  // every rank learns the full matrix: all-reduce the (disjoint) rows in fp32 via NCCL
+  {
+    std::vector<float> h(static_cast<size_t>(N) * N);
+    for (size_t i = 0; i < h.size(); ++i) h[i] = static_cast<float>(pm[i]);
+    float* d = static_cast<float*>(scratch);
+    cudaMemcpyAsync(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, st);
+    r = ncclAllReduce(d, d, h.size(), ncclFloat32, ncclSum, world->world, st);
+    if (r != ncclSuccess) return nccl_fail("probe matrix exchange");
+    cudaMemcpyAsync(h.data(), d, h.size() * sizeof(float), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    for (size_t i = 0; i < h.size(); ++i) pm[i] = h[i];
+  }
+  double p2p_min = 0.0;
+  bool have = false;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j)
+      if (i != j) {
+        const double v = 0.5 * (pm[static_cast<size_t>(i) * N + j] + pm[static_cast<size_t>(j) * N + i]);
+        if (!have || v < p2p_min) p2p_min = v;
+        have = true;
+      }
+  if (p2p_matrix != nullptr)
+    for (size_t i = 0; i < pm.size(); ++i) p2p_matrix[i] = pm[i];
+  *hcm_out = atp_hcm{};
+  hcm_out->n_layers = 1;
+  hcm_out->ranks[0] = N;
+  hcm_out->p2p_gbps[0] = N > 1 ? p2p_min : 1.0;
+  hcm_out->group_gbps[0] = N > 1 ? group : 1.0;
+  // calibration: every mesh of N, both dimensions, all groups concurrently
+  if (calib_out != nullptr) {
+    *calib_out = atp_calib{};
+    for (int d1 = N; d1 >= 1 && calib_out->n < ATP_MAX_PLAN; --d1) {
+      if (N % d1) continue;
+      const int d2 = N / d1;
+      const int i1 = me / d2, i2 = me % d2;
+      double bk[2] = {0.0, 0.0};
+      for (int dim = 1; dim <= 2; ++dim) {
+        const int p = dim == 1 ? d1 : d2;
+        ncclComm_t c = nullptr;
+        r = ncclCommSplit(world->world, dim == 1 ? i2 : i1, dim == 1 ? i1 : i2, &c, nullptr);
+        if (r != ncclSuccess) return nccl_fail("probe calibration split");
+        if (p > 1) {
+          const double t = time_allreduce(c, scratch, calib_bytes, iters, st, &r);
+          if (r != ncclSuccess) return nccl_fail("probe calibration");
+          bk[dim - 1] = static_cast<double>(calib_bytes) / t / 1e9;
+        }
+        ncclCommDestroy(c);
+      }
+      // every rank reports the slowest group: take the max time = min bandwidth over ranks
+      float v[2] = {static_cast<float>(bk[0] > 0 ? 1.0 / bk[0] : 0.0), static_cast<float>(bk[1] > 0 ? 1.0 / bk[1] : 0.0)};
+      float* d = static_cast<float*>(scratch);
+      cudaMemcpyAsync(d, v, sizeof(v), cudaMemcpyHostToDevice, st);
+      r = ncclAllReduce(d, d, 2, ncclFloat32, ncclMax, world->world, st);
+      if (r != ncclSuccess) return nccl_fail("probe calibration exchange");
+      cudaMemcpyAsync(v, d, sizeof(v), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const int k = calib_out->n++;
+      calib_out->d1[k] = d1;
+      calib_out->d2[k] = d2;
+      calib_out->b1[k] = v[0] > 0 ? 1.0 / v[0] : 0.0;
+      calib_out->b2[k] = v[1] > 0 ? 1.0 / v[1] : 0.0;
+    }
+  }
+  return ATP_OK;
+}

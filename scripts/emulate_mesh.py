@@ -12,7 +12,6 @@ import json
 import os
 import sys
 
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 CFGS = {3: (4096, 32), 4: (5120, 40), 5: (12288, 96)}
