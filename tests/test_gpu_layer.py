@@ -199,3 +199,33 @@ def test_shape_errors_before_enqueue():
             atp.atp_layer_fwd_bwd(mesh, bufs, 64, 64, 256, 4, 3)  # T % chunks != 0
     finally:
         mesh.destroy()
+
+
+def test_probe_single_rank_and_local_mesh():
+    """atp_probe_hcm on a 1-rank NCCL mesh (the only size this box has): no
+    pairs, no groups, one calibration entry with NoComm on both dimensions;
+    and a local dry-run mesh runs a schedule with its collectives elided."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    uid = atp.atp_get_unique_id()
+    mesh = atp.Mesh.distributed(1, 1, 0, uid, 0)
+    try:
+        scratch = torch.empty(1 << 20, dtype=torch.bfloat16, device="cuda")
+        layers, matrix, calib = atp.atp_probe_hcm(mesh, scratch, msg_bytes=(1 << 20,), calib_bytes=1 << 20, iters=2)
+        assert [(l.ranks) for l in layers] == [1] and matrix == [[0.0]]
+        assert calib == {(1, 1): (None, None)}
+        plan = atp.atp_search(layers, calibration=calib)
+        assert plan["chosen"] == (1, 1)
+    finally:
+        mesh.destroy()
+    loc = atp.Mesh.local(4, 2, 3)
+    try:
+        b = atp.alloc_layer_rank(4, 2, 3, 256, 256, 1024, "cuda", 3)
+        atp.atp_layer_fwd_bwd(loc, [b], 256, 256, 1024, 8, 2, True)
+        torch.cuda.synchronize()
+        assert torch.isfinite(b["z"].float()).all() and torch.isfinite(b["dw1"]).all()
+        with pytest.raises(atp.AtpError):
+            atp.atp_probe_hcm(loc, scratch, msg_bytes=(1 << 20,))
+    finally:
+        loc.destroy()
