@@ -319,6 +319,18 @@ atp_status atp_comm_volume(int d1, int d2, int64_t T, int64_t h, int64_t F, int 
                            atp_call* calls, int cap, int* n_calls, int64_t* dim1_elems,
                            int64_t* dim2_elems);
 
+/* Chunk-overlap timing model (§4.1 Fig. 7, §4.2; SPEC's overlap
+ * module): one compute and one communication stream; stage i has compute
+ * comp[i] (its GEMM over all chunks), extra compute dw[i] after it on the
+ * compute stream (§4.2's dW GEMM) and all-reduce time comm[i]; chunks split
+ * comp and comm evenly.  mode 0 = signalled stages (the next stage's GEMM waits
+ * for the last all-reduce of the previous stage), 1 = per-chunk (chunk k waits
+ * for chunk k's all-reduce, Fig. 7).  Outputs the makespan and the exposed
+ * communication (makespan - total compute), in the inputs' time unit.
+ * Pure host code; bit-identical to oracle/overlap.py. */
+atp_status atp_overlap_estimate(int n_stages, const double* comp, const double* dw, const double* comm, int chunks,
+                                int mode, double* makespan, double* exposed);
+
 /* ------------------------------------------------------------------ probe
  * Bandwidth probe feeding the HCM (§3.4) and the calibration, on a
  * distributed mesh spanning all ranks: times ncclAllReduce on each mesh

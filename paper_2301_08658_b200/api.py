@@ -313,3 +313,13 @@ def atp_probe_hcm(mesh: Mesh, scratch, msg_bytes=(64 << 20, 256 << 20), calib_by
     matrix = [[pm[i * n + j] for j in range(n)] for i in range(n)]
     calib = {(cal.d1[k], cal.d2[k]): (cal.b1[k] or None, cal.b2[k] or None) for k in range(cal.n)}
     return layers, matrix, calib
+
+
+def atp_overlap_estimate(stages, chunks: int, mode: str = "signalled"):
+    """stages = [(comp, dw, comm), ...] -> (makespan, exposed) of the chunk pipeline model."""
+    n = len(stages)
+    arr = lambda i: (C.c_double * max(n, 1))(*[s[i] for s in stages])
+    mk, ex = C.c_double(), C.c_double()
+    check(lib().atp_overlap_estimate(n, arr(0), arr(1), arr(2), chunks, 0 if mode == "signalled" else 1,
+                                     C.byref(mk), C.byref(ex)))
+    return mk.value, ex.value

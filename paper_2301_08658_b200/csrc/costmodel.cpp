@@ -245,3 +245,47 @@ atp_status atp_comm_volume(int d1, int d2, int64_t T, int64_t h, int64_t F, int 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- overlap model
+// Event simulation of the chunk pipeline (§4.1 Fig. 7, §4.2), the same
+// max/plus operations in the same order as oracle/overlap.py.
+extern "C" atp_status atp_overlap_estimate(int n_stages, const double* comp, const double* dw, const double* comm,
+                                           int chunks, int mode, double* makespan, double* exposed) {
+  if (n_stages < 0 || chunks < 1 || (mode != 0 && mode != 1) || makespan == nullptr ||
+      (n_stages > 0 && (comp == nullptr || dw == nullptr || comm == nullptr))) {
+    atp::set_error("atp_overlap_estimate: invalid arguments");
+    return ATP_ERR_INVALID;
+  }
+  const int c = chunks;
+  std::vector<double> prev(c, 0.0), cend(c, 0.0);
+  double t_cmp = 0.0, t_com = 0.0, total = 0.0;
+  for (int s = 0; s < n_stages; ++s) {
+    const double gk = comp[s] / c, ak = comm[s] / c;
+    if (mode == 0) {
+      const double start = t_cmp > prev[c - 1] ? t_cmp : prev[c - 1];
+      for (int k = 0; k < c; ++k) cend[k] = start + (k + 1) * gk;
+      t_cmp = cend[c - 1];
+    } else {
+      for (int k = 0; k < c; ++k) {
+        const double start = t_cmp > prev[k] ? t_cmp : prev[k];
+        cend[k] = start + gk;
+        t_cmp = cend[k];
+      }
+    }
+    t_cmp = t_cmp + dw[s];
+    for (int k = 0; k < c; ++k) {
+      if (comm[s] > 0.0) {
+        const double start = t_com > cend[k] ? t_com : cend[k];
+        t_com = start + ak;
+        prev[k] = t_com;
+      } else {
+        prev[k] = cend[k];
+      }
+    }
+    total += comp[s] + dw[s];
+  }
+  const double mk = t_cmp > t_com ? t_cmp : t_com;
+  *makespan = mk;
+  if (exposed) *exposed = mk - total;
+  return ATP_OK;
+}

@@ -1,0 +1,74 @@
+"""Pins for oracle.overlap (PAPER §4.1/§4.2) and bit-exactness
+of the library's atp_overlap_estimate against it."""
+import random
+
+import pytest
+
+from oracle import overlap as ov
+
+
+def test_spec_examples():
+    # S:570-572
+    assert ov.simulate_block(10, 10, 1) == 20
+    assert ov.simulate_block(10, 10, 2) == 15
+    for c in (1, 2, 4, 8):
+        assert ov.simulate_block(10, 0, c) == 10
+
+
+@pytest.mark.parametrize("mode", ["signalled", "per_chunk"])
+def test_single_stage_equals_closed_form(mode):
+    # one stage, no dW: the event simulation is exactly SPEC's closed form
+    for comp, comm in [(10.0, 10.0), (8.0, 2.0), (2.0, 8.0), (6.0, 6.0), (16.0, 4.0)]:
+        for c in (1, 2, 4, 8):
+            mk, ex = ov.simulate([(comp, 0.0, comm)], c, mode)
+            assert mk == ov.simulate_block(comp, comm, c), (comp, comm, c)
+    rnd = random.Random(3)
+    for _ in range(500):
+        comp, comm, c = rnd.uniform(0, 5), rnd.uniform(0, 5), rnd.choice([1, 2, 3, 4, 8, 16])
+        assert abs(ov.simulate([(comp, 0.0, comm)], c, mode)[0] - ov.simulate_block(comp, comm, c)) < 1e-12
+        # SPEC invariant: non-increasing in c, bounded by max and sum
+        assert ov.simulate_block(comp, comm, 2 * c) <= ov.simulate_block(comp, comm, c) + 1e-12
+
+
+def _random_stages(rnd, n):
+    return [(rnd.uniform(0.1, 2), rnd.choice([0.0, rnd.uniform(0, 1)]), rnd.choice([0.0, rnd.uniform(0, 2)]))
+            for _ in range(n)]
+
+
+def test_bounds_serial_and_orderings():
+    rnd = random.Random(11)
+    for _ in range(300):
+        st = _random_stages(rnd, rnd.randint(1, 8))
+        comp = sum(s[0] + s[1] for s in st)
+        comm = sum(s[2] for s in st)
+        for c in (1, 2, 4, 8):
+            for mode in ("signalled", "per_chunk"):
+                mk, ex = ov.simulate(st, c, mode)
+                assert max(comp, comm) - 1e-12 <= mk <= comp + comm + 1e-12
+                assert abs(ex - (mk - comp)) < 1e-12
+            # fewer dependencies can only help: per-chunk <= signalled
+            assert ov.simulate(st, c, "per_chunk")[0] <= ov.simulate(st, c, "signalled")[0] + 1e-12
+        # c = 1 without dW: fully serial
+        st0 = [(s[0], 0.0, s[2]) for s in st]
+        assert abs(ov.simulate(st0, 1)[0] - sum(s[0] + s[2] for s in st0)) < 1e-12
+
+
+def test_dw_overlap_strictly_helps_p345():
+    # the dX all-reduce overlaps the dW GEMM
+    for c in (1, 2, 4):
+        overlapped = ov.simulate([(4.0, 3.0, 2.0)], c)[0]
+        serial = ov.simulate([(4.0, 0.0, 2.0), (3.0, 0.0, 0.0)], c)[0]
+        assert overlapped < serial
+
+
+def test_library_estimate_bit_exact():
+    import paper_2301_08658_b200 as atp
+    from paper_2301_08658_b200 import build
+
+    build.build()
+    rnd = random.Random(5)
+    for _ in range(300):
+        st = _random_stages(rnd, rnd.randint(1, 12))
+        c = rnd.choice([1, 2, 3, 4, 8, 16])
+        for mode in ("signalled", "per_chunk"):
+            assert atp.atp_overlap_estimate(st, c, mode) == ov.simulate(st, c, mode)
