@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--batch", type=int, default=4)
     p.add_argument("--seq", type=int, default=2048)
     p.add_argument("--mesh", default="", help="d1xd2; default: atp_search (uniform NVSwitch HCM, or --probe)")
+    p.add_argument("--fused-ar", action="store_true",
+                   help="N>1: fused peer-memory all-reduce (CUDA IPC) instead of NCCL on the data path")
     p.add_argument("--probe", action="store_true",
                    help="N>1: measure the HCM + per-mesh calibration with atp_probe_hcm and search on that")
     p.add_argument("--chunks", type=int, default=0, help="default 1 at N=1, 4 otherwise")
@@ -312,6 +314,9 @@ def main() -> None:
     mesh = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, uid, local_rank))
     ctas = a.gemm_ctas if a.gemm_ctas >= 0 else (0 if world == 1 else 132)
     mesh.set_gemm_ctas(ctas)
+    if a.fused_ar and world > 1:
+        # one stage's partial sums [T, widest local output] in bf16
+        mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
 
     bufs = atp.alloc_layer_rank(d1, d2, rank, T, h, F, dev, a.seed)
     call = atp.LayerCall(mesh, [bufs], T, h, F, heads, chunks, True)
@@ -463,6 +468,7 @@ def main() -> None:
                                    f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}",
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
+                       "allreduce": "fused peer-memory kernel" if (a.fused_ar and world > 1) else "nccl",
                        "mesh_source": mesh_source,
                        "l2": "working set > 126 MB L2 (weights+activations ~1-2 GB), no flush"},
             "tflops_per_gpu": per_gpu, "exposed_comm_ms": exposed, "ms_per_step_comm_disabled": ms_nocomm,

@@ -98,6 +98,19 @@ atp_status atp_mesh_groups(int d1, int d2, int dim, int* out);
  * NCCL kernel keeps SMs of its own (SURVEY §7 "SM sharing"). */
 atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas);
 
+/* Fused all-reduce over peer memory (opt-in).  Allocates this rank's
+ * peer-visible buffer (`part_bytes` for one stage's partial sums [T, width]
+ * bf16, plus counters) and maps the buffers of its dim-1 and dim-2 group
+ * members (CUDA IPC handles all-gathered over the world communicator; a
+ * virtual mesh uses the other virtual ranks' buffers).  Collective on a
+ * distributed mesh.  Afterwards every communicating bf16 stage whose output
+ * fits runs as: signalled GEMM into the buffer, then per chunk ONE kernel that
+ * all-reduces over peer memory (reduce-scatter by row slice + pull
+ * all-gather, 2(p-1)/p of the chunk per member) and applies the
+ * post-all-reduce elementwise step — no NCCL call on the data path.
+ * Errors: ATP_ERR_INVALID (already enabled), ATP_ERR_CUDA, ATP_ERR_NCCL. */
+atp_status atp_mesh_enable_fused_ar(atp_mesh* mesh, size_t part_bytes);
+
 /* Measurement hooks (bench.py).  atp_mesh_set_comm_enabled(mesh, 0) replaces
  * every all-reduce by a no-op (events still recorded, so the schedule and its
  * dependencies are unchanged): the comm-disabled twin of SURVEY §8(d) that

@@ -111,6 +111,12 @@ atp_status atp_mesh_groups(int d1, int d2, int dim, int* out) {
   return fail(ATP_ERR_INVALID, "atp_mesh_groups: dim must be 1 or 2");
 }
 
+atp_status atp_mesh_enable_fused_ar(atp_mesh* mesh, size_t part_bytes) {
+  if (mesh == nullptr || part_bytes == 0) return fail(ATP_ERR_INVALID, "atp_mesh_enable_fused_ar: bad arguments");
+  cudaSetDevice(mesh->device);
+  return static_cast<atp_status>(atp::enable_fused_ar(mesh, part_bytes));
+}
+
 atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas) {
   if (mesh == nullptr || max_ctas < 0) return fail(ATP_ERR_INVALID, "atp_mesh_set_gemm_ctas: bad arguments");
   mesh->gemm_ctas = max_ctas;

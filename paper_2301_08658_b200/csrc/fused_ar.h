@@ -1,0 +1,31 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace atp {
+
+constexpr int kSigSlots = 4096;  // per-rank counters per kind (tile, ready, done)
+
+// One fused all-reduce of one chunk (fused_ar.cu).
+struct FusedArArgs {
+  int p = 1, me = 0;                  // group size, my index in the group
+  char* peer_base[16] = {};           // members' symmetric buffers (mine at [me])
+  int64_t part_off = 0;               // byte offset of the stage's partial [T, ld] bf16 matrix
+  int64_t flag_off = 0;               // byte offset of the counters: tile[kSigSlots] ready[..] done[..]
+  int64_t ld = 0, width = 0;          // row pitch / valid columns (elements)
+  int64_t row0 = 0, rows = 0;         // the chunk's rows
+  int sig_slot = 0;
+  uint32_t sig_target = 0, ready_target = 0, done_target = 0;
+  void* out = nullptr;                // caller's output [T, ld] (gets the all-reduced values)
+  int ew_kind = -1;                   // fused elementwise step (EwKind) or -1
+  void* ew_out = nullptr;
+  const void* ew_a = nullptr;
+  int64_t ew_ld = 0, ew_lda = 0, ew_width = 0;
+  int64_t head_dim = 0;
+  int n_ctas = 16;
+};
+
+cudaError_t fused_ar_launch(const FusedArArgs& a, cudaStream_t st);
+
+}  // namespace atp

@@ -50,6 +50,23 @@ bool stream_wait_available() {
   return g_wait32 != nullptr;
 }
 
+// Fill the dynamic part of a fused all-reduce and launch it (or, with the
+// communication disabled, only account for the tile counter the GEMM bumped).
+static cudaError_t launch_fused(atp_mesh* m, RankState& s, const Op& op, cudaStream_t st) {
+  FusedArArgs a = op.far;
+  const int d = op.ar_dim - 1;
+  a.p = op.ar_dim == 1 ? m->d1 : m->d2;
+  a.me = s.me_in[d];
+  for (int j = 0; j < a.p; ++j) a.peer_base[j] = s.peers[d][j];
+  s.sig_total[a.sig_slot] += op.sig_inc;
+  if (!m->comm_enabled) return cudaSuccess;
+  a.sig_target = s.sig_total[a.sig_slot];
+  a.ready_target = (s.ready_total[a.sig_slot] += static_cast<uint32_t>(a.n_ctas));
+  a.done_target = (s.done_total[a.sig_slot] += static_cast<uint32_t>(a.p * a.n_ctas));
+  count_launch(1);
+  return fused_ar_launch(a, st);
+}
+
 static cudaError_t wait_sig(RankState& s, const Op& op, cudaStream_t st) {
   s.sig_total[op.sig_slot] += op.sig_inc;
   CUresult r = g_wait32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(s.sig_buf + op.sig_slot),
@@ -118,6 +135,8 @@ RankView rank_view(const atp_mesh* m, int r) {
   }
   v.gemm_ctas = m->gemm_ctas;
   v.sig_buf = m->rs[m->is_virtual ? r : 0].sig_buf;
+  v.sym_base = m->rs[m->is_virtual ? r : 0].sym_base;
+  v.sym_part_bytes = m->rs[m->is_virtual ? r : 0].sym_part_bytes;
   v.signalled = m->signalled && stream_wait_available();
   return v;
 }
@@ -186,7 +205,9 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
         continue;
       }
       ProfRec* pr = prof_begin(m, op, st);
-      if (op.kind == OP_AR) {
+      if (op.kind == OP_FUSED_AR) {
+        if ((e = launch_fused(m, s, op, st)) != cudaSuccess) return cuda_fail(e, "fused all-reduce launch");
+      } else if (op.kind == OP_AR) {
         if (m->comm_enabled) {
           ncclComm_t comm = op.ar_dim == 1 ? m->dim1 : m->dim2;
           ncclResult_t nr = ncclAllReduce(op.ar_ptr, op.ar_ptr, static_cast<size_t>(op.ar_count),
@@ -229,8 +250,11 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
           continue;
         }
         ProfRec* pr = prof_begin(m, op, st);
-        if ((e = launch_local(op, st)) != cudaSuccess)
+        if (op.kind == OP_FUSED_AR) {
+          if ((e = launch_fused(m, s, op, st)) != cudaSuccess) return cuda_fail(e, "fused all-reduce launch");
+        } else if ((e = launch_local(op, st)) != cudaSuccess) {
           return cuda_fail(e, op.kind == OP_GEMM ? "gemm launch" : "elementwise launch");
+        }
         prof_end(pr, st);
         if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
       }
@@ -287,6 +311,85 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
   return 0;
 }
 
+// ---------------------------------------------------------------- fused all-reduce setup
+// Every rank gets one "symmetric" allocation: the partial-sum region followed by
+// its counters (tile / ready / done).  The GEMM counters move into it so peers
+// can read them.  Virtual mesh: peers are the other virtual ranks' allocations;
+// distributed mesh: CUDA IPC handles all-gathered over the world communicator
+// and opened for the members of this rank's dim-1 and dim-2 groups.
+int enable_fused_ar(atp_mesh* m, size_t part_bytes) {
+  part_bytes = (part_bytes + 255) & ~static_cast<size_t>(255);
+  const size_t flag_bytes = 3 * static_cast<size_t>(kSigSlots) * sizeof(uint32_t);
+  const int n_local = static_cast<int>(m->rs.size());
+  for (int r = 0; r < n_local; ++r) {
+    RankState& s = m->rs[r];
+    if (s.sym_base != nullptr) {
+      set_error("fused all-reduce already enabled on this mesh");
+      return 1;
+    }
+    cudaError_t e = cudaMalloc(&s.sym_base, part_bytes + flag_bytes);
+    if (e == cudaSuccess) e = cudaMemset(s.sym_base + part_bytes, 0, flag_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "fused all-reduce buffer");
+    s.sym_part_bytes = part_bytes;
+    if (s.sig_owned) cudaFree(s.sig_buf);
+    s.sig_buf = reinterpret_cast<uint32_t*>(s.sym_base + part_bytes);
+    s.sig_owned = false;
+    s.sig_total.assign(kSigSlots, 0u);
+    s.ready_total.assign(kSigSlots, 0u);
+    s.done_total.assign(kSigSlots, 0u);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "fused all-reduce setup");
+  const int d1 = m->d1, d2 = m->d2;
+  if (m->is_virtual) {
+    for (int r = 0; r < n_local; ++r) {
+      const int i1 = r / d2, i2 = r % d2;
+      RankState& s = m->rs[r];
+      for (int j = 0; j < d1; ++j) s.peers[0][j] = m->rs[j * d2 + i2].sym_base;
+      for (int j = 0; j < d2; ++j) s.peers[1][j] = m->rs[i1 * d2 + j].sym_base;
+      s.me_in[0] = i1;
+      s.me_in[1] = i2;
+    }
+    return 0;
+  }
+  RankState& s = m->rs[0];
+  const int n = d1 * d2;
+  std::vector<cudaIpcMemHandle_t> all(n);
+  if (!m->local_only && n > 1) {
+    cudaIpcMemHandle_t h;
+    if ((e = cudaIpcGetMemHandle(&h, s.sym_base)) != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    uint8_t* dbuf = nullptr;
+    if ((e = cudaMalloc(&dbuf, sizeof(h) * (n + 1))) != cudaSuccess) return cuda_fail(e, "ipc exchange buffer");
+    cudaMemcpy(dbuf, &h, sizeof(h), cudaMemcpyHostToDevice);
+    ncclResult_t r = ncclAllGather(dbuf, dbuf + sizeof(h), sizeof(h), ncclUint8, m->world, s.comm);
+    cudaStreamSynchronize(s.comm);
+    if (r == ncclSuccess) cudaMemcpy(all.data(), dbuf + sizeof(h), sizeof(h) * n, cudaMemcpyDeviceToHost);
+    cudaFree(dbuf);
+    if (r != ncclSuccess) {
+      set_error(std::string("ipc handle exchange: ") + ncclGetErrorString(r));
+      return 4;
+    }
+  }
+  auto open = [&](int rank) -> char* {
+    if (rank == m->rank || m->local_only) return s.sym_base;
+    void* p = nullptr;
+    cudaError_t err = cudaIpcOpenMemHandle(&p, all[rank], cudaIpcMemLazyEnablePeerAccess);
+    if (err != cudaSuccess) {
+      cuda_fail(err, "cudaIpcOpenMemHandle");
+      return nullptr;
+    }
+    s.ipc_opened.push_back(static_cast<char*>(p));
+    return static_cast<char*>(p);
+  };
+  for (int j = 0; j < d1; ++j)
+    if (!(s.peers[0][j] = open(j * d2 + m->i2))) return 3;
+  for (int j = 0; j < d2; ++j)
+    if (!(s.peers[1][j] = open(m->i1 * d2 + j))) return 3;
+  s.me_in[0] = m->i1;
+  s.me_in[1] = m->i2;
+  return 0;
+}
+
 // ---------------------------------------------------------------- mesh lifetime
 static int make_rank_state(RankState& s, bool with_compute) {
   int lo, hi;
@@ -312,7 +415,9 @@ static void free_rank_state(RankState& s) {
   if (s.join) cudaEventDestroy(s.join);
   if (s.comm) cudaStreamDestroy(s.comm);
   if (s.compute) cudaStreamDestroy(s.compute);
-  if (s.sig_buf) cudaFree(s.sig_buf);
+  if (s.sig_buf && s.sig_owned) cudaFree(s.sig_buf);
+  for (char* p : s.ipc_opened) cudaIpcCloseMemHandle(p);
+  if (s.sym_base) cudaFree(s.sym_base);
   s = RankState();
 }
 

@@ -8,6 +8,7 @@
 
 #include "atp_internal.h"
 #include "elementwise.h"
+#include "fused_ar.h"
 
 struct atp_mesh;
 
@@ -15,9 +16,9 @@ namespace atp {
 
 void set_error(const std::string& msg);
 
-enum OpKind : int { OP_GEMM = 0, OP_EW = 1, OP_AR = 2, OP_WAITSIG = 3 };
+enum OpKind : int { OP_GEMM = 0, OP_EW = 1, OP_AR = 2, OP_WAITSIG = 3, OP_FUSED_AR = 4 };
 
-constexpr int kSigSlots = 4096;  // per-rank chunk-completion counters
+// kSigSlots (fused_ar.h): per-rank chunk-completion counters
 constexpr int kMaxChunks = 16;   // chunk count limit (bounds the waits of one op)
 
 // One enqueue on one of a rank's two streams.  `waits` are schedule-local
@@ -38,6 +39,9 @@ struct Op {
   // `sig_inc` since the previous wait on that slot (cyclic >=).
   int sig_slot = 0;
   uint32_t sig_inc = 0;
+  // OP_FUSED_AR: static part of the fused all-reduce (targets and peer
+  // pointers are filled in by the executor); ar_dim names the group.
+  FusedArArgs far;
 };
 
 struct Sched {
@@ -50,6 +54,8 @@ struct RankView {
   int gemm_ctas = 0;
   uint32_t* sig_buf = nullptr;  // this rank's chunk-completion counters (device)
   bool signalled = true;        // use signalled stages when possible
+  char* sym_base = nullptr;     // fused all-reduce: this rank's peer-visible buffer
+  size_t sym_part_bytes = 0;    //   capacity of its partial-sum region
 };
 
 struct RankState {
@@ -58,7 +64,16 @@ struct RankState {
   std::vector<cudaEvent_t> ev;
   cudaEvent_t arrive = nullptr, done = nullptr, join = nullptr;
   uint32_t* sig_buf = nullptr;       // device counters [kSigSlots]
+  bool sig_owned = true;             // false once moved into the symmetric buffer
   std::vector<uint32_t> sig_total;   // host mirror of the values the counters reach
+  // fused all-reduce ("symmetric" buffer: partials [part_bytes] + counters
+  // tile[kSigSlots] ready[kSigSlots] done[kSigSlots]); peers per mesh dim
+  char* sym_base = nullptr;
+  size_t sym_part_bytes = 0;
+  char* peers[2][16] = {};  // [dim-1][member index] -> member's sym_base
+  int me_in[2] = {0, 0};
+  std::vector<char*> ipc_opened;
+  std::vector<uint32_t> ready_total, done_total;
 };
 
 }  // namespace atp
@@ -97,5 +112,7 @@ void count_launch(uint64_t n);
 uint64_t launch_count();
 void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes);
 bool stream_wait_available();
+int enable_fused_ar(atp_mesh* m, size_t part_bytes);
+constexpr int kFusedCtas = 16;
 
 }  // namespace atp

@@ -177,6 +177,56 @@ struct Builder {
     const void* bias_here = coord0(dim) ? bias : nullptr;
     int bn = 128, cg = 1;  // fp32 check mode: 128 x 128 tiles
     if (dtype == 0) gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
+    if (rv.sym_base != nullptr && dtype == 0 && Mc % (128 * cg) == 0 &&
+        static_cast<size_t>(T) * out_w * 2 <= rv.sym_part_bytes && next_slot + chunks <= kSigSlots) {
+      // ---- fused stage: the GEMM writes its partial sums into this rank's
+      // peer-visible buffer and counts tiles per chunk; per chunk, ONE kernel
+      // all-reduces over peer memory and applies the elementwise step.
+      std::vector<int> waits = prologue_all();
+      EpiParams ep;
+      ep.C = rv.sym_base;
+      ep.ldc = out_w;
+      ep.bias = bias_here;
+      Op* g = gemm(in, in_w, false, w, ldw, b_mn, T, out_w, in_w, EPI_BF16, ep, waits, -1);
+      if (!g) return false;
+      const int slot0 = next_slot;
+      next_slot += chunks;
+      g->g.sig = rv.sig_buf + slot0;
+      g->g.sig_rows = static_cast<int>(Mc);
+      const uint32_t per_chunk = static_cast<uint32_t>((Mc / 128) * ((out_w + g->g.bn - 1) / g->g.bn));
+      if (!extra()) return false;
+      const EwList post = after_ar(0, 0, T);  // base pointers of the elementwise step
+      for (int k = 0; k < chunks; ++k) {
+        Op& o = push(OP_FUSED_AR, 1);
+        o.ar_dim = dim;
+        o.ar_count = Mc * out_w;
+        o.sig_inc = per_chunk;
+        FusedArArgs& f = o.far;
+        f.part_off = 0;
+        f.flag_off = static_cast<int64_t>(rv.sym_part_bytes);
+        f.ld = out_w;
+        f.width = out_w;
+        f.row0 = k * Mc;
+        f.rows = Mc;
+        f.sig_slot = slot0 + k;
+        f.out = out;
+        f.n_ctas = kFusedCtas;
+        if (!post.empty()) {
+          const EwDesc& e = post[0];
+          f.ew_kind = e.kind;
+          f.ew_out = e.out;
+          f.ew_a = e.a;
+          f.ew_ld = e.kind == EW_CORE_BWD ? 3 * e.cols : e.cols;
+          f.ew_lda = e.cols;
+          f.ew_width = e.cols;
+          f.head_dim = e.cols / e.heads;
+        }
+      }
+      const int last = ev();
+      s.ops.back().record = last;
+      for (int k = 0; k < chunks; ++k) pend[k] = last;
+      return true;
+    }
     if (rv.signalled && rv.sig_buf != nullptr && chunks > 1 && Mc % (128 * cg) == 0 &&
         next_slot + chunks <= kSigSlots) {
       // ---- signalled stage: one GEMM over all T rows, per-chunk counters

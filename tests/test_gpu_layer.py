@@ -229,3 +229,33 @@ def test_probe_single_rank_and_local_mesh():
             atp.atp_probe_hcm(loc, scratch, msg_bytes=(1 << 20,))
     finally:
         loc.destroy()
+
+
+@pytest.mark.parametrize("d1,d2", [(2, 1), (1, 2), (2, 2), (4, 2), (2, 4), (8, 1), (1, 8)])
+@pytest.mark.parametrize("chunks", [1, 4])
+def test_layer_fused_peer_allreduce(d1, d2, chunks):
+    """Fused stages: signalled GEMM into the peer-visible buffer + one kernel
+    per chunk doing the grouped all-reduce over peer memory with the
+    elementwise step fused; parity, replicas and a repeated call."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, seed = 1024, 512, 2048, 8, 31
+    g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, d1, d2, chunks, seed)
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        mesh.enable_fused_ar(T * F * 2)
+        bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(d1 * d2)]
+        call = atp.LayerCall(mesh, bufs, T, h, F, heads, chunks, True)
+        call()
+        torch.cuda.synchronize()
+        snap = [{k: b[k].clone() for k in ("z", "dx", "dw1", "dwqkv")} for b in bufs]
+        call()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    compare(bufs, fw, bw, d1, d2)
+    check_replicas(bufs, d1, d2)
+    for b, s in zip(bufs, snap):
+        for k, v in s.items():
+            assert torch.equal(b[k], v), k
