@@ -107,59 +107,63 @@ __global__ void __launch_bounds__(512) fused_ar_kernel(FusedArArgs a) {
     atomicAdd(my_flags + kSigSlots + a.sig_slot, 1u);  // ready
   }
 
-  // ---- 3. all-gather by pull + the stage's elementwise step, row by row
+  // ---- 3. all-gather by pull + the stage's elementwise step: a flat
+  // grid-stride loop over (row, 8-column vector) pairs of each slice.  For the
+  // stand-in core the loop runs over ctx vectors and pulls the q, k, v vectors
+  // of the head (each is written exactly once), so no intra-row sync is needed.
+  const bool core_fwd = a.ew_kind == EW_CORE_FWD;
+  const int64_t vec_per_row = core_fwd ? a.ew_width / 8 : w8;
   for (int j = 0; j < a.p; ++j) {
     if (tid == 0)
       spin_geq(reinterpret_cast<const uint32_t*>(a.peer_base[j] + a.flag_off) + kSigSlots + a.sig_slot, a.ready_target);
     __syncthreads();
     const int64_t r0 = slice_begin(j), r1 = slice_begin(j + 1);
-    for (int64_t row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
+    const int64_t n = (r1 - r0) * vec_per_row;
+    for (int64_t i = blockIdx.x * (int64_t)nt + tid; i < n; i += (int64_t)gridDim.x * nt) {
+      const int64_t row = r0 + i / vec_per_row, c8 = (i % vec_per_row) * 8;
       bf* orow = static_cast<bf*>(a.out) + row * a.ld;
       const bf* src = part(j, row);
-      for (int64_t c = tid; c < w8; c += nt) {
-        float v[8];
-        load8(src + 8 * c, v);  // the all-reduced (bf16) values
-        if (a.ew_kind == EW_GELU) {
-          float h[8];
+      if (core_fwd) {
+        const int64_t hd = c8 / a.head_dim, jj = c8 % a.head_dim;
+        const int64_t q = hd * 3 * a.head_dim + jj;
+        float x[8], k[8], v[8];
+        load8(src + q, x);
+        load8(src + q + a.head_dim, k);
+        load8(src + q + 2 * a.head_dim, v);
+        store8(orow + q, x);
+        store8(orow + q + a.head_dim, k);
+        store8(orow + q + 2 * a.head_dim, v);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) h[e] = gelu_f(v[e]);
-          store8(static_cast<bf*>(a.ew_out) + row * a.ew_ld + 8 * c, h);
-        } else if (a.ew_kind == EW_DGELU) {
-          float u[8];
-          load8(static_cast<const bf*>(a.ew_a) + row * a.ew_lda + 8 * c, u);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] *= gelu_grad_f(u[e]);
-        } else if (a.ew_kind == EW_ADD) {
-          float x[8];
-          load8(static_cast<const bf*>(a.ew_a) + row * a.ew_lda + 8 * c, x);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = x[e] + v[e];
-        } else if (a.ew_kind == EW_CORE_BWD) {
-          // dQ = dK = dV = dctx of the head (row-local)
-          const int64_t col = 8 * c, hd = col / a.head_dim, jj = col % a.head_dim;
-          bf* dst = static_cast<bf*>(a.ew_out) + row * a.ew_ld + hd * 3 * a.head_dim + jj;
-          store8(dst, v);
-          store8(dst + a.head_dim, v);
-          store8(dst + 2 * a.head_dim, v);
-        }
-        store8(orow + 8 * c, v);
+        for (int e = 0; e < 8; ++e) x[e] = (x[e] + k[e]) + v[e];
+        store8(static_cast<bf*>(a.ew_out) + row * a.ew_ld + c8, x);
+        continue;
       }
-      if (a.ew_kind == EW_CORE_FWD) {
-        // ctx = Q + K + V per head, from the all-reduced QKV row just written
-        __syncthreads();
-        const int64_t wc8 = a.ew_width / 8;
-        for (int64_t c = tid; c < wc8; c += nt) {
-          const int64_t col = 8 * c, hd = col / a.head_dim, jj = col % a.head_dim;
-          const bf* q = orow + hd * 3 * a.head_dim + jj;
-          float s[8], k[8], vv[8];
-          load8(q, s);
-          load8(q + a.head_dim, k);
-          load8(q + 2 * a.head_dim, vv);
+      float v[8];
+      load8(src + c8, v);  // the all-reduced (bf16) values
+      if (a.ew_kind == EW_GELU) {
+        float h[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) s[e] = (s[e] + k[e]) + vv[e];
-          store8(static_cast<bf*>(a.ew_out) + row * a.ew_ld + col, s);
-        }
+        for (int e = 0; e < 8; ++e) h[e] = gelu_f(v[e]);
+        store8(static_cast<bf*>(a.ew_out) + row * a.ew_ld + c8, h);
+      } else if (a.ew_kind == EW_DGELU) {
+        float u[8];
+        load8(static_cast<const bf*>(a.ew_a) + row * a.ew_lda + c8, u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] *= gelu_grad_f(u[e]);
+      } else if (a.ew_kind == EW_ADD) {
+        float x[8];
+        load8(static_cast<const bf*>(a.ew_a) + row * a.ew_lda + c8, x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = x[e] + v[e];
+      } else if (a.ew_kind == EW_CORE_BWD) {
+        // dQ = dK = dV = dctx of the head (row-local)
+        const int64_t hd = c8 / a.head_dim, jj = c8 % a.head_dim;
+        bf* dst = static_cast<bf*>(a.ew_out) + row * a.ew_ld + hd * 3 * a.head_dim + jj;
+        store8(dst, v);
+        store8(dst + a.head_dim, v);
+        store8(dst + 2 * a.head_dim, v);
       }
+      store8(orow + c8, v);
     }
   }
 

@@ -59,7 +59,9 @@ static cudaError_t launch_fused(atp_mesh* m, RankState& s, const Op& op, cudaStr
   a.me = s.me_in[d];
   for (int j = 0; j < a.p; ++j) a.peer_base[j] = s.peers[d][j];
   s.sig_total[a.sig_slot] += op.sig_inc;
-  if (!m->comm_enabled) return cudaSuccess;
+  // a local dry-run mesh runs the kernel against its own buffer only (every
+  // "peer" is itself): the per-rank cost of the fused step without NVLink.
+  if (!m->comm_enabled && !m->local_only) return cudaSuccess;
   a.sig_target = s.sig_total[a.sig_slot];
   a.ready_target = (s.ready_total[a.sig_slot] += static_cast<uint32_t>(a.n_ctas));
   a.done_target = (s.done_total[a.sig_slot] += static_cast<uint32_t>(a.p * a.n_ctas));
@@ -191,13 +193,14 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   for (int r = 0; r < n; ++r) {
     cudaStreamWaitEvent(m->rs[r].comm, m->ev_start, 0);
+    cudaStreamWaitEvent(m->rs[r].aux, m->ev_start, 0);
     if (m->is_virtual) cudaStreamWaitEvent(m->rs[r].compute, m->ev_start, 0);
   }
 
   if (!m->is_virtual) {
     RankState& s = m->rs[0];
     for (const Op& op : sch[0].ops) {
-      cudaStream_t st = op.stream ? s.comm : stream;
+      cudaStream_t st = op.stream == 1 ? s.comm : (op.stream == 2 ? s.aux : stream);
       if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
       if (op.kind == OP_WAITSIG) {
         if ((e = wait_sig(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWaitValue32");
@@ -225,6 +228,8 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
     }
     cudaEventRecord(s.join, s.comm);
     cudaStreamWaitEvent(stream, s.join, 0);
+    cudaEventRecord(s.join, s.aux);
+    cudaStreamWaitEvent(stream, s.join, 0);
     return 0;
   }
 
@@ -242,7 +247,7 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
       for (int r = 0; r < n; ++r) {
         const Op& op = sch[r].ops[i];
         RankState& s = m->rs[r];
-        cudaStream_t st = op.stream ? s.comm : s.compute;
+        cudaStream_t st = op.stream == 1 ? s.comm : (op.stream == 2 ? s.aux : s.compute);
         if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
         if (op.kind == OP_WAITSIG) {
           if ((e = wait_sig(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWaitValue32");
@@ -305,6 +310,8 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
     cudaEventRecord(s.join, s.comm);
     cudaStreamWaitEvent(stream, s.join, 0);
     cudaEventRecord(s.join, s.compute);
+    cudaStreamWaitEvent(stream, s.join, 0);
+    cudaEventRecord(s.join, s.aux);
     cudaStreamWaitEvent(stream, s.join, 0);
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "virtual executor");
@@ -396,6 +403,7 @@ static int make_rank_state(RankState& s, bool with_compute) {
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   cudaError_t e = cudaStreamCreateWithPriority(&s.comm, cudaStreamNonBlocking, hi);
   if (e == cudaSuccess && with_compute) e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&s.aux, cudaStreamNonBlocking, lo);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.arrive, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming);
@@ -415,6 +423,7 @@ static void free_rank_state(RankState& s) {
   if (s.join) cudaEventDestroy(s.join);
   if (s.comm) cudaStreamDestroy(s.comm);
   if (s.compute) cudaStreamDestroy(s.compute);
+  if (s.aux) cudaStreamDestroy(s.aux);
   if (s.sig_buf && s.sig_owned) cudaFree(s.sig_buf);
   for (char* p : s.ipc_opened) cudaIpcCloseMemHandle(p);
   if (s.sym_base) cudaFree(s.sym_base);
@@ -494,6 +503,7 @@ int mesh_destroy(atp_mesh* m) {
   for (auto& s : m->rs) {
     if (s.comm) cudaStreamSynchronize(s.comm);
     if (s.compute) cudaStreamSynchronize(s.compute);
+    if (s.aux) cudaStreamSynchronize(s.aux);
   }
   if (m->dim2) ncclCommDestroy(m->dim2);
   if (m->dim1) ncclCommDestroy(m->dim1);

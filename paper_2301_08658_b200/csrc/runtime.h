@@ -25,7 +25,7 @@ constexpr int kMaxChunks = 16;   // chunk count limit (bounds the waits of one o
 // event ids the op's stream waits on first; `record` is recorded after it.
 struct Op {
   OpKind kind = OP_GEMM;
-  int stream = 0;  // 0 = compute (caller's stream), 1 = communication
+  int stream = 0;  // 0 = compute (caller's stream), 1 = communication, 2 = auxiliary
   int waits[kMaxChunks] = {};
   int n_waits = 0;
   int record = -1;
@@ -61,6 +61,7 @@ struct RankView {
 struct RankState {
   cudaStream_t comm = nullptr;
   cudaStream_t compute = nullptr;  // virtual mesh only (one per virtual rank)
+  cudaStream_t aux = nullptr;      // off-critical-path work (bias-gradient column sums)
   std::vector<cudaEvent_t> ev;
   cudaEvent_t arrive = nullptr, done = nullptr, join = nullptr;
   uint32_t* sig_buf = nullptr;       // device counters [kSigSlots]
@@ -113,6 +114,6 @@ uint64_t launch_count();
 void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes);
 bool stream_wait_available();
 int enable_fused_ar(atp_mesh* m, size_t part_bytes);
-constexpr int kFusedCtas = 16;
+constexpr int kFusedCtas = 16;  // CTAs of one fused all-reduce kernel (fits the SMs the GEMM cap leaves)
 
 }  // namespace atp

@@ -35,6 +35,7 @@
 // Bias placement (reading G16): a bias is added exactly once per reduction
 // group — in the GEMM epilogue of the coordinate-0 rank before the all-reduce,
 // or unconditionally when the reducing dimension has size 1.
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -55,6 +56,15 @@ inline const char* cptr(const void* p, int64_t off_elems) {
 inline char* mptr(void* p, int64_t off_elems) { return static_cast<char*>(p) + off_elems * g_esz; }
 
 using EwList = std::vector<EwDesc>;
+
+// ATP_AUX_COLSUM=0 keeps the bias-gradient column sums on the compute stream (A/B runs).
+bool aux_colsum() {
+  static const bool on = [] {
+    const char* e = getenv("ATP_AUX_COLSUM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 struct Builder {
   Sched s;
@@ -273,12 +283,25 @@ struct Builder {
     return extra();
   }
 
-  // dW[x_w, dy_w] (fp32) = X[T, x_w]^T dY[T, dy_w]  (both MN-major), + dbias = colsum(dY)
+  // Event marking "everything enqueued on the compute stream so far is done"
+  // (reuses the last compute op's record event); -1 if there is none.
+  int mark_compute() {
+    for (auto it = s.ops.rbegin(); it != s.ops.rend(); ++it) {
+      if (it->stream != 0) continue;
+      if (it->record < 0) it->record = ev();
+      return it->record;
+    }
+    return -1;
+  }
+
+  // dW[x_w, dy_w] (fp32) = X[T, x_w]^T dY[T, dy_w]  (both MN-major), + dbias = colsum(dY).
+  // The column sum is HBM-bound and nothing downstream needs it: it runs on the
+  // auxiliary stream, gated on the compute stream having produced dY, so it
+  // overlaps the compute-bound dW GEMM instead of sitting between GEMMs.
   bool dw(const void* x, int64_t x_w, const void* dy, int64_t dy_w, float* dwp, float* dbias) {
     EpiParams ep;
     ep.C = dwp;
     ep.ldc = dy_w;
-    if (dwp != nullptr && !gemm(x, x_w, true, dy, dy_w, true, x_w, dy_w, T, EPI_F32, ep, {}, -1)) return false;
     if (dbias != nullptr) {
       EwDesc e;
       e.kind = EW_COLSUM;
@@ -286,10 +309,12 @@ struct Builder {
       e.a = dy;
       e.rows = T;
       e.cols = dy_w;
-      ew(e, 0);
+      ew(e, aux_colsum() ? 2 : 0, mark_compute());
     }
+    if (dwp != nullptr && !gemm(x, x_w, true, dy, dy_w, true, x_w, dy_w, T, EPI_F32, ep, {}, -1)) return false;
     return true;
   }
+
   // Remaining deferred work; a trailing all-reduce with no consumer is joined
   // by the executor.
   void flush() { prologue_all(); }

@@ -24,6 +24,9 @@ def main():
     p.add_argument("--meshes", default="8x1,4x2,2x4,1x8")
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--tokens", type=int, default=8192)
+    p.add_argument("--gemm-ctas", type=int, default=132)
+    p.add_argument("--fused-ar", action="store_true",
+                   help="fused peer-memory all-reduce stages (run against the rank's own buffer)")
     a = p.parse_args()
     import torch
     import paper_2301_08658_b200 as atp
@@ -37,6 +40,9 @@ def main():
             if heads % d1:
                 continue
             mesh = atp.Mesh.local(d1, d2, 0)
+            mesh.set_gemm_ctas(a.gemm_ctas)  # the N>1 default of bench.py: SMs left for the communication kernels
+            if a.fused_ar:
+                mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
             bufs = atp.alloc_layer_rank(d1, d2, 0, T, h, F, "cuda", 2301)
             for c in [int(x) for x in a.chunks.split(",")]:
                 call = atp.LayerCall(mesh, [bufs], T, h, F, heads, c, True)
@@ -52,7 +58,7 @@ def main():
                 ms = e0.elapsed_time(e1) / a.steps
                 fl = 72.0 * T * h * h / (d1 * d2)
                 print(json.dumps({"cfg": cfg, "h": h, "mesh": [d1, d2], "chunks": c, "ms_compute_per_rank": round(ms, 4),
-                                  "tflops_per_rank": round(fl / ms / 1e9, 1)}), flush=True)
+                                  "tflops_per_rank": round(fl / ms / 1e9, 1), "fused_ar": a.fused_ar}), flush=True)
             del bufs
             mesh.destroy()
             torch.cuda.empty_cache()
