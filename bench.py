@@ -59,7 +59,10 @@ def parse():
                    help="N>1: fused peer-memory all-reduce (CUDA IPC) instead of NCCL on the data path")
     p.add_argument("--probe", action="store_true",
                    help="N>1: measure the HCM + per-mesh calibration with atp_probe_hcm and search on that")
-    p.add_argument("--chunks", type=int, default=0, help="default 1 at N=1, 4 otherwise")
+    p.add_argument("--chunks", type=int, default=0,
+                   help="0 = 1 at N=1; at N>1 chosen by the overlap model from measured compute (planner.py)")
+    p.add_argument("--busbw", type=float, default=725.0,
+                   help="all-reduce bus GB/s for the chunk planner (8-rank NCCL on this pool, B200_PROFILING.md)")
     p.add_argument("--gemm-ctas", type=int, default=-1, help="GEMM CTA cap (default: all SMs at N=1, SMs-16 else)")
     p.add_argument("--seed", type=int, default=2301)
     p.add_argument("--no-e2e", action="store_true")
@@ -271,7 +274,7 @@ def main() -> None:
     h, heads = a.hidden, a.heads
     F = a.ffn or 4 * h
     T = a.batch * a.seq
-    chunks = a.chunks or (1 if world == 1 else 4)
+    chunks = a.chunks or (1 if world == 1 else 4)  # N>1 with --chunks 0: replaced by the planner below
 
     # ---- mesh: explicit, or ATP's search (§3.5) on the single-layer NVSwitch HCM
     # (P:488, 900 GB/s per direction), or with --probe on the HCM measured by
@@ -319,7 +322,6 @@ def main() -> None:
         mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
 
     bufs = atp.alloc_layer_rank(d1, d2, rank, T, h, F, dev, a.seed)
-    call = atp.LayerCall(mesh, [bufs], T, h, F, heads, chunks, True)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -327,12 +329,13 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(n_steps: int) -> float:
+    def timed(n_steps: int, fn=None) -> float:
+        fn = fn or call
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(n_steps):
-            call(stream)
+            fn(stream)
         e1.record(stream)
         e1.synchronize()
         ms = e0.elapsed_time(e1) / n_steps
@@ -342,6 +345,28 @@ def main() -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
+
+    # ---- chunk count (N>1, --chunks 0): measure the compute side of each
+    # candidate with the all-reduces disabled, predict the step with the overlap
+    # model (planner.py, §4.1/§4.2) at --busbw, take the fastest (same on every
+    # rank: the timings are max-reduced over ranks before the choice).
+    chunk_choice = None
+    if world > 1 and a.chunks == 0 and (d1 > 1 or d2 > 1):
+        from paper_2301_08658_b200 import planner
+
+        comp = {}
+        _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 0))
+        for c in (1, 2, 4, 8):
+            if T % c or (T // c) % 8:
+                continue
+            cc = atp.LayerCall(mesh, [bufs], T, h, F, heads, c, True)
+            for _ in range(2):
+                cc(stream)
+            comp[c] = timed(5, cc)
+        _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 1))
+        chunks, pred = planner.choose_chunks(T, h, F, d1, d2, comp, a.busbw)
+        chunk_choice = {"compute_ms": comp, "predicted_ms": pred, "busbw_gbs": a.busbw, "chosen": chunks}
+    call = atp.LayerCall(mesh, [bufs], T, h, F, heads, chunks, True)
 
     for _ in range(max(3, a.warmup)):
         call(stream)
@@ -475,6 +500,8 @@ def main() -> None:
             "flops_per_step": fl, "clocks": clocks, "gpu_launches": launches,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
         }
+        if chunk_choice is not None:
+            out["chunk_choice"] = chunk_choice
         if plan is not None:
             out["search"] = {"chosen": plan["chosen"], "ranked": [(r["d1"], r["d2"], r["t_comm"], r["calibrated"])
                                                                    for r in plan["ranked"]]}

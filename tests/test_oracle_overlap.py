@@ -72,3 +72,26 @@ def test_library_estimate_bit_exact():
         c = rnd.choice([1, 2, 3, 4, 8, 16])
         for mode in ("signalled", "per_chunk"):
             assert atp.atp_overlap_estimate(st, c, mode) == ov.simulate(st, c, mode)
+
+
+def test_chunk_planner():
+    """planner: per-stage split conserves the measured compute and the executed
+    all-reduce bytes (oracle comm_volume); more chunks win when compute is
+    chunk-invariant; the per-chunk compute penalty can make fewer chunks win."""
+    from oracle import costmodel as cm
+    from paper_2301_08658_b200 import build, planner
+
+    build.build()
+    T, h, F = 8192, 4096, 16384
+    for d1, d2 in [(8, 1), (4, 2), (2, 4), (1, 1)]:
+        st = planner.layer_stages(T, h, F, d1, d2, 2.0, 725.0)
+        assert abs(sum(s[0] + s[1] for s in st) - 2.0) < 1e-12
+        ring = cm.ring_bytes_per_gpu(cm.comm_volume(d1, d2, T, h, 1))
+        assert abs(sum(s[2] for s in st) - ring / 725e9 * 1e3) < 1e-9
+    c, pred = planner.choose_chunks(T, h, F, 4, 2, {1: 1.3, 2: 1.3, 4: 1.3, 8: 1.3}, 725.0)
+    assert c == 8 and pred[8] <= pred[4] <= pred[2] <= pred[1]
+    c, pred = planner.choose_chunks(T, h, F, 4, 2, {1: 1.2, 2: 1.25, 4: 1.6, 8: 2.5}, 725.0)
+    assert c == 2
+    # no communication (1,1): chunking cannot help
+    c, _ = planner.choose_chunks(T, h, F, 1, 1, {1: 1.0, 2: 1.0}, 725.0)
+    assert c == 1
