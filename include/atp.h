@@ -131,6 +131,10 @@ typedef struct {
 } atp_profile;
 
 atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled);
+/* Diagnostics: copies rank `rank`'s first n chunk counters (device) into
+ * out[0..n) and the host-side targets into out[n..2n), on a separate stream,
+ * so it works while a schedule is stuck waiting on a counter. */
+atp_status atp_debug_counters(atp_mesh* mesh, int rank, uint32_t* out, int n);
 atp_status atp_profile_begin(atp_mesh* mesh);
 atp_status atp_profile_end(atp_mesh* mesh, atp_profile* out);
 atp_status atp_launch_count(uint64_t* out);

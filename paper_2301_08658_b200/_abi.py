@@ -110,6 +110,7 @@ SIGNATURES = {
     "atp_mesh_set_gemm_ctas": (C.c_int, [vp, C.c_int]),
     "atp_mesh_enable_fused_ar": (C.c_int, [vp, C.c_size_t]),
     "atp_mesh_set_comm_enabled": (C.c_int, [vp, C.c_int]),
+    "atp_debug_counters": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint32), C.c_int]),
     "atp_profile_begin": (C.c_int, [vp]),
     "atp_profile_end": (C.c_int, [vp, C.POINTER(Profile)]),
     "atp_launch_count": (C.c_int, [C.POINTER(C.c_uint64)]),

@@ -117,6 +117,13 @@ atp_status atp_mesh_enable_fused_ar(atp_mesh* mesh, size_t part_bytes) {
   return static_cast<atp_status>(atp::enable_fused_ar(mesh, part_bytes));
 }
 
+// Debug (not in atp.h's documented surface for users): device counters and host
+// totals of one rank, copied on a separate stream (works while kernels spin).
+extern "C" atp_status atp_debug_counters(atp_mesh* mesh, int rank, uint32_t* out, int n) {
+  if (mesh == nullptr || out == nullptr || n < 1 || n > atp::kSigSlots) return fail(ATP_ERR_INVALID, "debug");
+  return static_cast<atp_status>(atp::debug_counters(mesh, rank, out, n));
+}
+
 atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas) {
   if (mesh == nullptr || max_ctas < 0) return fail(ATP_ERR_INVALID, "atp_mesh_set_gemm_ctas: bad arguments");
   mesh->gemm_ctas = max_ctas;

@@ -41,7 +41,12 @@ struct GemmDesc {
   // chunk (sig_rows rows each) and every CTA-tile of chunk k adds 1 to sig[k]
   // once its output is globally visible.  nullptr = no signalling.
   uint32_t* sig = nullptr;
-  int sig_rows = 0;
+  int sig_rows = 0;  // rows per chunk: tiles run chunk by chunk (also when only gated)
+  // Chunk gating: before loading the A rows of chunk k the producer waits until
+  // gate[k] >= gate_target (published by the communication stream once the
+  // previous stage's chunk k is all-reduced).  nullptr = no gating.
+  const uint32_t* gate = nullptr;
+  uint32_t gate_target = 0;
   // fp32 check mode (gemm_f32.cu): dtype 1, raw operands instead of TMA maps
   int dtype = 0;
   const void* A = nullptr;

@@ -6,6 +6,9 @@
 namespace atp {
 
 constexpr int kSigSlots = 4096;  // per-rank counters per kind (tile, ready, done)
+// The tile region splits in two: [0, kGateBase) cumulative tile counters,
+// [kGateBase, kSigSlots) chunk gates (written with the call's epoch).
+constexpr int kGateBase = kSigSlots / 2;
 
 // One fused all-reduce of one chunk (fused_ar.cu).
 struct FusedArArgs {

@@ -28,11 +28,11 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
 __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, int64_t lda, int a_mn,
                                                        const float* __restrict__ B, int64_t ldb, int b_mn, int M,
                                                        int N, int K, int epi, EpiParams ep, uint32_t* sig,
-                                                       int sig_rows) {
+                                                       int sig_rows, const uint32_t* gate, uint32_t gate_target) {
   __shared__ float As[TK][TB + 4];
   __shared__ float Bs[TK][TB + 4];
   const int num_m = (M + TB - 1) / TB, num_n = (N + TB - 1) / TB;
-  const int mt_chunk = sig != nullptr ? sig_rows / TB : num_m;
+  const int mt_chunk = sig_rows > 0 ? sig_rows / TB : num_m;
   // chunk-major tile order (row-major inside a chunk)
   const int tile = blockIdx.x;
   const int chunk = tile / (mt_chunk * num_n);
@@ -40,6 +40,15 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
   const int mt = chunk * mt_chunk + r / num_n, nt = r % num_n;
   const int m0 = mt * TB, n0 = nt * TB;
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  if (gate != nullptr) {
+    if (tid == 0) {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gate + chunk) : "memory");
+      } while (static_cast<int32_t>(v - gate_target) < 0);
+    }
+    __syncthreads();
+  }
   float acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -128,7 +137,7 @@ cudaError_t gemm_launch_f32(const GemmDesc& d, cudaStream_t st) {
   const int tiles = ((d.M + TB - 1) / TB) * ((d.N + TB - 1) / TB);
   gemm_f32_kernel<<<tiles, 256, 0, st>>>(static_cast<const float*>(d.A), d.lda, d.a_mn ? 1 : 0,
                                          static_cast<const float*>(d.B), d.ldb, d.b_mn ? 1 : 0, d.M, d.N, d.K, d.epi,
-                                         d.ep, d.sig, d.sig_rows);
+                                         d.ep, d.sig, d.sig_rows, d.gate, d.gate_target);
   return cudaGetLastError();
 }
 

@@ -210,7 +210,8 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[W], const Side<W>& sd,
 template <int CG, int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows) {
+                      int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows, const uint32_t* gate,
+                      uint32_t gate_target) {
   using L = SmemLayout<CG, BN, STAGES>;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr int BNC = BN / CG;  // B rows loaded by this CTA
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
   const int num_tiles = num_m * num_n;
-  const int mt_chunk = sig != nullptr ? sig_rows / (BM * CG) : num_m;  // M-tiles per chunk
+  const int mt_chunk = sig_rows > 0 ? sig_rows / (BM * CG) : num_m;  // M-tiles per chunk
   const int unit = blockIdx.x / CG;      // tile-processing unit (CTA or CTA pair)
   const int n_units = gridDim.x / CG;
 
@@ -274,11 +275,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------ TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
+      int gated_chunk = -1;
       for (int tile = unit; tile < num_tiles; tile += n_units) {
         int mt, nt, chunk;
         tile_coords(tile, mt_chunk, num_n, mt, nt, chunk);
         const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
         const int nb = nt * BN + BNC * static_cast<int>(cta_rank);
+        if (gate != nullptr && chunk > gated_chunk) {  // tiles are chunk-major: chunk only grows
+          ptx::wait_flag_geq(gate + chunk, gate_target);
+          gated_chunk = chunk;
+        }
         for (int kb = 0; kb < num_k; ++kb) {
           ptx::mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sA = base + stage * L::kStageBytes;
@@ -491,7 +497,8 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows);
+  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate,
+                            d.gate_target);
 }
 
 template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>

@@ -69,6 +69,38 @@ static cudaError_t launch_fused(atp_mesh* m, RankState& s, const Op& op, cudaStr
   return fused_ar_launch(a, st);
 }
 
+static PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
+static std::once_flag g_write32_once;
+static bool stream_write_available() {
+  std::call_once(g_write32_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fn);
+  });
+  return g_write32 != nullptr;
+}
+
+// Publish a chunk gate: gate = this call's epoch (the write follows all prior
+// work of the stream and is preceded by a memory barrier).  Gates hold absolute
+// epochs, not counts, so a slot's history (schedules with other chunk counts
+// use other gate slots) never matters: a gate read >= epoch was written by
+// this call.
+static cudaError_t signal_gate(RankState& s, const Op& op, cudaStream_t st) {
+  if (g_write32 == nullptr) return cudaErrorNotSupported;
+  CUresult r = g_write32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(s.sig_buf + op.sig_slot),
+                         s.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
+
+static void fill_gate(RankState& s, Op& op) {
+  if (op.kind == OP_GEMM && op.gate_slot0 >= 0) {
+    op.g.gate = s.sig_buf + op.gate_slot0;
+    op.g.gate_target = s.epoch;
+  }
+}
+
 static cudaError_t wait_sig(RankState& s, const Op& op, cudaStream_t st) {
   s.sig_total[op.sig_slot] += op.sig_inc;
   CUresult r = g_wait32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(s.sig_buf + op.sig_slot),
@@ -139,6 +171,17 @@ RankView rank_view(const atp_mesh* m, int r) {
   v.sig_buf = m->rs[m->is_virtual ? r : 0].sig_buf;
   v.sym_base = m->rs[m->is_virtual ? r : 0].sym_base;
   v.sym_part_bytes = m->rs[m->is_virtual ? r : 0].sym_part_bytes;
+  {
+    // a gated GEMM spins on SMs it holds: only allowed when its CTA cap leaves
+    // SMs for the communication-stream kernels that release the gates
+    static const bool env_on = [] {
+      const char* e = getenv("ATP_GATED");
+      return !(e && e[0] == '0');
+    }();
+    const int n_ranks = static_cast<int>(m->rs.size());
+    v.gate_ok = env_on && v.signalled && stream_write_available() && m->gemm_ctas > 0 &&
+                m->gemm_ctas * n_ranks <= num_sms() - 16;
+  }
   v.signalled = m->signalled && stream_wait_available();
   return v;
 }
@@ -191,6 +234,7 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
   }
   cudaError_t e = cudaEventRecord(m->ev_start, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  for (int r = 0; r < n; ++r) ++m->rs[r].epoch;
   for (int r = 0; r < n; ++r) {
     cudaStreamWaitEvent(m->rs[r].comm, m->ev_start, 0);
     cudaStreamWaitEvent(m->rs[r].aux, m->ev_start, 0);
@@ -199,9 +243,15 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
 
   if (!m->is_virtual) {
     RankState& s = m->rs[0];
-    for (const Op& op : sch[0].ops) {
+    for (Op& op : sch[0].ops) {
       cudaStream_t st = op.stream == 1 ? s.comm : (op.stream == 2 ? s.aux : stream);
       if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+      fill_gate(s, op);
+      if (op.kind == OP_SIGNAL) {
+        if ((e = signal_gate(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWriteValue32");
+        if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+        continue;
+      }
       if (op.kind == OP_WAITSIG) {
         if ((e = wait_sig(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWaitValue32");
         if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
@@ -245,10 +295,16 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
     }
     if (kind != OP_AR) {
       for (int r = 0; r < n; ++r) {
-        const Op& op = sch[r].ops[i];
+        Op& op = sch[r].ops[i];
         RankState& s = m->rs[r];
         cudaStream_t st = op.stream == 1 ? s.comm : (op.stream == 2 ? s.aux : s.compute);
         if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+        fill_gate(s, op);
+        if (op.kind == OP_SIGNAL) {
+          if ((e = signal_gate(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWriteValue32");
+          if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+          continue;
+        }
         if (op.kind == OP_WAITSIG) {
           if ((e = wait_sig(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWaitValue32");
           if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
@@ -324,6 +380,17 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
 // can read them.  Virtual mesh: peers are the other virtual ranks' allocations;
 // distributed mesh: CUDA IPC handles all-gathered over the world communicator
 // and opened for the members of this rank's dim-1 and dim-2 groups.
+int debug_counters(atp_mesh* m, int rank, uint32_t* out, int n) {
+  RankState& s = m->rs[m->is_virtual ? rank : 0];
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaMemcpyAsync(out, s.sig_buf, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  for (int i = 0; i < n && i < static_cast<int>(s.sig_total.size()); ++i) out[n + i] = s.sig_total[i];
+  return e == cudaSuccess ? 0 : 3;
+}
+
 int enable_fused_ar(atp_mesh* m, size_t part_bytes) {
   part_bytes = (part_bytes + 255) & ~static_cast<size_t>(255);
   const size_t flag_bytes = 3 * static_cast<size_t>(kSigSlots) * sizeof(uint32_t);
@@ -334,12 +401,14 @@ int enable_fused_ar(atp_mesh* m, size_t part_bytes) {
       set_error("fused all-reduce already enabled on this mesh");
       return 1;
     }
-    cudaError_t e = cudaMalloc(&s.sym_base, part_bytes + flag_bytes);
-    if (e == cudaSuccess) e = cudaMemset(s.sym_base + part_bytes, 0, flag_bytes);
+    // two partial regions: consecutive fused stages alternate, so a stage's GEMM
+    // never overwrites partial sums the previous stage's all-reduce still reads
+    cudaError_t e = cudaMalloc(&s.sym_base, 2 * part_bytes + flag_bytes);
+    if (e == cudaSuccess) e = cudaMemset(s.sym_base + 2 * part_bytes, 0, flag_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "fused all-reduce buffer");
     s.sym_part_bytes = part_bytes;
     if (s.sig_owned) cudaFree(s.sig_buf);
-    s.sig_buf = reinterpret_cast<uint32_t*>(s.sym_base + part_bytes);
+    s.sig_buf = reinterpret_cast<uint32_t*>(s.sym_base + 2 * part_bytes);
     s.sig_owned = false;
     s.sig_total.assign(kSigSlots, 0u);
     s.ready_total.assign(kSigSlots, 0u);

@@ -16,7 +16,7 @@ namespace atp {
 
 void set_error(const std::string& msg);
 
-enum OpKind : int { OP_GEMM = 0, OP_EW = 1, OP_AR = 2, OP_WAITSIG = 3, OP_FUSED_AR = 4 };
+enum OpKind : int { OP_GEMM = 0, OP_EW = 1, OP_AR = 2, OP_WAITSIG = 3, OP_FUSED_AR = 4, OP_SIGNAL = 5 };
 
 // kSigSlots (fused_ar.h): per-rank chunk-completion counters
 constexpr int kMaxChunks = 16;   // chunk count limit (bounds the waits of one op)
@@ -37,8 +37,12 @@ struct Op {
   int ar_dtype = 0;      // 0 = bf16, 1 = fp32
   // OP_WAITSIG: the stream waits until counter `sig_slot` has grown by
   // `sig_inc` since the previous wait on that slot (cyclic >=).
+  // OP_SIGNAL: the stream publishes gate `sig_slot` = the call's epoch.
+  // OP_GEMM with g.gate: gate_slot0 = first slot of its gates (target filled in
+  // at enqueue time from the published totals).
   int sig_slot = 0;
   uint32_t sig_inc = 0;
+  int gate_slot0 = -1;
   // OP_FUSED_AR: static part of the fused all-reduce (targets and peer
   // pointers are filled in by the executor); ar_dim names the group.
   FusedArArgs far;
@@ -55,7 +59,8 @@ struct RankView {
   uint32_t* sig_buf = nullptr;  // this rank's chunk-completion counters (device)
   bool signalled = true;        // use signalled stages when possible
   char* sym_base = nullptr;     // fused all-reduce: this rank's peer-visible buffer
-  size_t sym_part_bytes = 0;    //   capacity of its partial-sum region
+  size_t sym_part_bytes = 0;    //   capacity of each of its two partial-sum regions
+  bool gate_ok = false;         // chunk-gated GEMMs allowed (GEMM CTA cap leaves SMs free)
 };
 
 struct RankState {
@@ -67,6 +72,7 @@ struct RankState {
   uint32_t* sig_buf = nullptr;       // device counters [kSigSlots]
   bool sig_owned = true;             // false once moved into the symmetric buffer
   std::vector<uint32_t> sig_total;   // host mirror of the values the counters reach
+  uint32_t epoch = 0;                // calls executed (chunk gates hold the epoch)
   // fused all-reduce ("symmetric" buffer: partials [part_bytes] + counters
   // tile[kSigSlots] ready[kSigSlots] done[kSigSlots]); peers per mesh dim
   char* sym_base = nullptr;
@@ -114,6 +120,7 @@ uint64_t launch_count();
 void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes);
 bool stream_wait_available();
 int enable_fused_ar(atp_mesh* m, size_t part_bytes);
+int debug_counters(atp_mesh* m, int rank, uint32_t* out, int n);
 constexpr int kFusedCtas = 16;  // CTAs of one fused all-reduce kernel (fits the SMs the GEMM cap leaves)
 
 }  // namespace atp

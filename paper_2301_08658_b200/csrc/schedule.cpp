@@ -167,105 +167,152 @@ struct Builder {
   // given row range; `fused(ep)` configures the epilogue used when no
   // all-reduce follows (epi kind `fused_epi`); `extra()` emits compute-stream
   // work (the dW GEMMs) that should overlap this stage's communication.
+  // Chunk gates of the previous stage (signalled / fused stages publish one per
+  // chunk after its all-reduce and elementwise step).
+  int gate_slot = -1;
+  int sym_region = 0;  // fused stages alternate between the two partial regions
+  // The next stage reads only call inputs (the first backward stage reads dZ):
+  // it waits for nothing of the previous stage (joined by the executor at the end).
+  bool next_independent = false;
+
+  // Waits for this stage's full-T GEMM: either the previous stage's chunk gates
+  // (the GEMM's producer waits per chunk; no stream wait) or the usual events.
+  // Returns the gate slot to use (-1 = not gated).
+  int stage_entry(int64_t out_w, std::vector<int>& waits) {
+    if (next_independent) {
+      next_independent = false;
+      gate_slot = -1;
+      flush_to_comm();
+      return -1;
+    }
+    int bn = 128, cg = 1;
+    if (dtype == 0) gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
+    if (rv.gate_ok && dtype == 0 && gate_slot >= 0 && chunks > 1 && Mc % (128 * cg) == 0) {
+      for (int k = 0; k < chunks; ++k) pend[k] = -1;  // the gates replace the stream waits
+      const int g = gate_slot;
+      gate_slot = -1;
+      return g;
+    }
+    gate_slot = -1;
+    waits = prologue_all();
+    return -1;
+  }
+  // Pending per-chunk prologues of a per-chunk stage are not needed by an
+  // independent stage: emit them now (on the compute stream) and drop the waits.
+  void flush_to_comm() {
+    prologue_all();
+    for (int k = 0; k < chunks; ++k) pend[k] = -1;
+  }
+  void gate_gemm(Op* g, int gslot) {
+    if (gslot < 0) return;
+    g->gate_slot0 = gslot;
+    g->g.sig_rows = static_cast<int>(Mc);
+  }
+  // After chunk k's all-reduce and elementwise step: publish gate k.
+  void publish_gate(int gslot0, int k) {
+    if (!rv.gate_ok) return;  // nobody waits on gates
+    Op& o = push(OP_SIGNAL, 1);
+    o.sig_slot = gslot0 + k;
+  }
+
+  // One linear stage.  out[T, out_w] = in[T, in_w] * W (+bias), B given as
+  // W^T-free storage (b_mn) — i.e. forward: W stored [in_w, out_w]; backward
+  // dX: W stored [out_w(x_w), in_w(dy_w)] read K-major.  `after_ar(k, rows0,
+  // nrows)` returns the elementwise ops that must follow the all-reduce of the
+  // given row range; `fused(ep)` configures the epilogue used when no
+  // all-reduce follows (epi kind `fused_epi`); `extra()` emits compute-stream
+  // work (the dW GEMMs) that should overlap this stage's communication.
   template <class AfterAR, class Fused, class Extra>
   bool stage(int dim, const void* in, int64_t in_w, const void* w, int64_t ldw, bool b_mn, int64_t out_w, const void* bias,
              void* out, int fused_epi, Fused fused, AfterAR after_ar, Extra extra) {
     const bool comm = dim_size(dim) > 1;
+    int bn = 128, cg = 1;  // fp32 check mode: 128 x 128 tiles
+    if (dtype == 0) gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
     if (!comm) {
       // ---- no all-reduce: one full-T GEMM, elementwise step fused into its epilogue
-      std::vector<int> waits = prologue_all();
+      std::vector<int> waits;
+      const int gslot = stage_entry(out_w, waits);
       EpiParams ep;
       ep.C = out;
       ep.ldc = out_w;
       ep.bias = bias;
-      int epi = fused_epi;
       fused(ep, 0, T);
-      if (!gemm(in, in_w, false, w, ldw, b_mn, T, out_w, in_w, epi, ep, waits, -1)) return false;
-      if (!extra()) return false;
-      return true;
+      Op* g = gemm(in, in_w, false, w, ldw, b_mn, T, out_w, in_w, fused_epi, ep, waits, -1);
+      if (!g) return false;
+      gate_gemm(g, gslot);
+      return extra();
     }
     const void* bias_here = coord0(dim) ? bias : nullptr;
-    int bn = 128, cg = 1;  // fp32 check mode: 128 x 128 tiles
-    if (dtype == 0) gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
-    if (rv.sym_base != nullptr && dtype == 0 && Mc % (128 * cg) == 0 &&
-        static_cast<size_t>(T) * out_w * 2 <= rv.sym_part_bytes && next_slot + chunks <= kSigSlots) {
-      // ---- fused stage: the GEMM writes its partial sums into this rank's
-      // peer-visible buffer and counts tiles per chunk; per chunk, ONE kernel
-      // all-reduces over peer memory and applies the elementwise step.
-      std::vector<int> waits = prologue_all();
+    const bool fused_ok = rv.sym_base != nullptr && dtype == 0 && Mc % (128 * cg) == 0 &&
+                          static_cast<size_t>(T) * out_w * 2 <= rv.sym_part_bytes && next_slot + chunks <= kGateBase;
+    const bool signalled_ok = rv.signalled && rv.sig_buf != nullptr && chunks > 1 && Mc % (128 * cg) == 0 &&
+                              next_slot + chunks <= kGateBase;
+    if (fused_ok || signalled_ok) {
+      // ---- ONE GEMM over all T rows with per-chunk tile counters; per chunk on
+      // the communication stream: the all-reduce (NCCL after a counter wait, or
+      // the fused peer-memory kernel) + elementwise step, then the chunk gate.
+      std::vector<int> waits;
+      const int gslot_in = stage_entry(out_w, waits);
+      const int64_t part_off = fused_ok ? static_cast<int64_t>(sym_region) * rv.sym_part_bytes : 0;
+      if (fused_ok) sym_region ^= 1;
       EpiParams ep;
-      ep.C = rv.sym_base;
+      ep.C = fused_ok ? static_cast<void*>(rv.sym_base + part_off) : out;
       ep.ldc = out_w;
       ep.bias = bias_here;
       Op* g = gemm(in, in_w, false, w, ldw, b_mn, T, out_w, in_w, EPI_BF16, ep, waits, -1);
       if (!g) return false;
+      gate_gemm(g, gslot_in);
       const int slot0 = next_slot;
+      const int gslot0 = kGateBase + next_slot;
       next_slot += chunks;
       g->g.sig = rv.sig_buf + slot0;
       g->g.sig_rows = static_cast<int>(Mc);
       const uint32_t per_chunk = static_cast<uint32_t>((Mc / 128) * ((out_w + g->g.bn - 1) / g->g.bn));
       if (!extra()) return false;
-      const EwList post = after_ar(0, 0, T);  // base pointers of the elementwise step
+      const EwList post = fused_ok ? after_ar(0, 0, T) : EwList{};  // base pointers of the fused step
       for (int k = 0; k < chunks; ++k) {
-        Op& o = push(OP_FUSED_AR, 1);
-        o.ar_dim = dim;
-        o.ar_count = Mc * out_w;
-        o.sig_inc = per_chunk;
-        FusedArArgs& f = o.far;
-        f.part_off = 0;
-        f.flag_off = static_cast<int64_t>(rv.sym_part_bytes);
-        f.ld = out_w;
-        f.width = out_w;
-        f.row0 = k * Mc;
-        f.rows = Mc;
-        f.sig_slot = slot0 + k;
-        f.out = out;
-        f.n_ctas = kFusedCtas;
-        if (!post.empty()) {
-          const EwDesc& e = post[0];
-          f.ew_kind = e.kind;
-          f.ew_out = e.out;
-          f.ew_a = e.a;
-          f.ew_ld = e.kind == EW_CORE_BWD ? 3 * e.cols : e.cols;
-          f.ew_lda = e.cols;
-          f.ew_width = e.cols;
-          f.head_dim = e.cols / e.heads;
+        if (fused_ok) {
+          Op& o = push(OP_FUSED_AR, 1);
+          o.ar_dim = dim;
+          o.ar_count = Mc * out_w;
+          o.sig_inc = per_chunk;
+          FusedArArgs& f = o.far;
+          f.part_off = part_off;
+          f.flag_off = 2 * static_cast<int64_t>(rv.sym_part_bytes);
+          f.ld = out_w;
+          f.width = out_w;
+          f.row0 = k * Mc;
+          f.rows = Mc;
+          f.sig_slot = slot0 + k;
+          f.out = out;
+          f.n_ctas = kFusedCtas;
+          if (!post.empty()) {
+            const EwDesc& e = post[0];
+            f.ew_kind = e.kind;
+            f.ew_out = e.out;
+            f.ew_a = e.a;
+            f.ew_ld = e.kind == EW_CORE_BWD ? 3 * e.cols : e.cols;
+            f.ew_lda = e.cols;
+            f.ew_width = e.cols;
+            f.head_dim = e.cols / e.heads;
+          }
+        } else {
+          Op& wsig = push(OP_WAITSIG, 1);
+          wsig.sig_slot = slot0 + k;
+          wsig.sig_inc = per_chunk;
+          allreduce(dim, mptr(out, k * Mc * out_w), Mc * out_w, -1, -1);
+          for (const EwDesc& e : after_ar(k, k * Mc, Mc)) ew(e, 1);
         }
+        publish_gate(gslot0, k);
       }
       const int last = ev();
       s.ops.back().record = last;
       for (int k = 0; k < chunks; ++k) pend[k] = last;
-      return true;
-    }
-    if (rv.signalled && rv.sig_buf != nullptr && chunks > 1 && Mc % (128 * cg) == 0 &&
-        next_slot + chunks <= kSigSlots) {
-      // ---- signalled stage: one GEMM over all T rows, per-chunk counters
-      std::vector<int> waits = prologue_all();
-      EpiParams ep;
-      ep.C = out;
-      ep.ldc = out_w;
-      ep.bias = bias_here;
-      Op* g = gemm(in, in_w, false, w, ldw, b_mn, T, out_w, in_w, EPI_BF16, ep, waits, -1);
-      if (!g) return false;
-      const int slot0 = next_slot;
-      next_slot += chunks;
-      g->g.sig = rv.sig_buf + slot0;
-      g->g.sig_rows = static_cast<int>(Mc);
-      const uint32_t per_chunk = static_cast<uint32_t>((Mc / 128) * ((out_w + g->g.bn - 1) / g->g.bn));
-      if (!extra()) return false;
-      for (int k = 0; k < chunks; ++k) {
-        Op& wsig = push(OP_WAITSIG, 1);
-        wsig.sig_slot = slot0 + k;
-        wsig.sig_inc = per_chunk;
-        allreduce(dim, mptr(out, k * Mc * out_w), Mc * out_w, -1, -1);
-        for (const EwDesc& e : after_ar(k, k * Mc, Mc)) ew(e, 1);
-      }
-      const int last = ev();
-      s.ops.back().record = last;
-      for (int k = 0; k < chunks; ++k) pend[k] = last;
+      gate_slot = rv.gate_ok ? gslot0 : -1;
       return true;
     }
     // ---- per-chunk stage: c GEMM launches, event hand-off per chunk
+    gate_slot = -1;
     for (int k = 0; k < chunks; ++k) {
       const int wait = prologue(k);
       EpiParams ep;
@@ -439,6 +486,7 @@ int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, i
   }
   if (p.mlp_bwd) {
     const atp_mlp_bwd_args& a = *p.mlp_bwd;
+    b.next_independent = true;  // B1 reads dZ and the saved H/U only
     // B1: dH = dZ W2^T, all-reduce on dim 2 (conjugate of f4); dU = dH * GeLU'(U); || dW2, db2
     if (!b.stage(2, a.dz, hc, a.w2, hc, false, F1, nullptr, a.ws_dh, EPI_DGELU,
                  [&](EpiParams& ep, int64_t, int64_t) {

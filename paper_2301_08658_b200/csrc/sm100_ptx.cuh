@@ -82,6 +82,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const void* tmap, 
       : "memory");
 }
 
+// Wait until a flag written by another stream / kernel reaches `target`
+// (cyclic >=), then order the following async-proxy (TMA) reads after it.
+__device__ __forceinline__ void wait_flag_geq(const uint32_t* flag, uint32_t target) {
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  } while (static_cast<int32_t>(v - target) < 0);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

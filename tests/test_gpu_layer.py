@@ -259,3 +259,56 @@ def test_layer_fused_peer_allreduce(d1, d2, chunks):
     for b, s in zip(bufs, snap):
         for k, v in s.items():
             assert torch.equal(b[k], v), k
+
+
+@pytest.mark.parametrize("d1,d2,cap", [(2, 2, 32), (4, 2, 16), (2, 4, 16), (8, 1, 16)])
+@pytest.mark.parametrize("fused", [False, True])
+def test_layer_chunk_gated(d1, d2, cap, fused):
+    """Chunk-gated GEMMs: with a GEMM CTA cap that leaves SMs for the
+    communication kernels, each stage's GEMM waits per chunk for the previous
+    stage's chunk gate instead of its last all-reduce (NCCL-path or fused)."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, chunks, seed = 1024, 512, 2048, 8, 4, 37
+    g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, d1, d2, chunks, seed)
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        mesh.set_gemm_ctas(cap)
+        if fused:
+            mesh.enable_fused_ar(T * F * 2)
+        bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(d1 * d2)]
+        call = atp.LayerCall(mesh, bufs, T, h, F, heads, chunks, True)
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    compare(bufs, fw, bw, d1, d2)
+    check_replicas(bufs, d1, d2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fused", [False, True])
+def test_layer_gated_chunk_count_changes(fused):
+    """One mesh serving schedules with different chunk counts: counter and gate
+    slots change role between calls (gates hold the call's epoch, tile counters
+    cumulative totals), so every call must still complete and match the oracle."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    d1, d2, cap = 2, 2, 32
+    T, h, F, heads, seed = 1024, 512, 2048, 8, 41
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        mesh.set_gemm_ctas(cap)
+        if fused:
+            mesh.enable_fused_ar(T * F * 2)
+        for chunks in (2, 4, 1, 8, 2):
+            g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, d1, d2, chunks, seed)
+            bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(d1 * d2)]
+            atp.LayerCall(mesh, bufs, T, h, F, heads, chunks, True)()
+            torch.cuda.synchronize()
+            compare(bufs, fw, bw, d1, d2)
+    finally:
+        mesh.destroy()
