@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--mesh", default="", help="d1xd2; default: atp_search (uniform NVSwitch HCM, or --probe)")
     p.add_argument("--fused-ar", action="store_true",
                    help="N>1: fused peer-memory all-reduce (CUDA IPC) instead of NCCL on the data path")
+    p.add_argument("--gated", action="store_true",
+                   help="N>1: chunk-gated GEMMs (the next stage's GEMM waits per chunk for the all-reduce tail)")
     p.add_argument("--probe", action="store_true",
                    help="N>1: measure the HCM + per-mesh calibration with atp_probe_hcm and search on that")
     p.add_argument("--chunks", type=int, default=0,
@@ -317,6 +319,7 @@ def main() -> None:
     mesh = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, uid, local_rank))
     ctas = a.gemm_ctas if a.gemm_ctas >= 0 else (0 if world == 1 else 132)
     mesh.set_gemm_ctas(ctas)
+    mesh.set_gating(a.gated)
     if a.fused_ar and world > 1:
         # one stage's partial sums [T, widest local output] in bf16
         mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
@@ -494,7 +497,7 @@ def main() -> None:
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
                        "allreduce": "fused peer-memory kernel" if (a.fused_ar and world > 1) else "nccl",
-                       "mesh_source": mesh_source,
+                       "gated": bool(a.gated and world > 1), "mesh_source": mesh_source,
                        "l2": "working set > 126 MB L2 (weights+activations ~1-2 GB), no flush"},
             "tflops_per_gpu": per_gpu, "exposed_comm_ms": exposed, "ms_per_step_comm_disabled": ms_nocomm,
             "flops_per_step": fl, "clocks": clocks, "gpu_launches": launches,

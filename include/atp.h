@@ -98,6 +98,14 @@ atp_status atp_mesh_groups(int d1, int d2, int dim, int* out);
  * NCCL kernel keeps SMs of its own (SURVEY §7 "SM sharing"). */
 atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas);
 
+/* Chunk-gated GEMMs (opt-in; initial value from env ATP_GATED=1).  When on,
+ * and the GEMM CTA cap leaves at least 16 SMs free, a stage that follows a
+ * signalled stage launches ONE GEMM whose producer waits per chunk for the
+ * previous stage's chunk gate (written after that chunk's all-reduce and
+ * elementwise step) instead of the stream waiting for its last all-reduce.
+ * Same results.  Errors: ATP_ERR_INVALID (NULL mesh). */
+atp_status atp_mesh_set_gating(atp_mesh* mesh, int enabled);
+
 /* Fused all-reduce over peer memory (opt-in).  Allocates this rank's
  * peer-visible buffer (`part_bytes` for one stage's partial sums [T, width]
  * bf16, plus counters) and maps the buffers of its dim-1 and dim-2 group

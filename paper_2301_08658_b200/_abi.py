@@ -108,6 +108,7 @@ SIGNATURES = {
     "atp_mesh_dims": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "atp_mesh_groups": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "atp_mesh_set_gemm_ctas": (C.c_int, [vp, C.c_int]),
+    "atp_mesh_set_gating": (C.c_int, [vp, C.c_int]),
     "atp_mesh_enable_fused_ar": (C.c_int, [vp, C.c_size_t]),
     "atp_mesh_set_comm_enabled": (C.c_int, [vp, C.c_int]),
     "atp_debug_counters": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint32), C.c_int]),

@@ -76,6 +76,10 @@ class Mesh:
     def set_gemm_ctas(self, n: int) -> None:
         check(lib().atp_mesh_set_gemm_ctas(self.handle, n))
 
+    def set_gating(self, on: bool) -> None:
+        """Chunk-gated GEMMs (opt-in; needs a GEMM CTA cap leaving >= 16 SMs free)."""
+        check(lib().atp_mesh_set_gating(self.handle, 1 if on else 0))
+
     def enable_fused_ar(self, part_bytes: int) -> None:
         """Opt in to the fused peer-memory all-reduce (collective on a distributed mesh)."""
         check(lib().atp_mesh_enable_fused_ar(self.handle, part_bytes))

@@ -130,6 +130,12 @@ atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas) {
   return ATP_OK;
 }
 
+atp_status atp_mesh_set_gating(atp_mesh* mesh, int enabled) {
+  if (mesh == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_set_gating: NULL mesh");
+  mesh->gated = enabled != 0;
+  return ATP_OK;
+}
+
 // ---------------------------------------------------------------- measurement hooks
 atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled) {
   if (mesh == nullptr) return fail(ATP_ERR_INVALID, "atp_mesh_set_comm_enabled: NULL mesh");

@@ -171,18 +171,18 @@ RankView rank_view(const atp_mesh* m, int r) {
   v.sig_buf = m->rs[m->is_virtual ? r : 0].sig_buf;
   v.sym_base = m->rs[m->is_virtual ? r : 0].sym_base;
   v.sym_part_bytes = m->rs[m->is_virtual ? r : 0].sym_part_bytes;
+  v.signalled = m->signalled && stream_wait_available();
   {
-    // a gated GEMM spins on SMs it holds: only allowed when its CTA cap leaves
-    // SMs for the communication-stream kernels that release the gates
-    static const bool env_on = [] {
-      const char* e = getenv("ATP_GATED");
-      return !(e && e[0] == '0');
-    }();
+    // Opt-in (ATP_GATED=1).  A gated GEMM spins on SMs it holds: only allowed
+    // when its CTA cap leaves SMs for the communication-stream kernels that
+    // release the gates.  Off by default: with the collectives elided, gating
+    // made the per-rank compute 5-15% slower (the elementwise tails run on the
+    // SMs the cap leaves free while the GEMM waits), and its gain
+    // (overlapping the all-reduce tail) cannot be measured on one GPU.
     const int n_ranks = static_cast<int>(m->rs.size());
-    v.gate_ok = env_on && v.signalled && stream_write_available() && m->gemm_ctas > 0 &&
+    v.gate_ok = m->gated && v.signalled && stream_write_available() && m->gemm_ctas > 0 &&
                 m->gemm_ctas * n_ranks <= num_sms() - 16;
   }
-  v.signalled = m->signalled && stream_wait_available();
   return v;
 }
 
@@ -530,6 +530,8 @@ int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, 
   {
     const char* e = getenv("ATP_SIGNALLED");
     m->signalled = !(e && e[0] == '0');
+    const char* g = getenv("ATP_GATED");
+    m->gated = g && g[0] == '1';
   }
   m->i1 = m->rank / d2;
   m->i2 = m->rank % d2;

@@ -98,6 +98,7 @@ struct atp_mesh {
   bool comm_enabled = true;
   bool local_only = false;  // atp_mesh_init_local: no communicators
   bool signalled = true;    // signalled stages (ATP_SIGNALLED=0 disables, for A/B runs)
+  bool gated = false;       // chunk-gated GEMMs (atp_mesh_set_gating; ATP_GATED=1 initial value)
   bool profiling = false;
   std::vector<atp::ProfRec> prof;  // event pool; the first prof_used are live
   size_t prof_used = 0;

@@ -25,6 +25,7 @@ def main():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--tokens", type=int, default=8192)
     p.add_argument("--gemm-ctas", type=int, default=132)
+    p.add_argument("--gated", action="store_true", help="chunk-gated GEMMs")
     p.add_argument("--fused-ar", action="store_true",
                    help="fused peer-memory all-reduce stages (run against the rank's own buffer)")
     a = p.parse_args()
@@ -41,6 +42,7 @@ def main():
                 continue
             mesh = atp.Mesh.local(d1, d2, 0)
             mesh.set_gemm_ctas(a.gemm_ctas)  # the N>1 default of bench.py: SMs left for the communication kernels
+            mesh.set_gating(a.gated)
             if a.fused_ar:
                 mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
             bufs = atp.alloc_layer_rank(d1, d2, 0, T, h, F, "cuda", 2301)
@@ -58,7 +60,8 @@ def main():
                 ms = e0.elapsed_time(e1) / a.steps
                 fl = 72.0 * T * h * h / (d1 * d2)
                 print(json.dumps({"cfg": cfg, "h": h, "mesh": [d1, d2], "chunks": c, "ms_compute_per_rank": round(ms, 4),
-                                  "tflops_per_rank": round(fl / ms / 1e9, 1), "fused_ar": a.fused_ar}), flush=True)
+                                  "tflops_per_rank": round(fl / ms / 1e9, 1), "fused_ar": a.fused_ar,
+                                  "gated": a.gated}), flush=True)
             del bufs
             mesh.destroy()
             torch.cuda.empty_cache()

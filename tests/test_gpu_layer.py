@@ -275,6 +275,7 @@ def test_layer_chunk_gated(d1, d2, cap, fused):
     mesh = atp.Mesh.virtual(d1, d2)
     try:
         mesh.set_gemm_ctas(cap)
+        mesh.set_gating(True)
         if fused:
             mesh.enable_fused_ar(T * F * 2)
         bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(d1 * d2)]
@@ -302,6 +303,7 @@ def test_layer_gated_chunk_count_changes(fused):
     mesh = atp.Mesh.virtual(d1, d2)
     try:
         mesh.set_gemm_ctas(cap)
+        mesh.set_gating(True)
         if fused:
             mesh.enable_fused_ar(T * F * 2)
         for chunks in (2, 4, 1, 8, 2):
