@@ -28,6 +28,8 @@ BASE_SEED = 2301
 TENSOR_IDS = {
     "x": 1, "wqkv": 2, "bqkv": 3, "wo": 4, "bo": 5,
     "w1": 6, "b1": 7, "w2": 8, "b2": 9, "dz": 10,
+    # full GPT layer (LayerNorm gamma / beta)
+    "g1": 11, "be1": 12, "g2": 13, "be2": 14,
     # stand-alone linear tests
     "lin_x": 20, "lin_w": 21, "lin_b": 22, "lin_dy": 23,
 }
@@ -35,11 +37,18 @@ TENSOR_IDS = {
 ACT_SCALE = math.sqrt(3.0)
 WEIGHT_SCALE = 0.02 * math.sqrt(3.0)
 BIAS_SCALE = 0.02
+GAMMA_SCALE = 0.1   # LayerNorm gamma = 1 + uniform(+-0.1) (never exactly the identity)
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 
+def default_offset(name: str) -> float:
+    return 1.0 if name in ("g1", "g2") else 0.0
+
+
 def default_scale(name: str) -> float:
+    if name in ("g1", "g2"):
+        return GAMMA_SCALE
     if name in ("x", "dz", "lin_x", "lin_dy"):
         return ACT_SCALE
     if name.startswith("b") or name == "lin_b":
@@ -65,7 +74,7 @@ def round_bf16(a: np.ndarray) -> np.ndarray:
 
 
 def uniform_block(tensor_id: int, shape_global, rows, cols, scale: float,
-                  seed: int = BASE_SEED, bf16: bool = True) -> np.ndarray:
+                  seed: int = BASE_SEED, bf16: bool = True, offset: float = 0.0) -> np.ndarray:
     """Values of the global 2-D tensor ``[shape_global]`` at ``rows x cols``.
 
     ``rows``/``cols`` are ``range``/``slice``-like (start, stop) pairs or index
@@ -78,7 +87,7 @@ def uniform_block(tensor_id: int, shape_global, rows, cols, scale: float,
     key = np.uint64(seed) ^ (np.uint64(tensor_id) << np.uint64(40))
     z = _splitmix64(idx ^ key)
     u = (z >> np.uint64(40)).astype(np.float64) / float(1 << 24)
-    v = (scale * (2.0 * u - 1.0)).astype(np.float32)
+    v = (offset + scale * (2.0 * u - 1.0)).astype(np.float32)
     return round_bf16(v) if bf16 else v
 
 
@@ -87,14 +96,15 @@ def tensor(name: str, shape, seed: int = BASE_SEED, bf16: bool = True,
     """Global tensor ``name`` of ``shape`` (1-D or 2-D), or a row/col sub-block."""
     tid = TENSOR_IDS[name]
     sc = default_scale(name) if scale is None else scale
+    off = default_offset(name)
     if len(shape) == 1:
         (n,) = shape
         c = np.arange(n) if cols is None else np.asarray(cols)
-        return uniform_block(tid, (1, n), [0], c, sc, seed, bf16).reshape(-1)
+        return uniform_block(tid, (1, n), [0], c, sc, seed, bf16, off).reshape(-1)
     nr, nc = shape
     r = np.arange(nr) if rows is None else np.asarray(rows)
     c = np.arange(nc) if cols is None else np.asarray(cols)
-    return uniform_block(tid, (nr, nc), r, c, sc, seed, bf16)
+    return uniform_block(tid, (nr, nc), r, c, sc, seed, bf16, off)
 
 
 def layer_shapes(T: int, h: int, F: int) -> dict:
@@ -103,6 +113,17 @@ def layer_shapes(T: int, h: int, F: int) -> dict:
         "x": (T, h), "wqkv": (h, 3 * h), "bqkv": (3 * h,), "wo": (h, h), "bo": (h,),
         "w1": (h, F), "b1": (F,), "w2": (F, h), "b2": (h,), "dz": (T, h),
     }
+
+
+def gpt_shapes(T: int, h: int, F: int) -> dict:
+    """Global shapes of the full GPT layer: the linear block plus LayerNorm gamma/beta."""
+    s = layer_shapes(T, h, F)
+    s.update({"g1": (h,), "be1": (h,), "g2": (h,), "be2": (h,)})
+    return s
+
+
+def gpt_globals(T: int, h: int, F: int, seed: int = BASE_SEED, bf16: bool = True) -> dict:
+    return {k: tensor(k, s, seed, bf16) for k, s in gpt_shapes(T, h, F).items()}
 
 
 def layer_globals(T: int, h: int, F: int, seed: int = BASE_SEED, bf16: bool = True) -> dict:
@@ -145,7 +166,7 @@ def torch_block(name: str, shape_global, row0: int, nrows: int, col0: int, ncols
         z = (z ^ _lsr(z, 27)) * _to_i64(0x94D049BB133111EB)
         z = z ^ _lsr(z, 31)
         u = _lsr(z, 40).to(torch.float64) / float(1 << 24)
-        v = (sc * (2.0 * u - 1.0)).to(torch.float32)
+        v = (default_offset(name) + sc * (2.0 * u - 1.0)).to(torch.float32)
         out[r0:r0 + rr] = v.to(torch.bfloat16) if bf16 else v  # torch's f32->bf16 cast is RNE
     return out
 
