@@ -160,6 +160,21 @@ atp_status atp_gemm(const void* A, int64_t lda, int a_mn, const void* B, int64_t
                     void* C, int64_t ldc, int out_f32, const void* bias, int64_t M, int64_t N,
                     int64_t K, int max_ctas, void* stream);
 
+/* ------------------------------------------------------------------ attention core
+ * Softmax attention of one rank's heads (Eq. 1):
+ * for every sequence n (rows [n*seq, (n+1)*seq) of the T token rows) and head j,
+ *     O = softmax(Q K^T / sqrt(d)) V        (causal: key t' > query t masked)
+ * on tcgen05 tensor cores.  qkv [T, 3*heads*d] bf16, row pitch ld_qkv, columns
+ * head-interleaved (head j: q at 3jd, k at 3jd+d, v at 3jd+2d; reading G19).
+ * ctx [T, heads*d] bf16 (pitch ld_ctx) receives O; lse [heads][T] fp32 receives
+ * the natural-log log-sum-exp of each row's scaled, masked scores (saved for
+ * the backward).  Caller-owned device buffers; asynchronous on `stream`.
+ * Requirements: head_dim == 128, seq % 128 == 0, T % seq == 0, pitches
+ * multiples of 8 elements, 16-byte aligned pointers; else ATP_ERR_SHAPE.
+ */
+atp_status atp_attn_core_fwd(const void* qkv, int64_t ld_qkv, int64_t T, int64_t seq, int heads, int head_dim,
+                             int causal, void* ctx, int64_t ld_ctx, float* lse, void* stream);
+
 /* ------------------------------------------------------------------ linears
  * Column-first TP linear (Fig. 5 right): x [M, K/d2] ([Replicate,
  * Shard(1)]), w [K/d2, N/d1] ([Shard(1), Shard(0)]), bias [N/d1] or NULL;

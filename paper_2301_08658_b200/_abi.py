@@ -115,6 +115,7 @@ SIGNATURES = {
     "atp_profile_begin": (C.c_int, [vp]),
     "atp_profile_end": (C.c_int, [vp, C.POINTER(Profile)]),
     "atp_launch_count": (C.c_int, [C.POINTER(C.c_uint64)]),
+    "atp_attn_core_fwd": (C.c_int, [vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64, vp, vp]),
     "atp_gemm": (C.c_int, [vp, i64, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int, vp, i64, i64, i64, C.c_int, vp]),
     "atp_linear_colfirst_fwd": (C.c_int, [vp, C.POINTER(LinearFwdArgs), i64, i64, i64, C.c_int, C.c_int, vp]),
     "atp_linear_rowfirst_fwd": (C.c_int, [vp, C.POINTER(LinearFwdArgs), i64, i64, i64, C.c_int, C.c_int, vp]),

@@ -112,6 +112,15 @@ def atp_gemm(A, B, Cout, a_mn: bool = False, b_mn: bool = False, bias=None, max_
                          M, N, K, max_ctas, _stream(stream)))
 
 
+# ------------------------------------------------------------------ attention core
+def atp_attn_core_fwd(qkv, ctx, lse, seq: int, heads: int, causal: bool = True, head_dim: int = 128, stream=None):
+    """ctx[T, heads*d] = softmax(Q K^T / sqrt(d)) V per sequence/head of the
+    head-interleaved qkv[T, 3*heads*d]; lse[heads, T] (fp32) = row log-sum-exp."""
+    T = qkv.shape[0]
+    check(lib().atp_attn_core_fwd(qkv.data_ptr(), qkv.stride(0), T, seq, heads, head_dim, int(causal),
+                                  ctx.data_ptr(), ctx.stride(0), lse.data_ptr(), _stream(stream)))
+
+
 # ------------------------------------------------------------------ linears
 def _arr(struct_cls, items):
     arr = (struct_cls * len(items))()

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/atp.h"
+#include "attention.h"
 #include "schedule.h"
 
 using atp::Sched;
@@ -195,6 +196,19 @@ atp_status atp_gemm(const void* A, int64_t lda, int a_mn, const void* B, int64_t
   atp::count_launch(1);
   cudaError_t e = atp::gemm_launch(d, as_stream(stream));
   if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("atp_gemm: ") + cudaGetErrorString(e));
+  return ATP_OK;
+}
+
+// ---------------------------------------------------------------- attention core
+atp_status atp_attn_core_fwd(const void* qkv, int64_t ld_qkv, int64_t T, int64_t seq, int heads, int head_dim,
+                             int causal, void* ctx, int64_t ld_ctx, float* lse, void* stream) {
+  if (qkv == nullptr || ctx == nullptr || lse == nullptr) return fail(ATP_ERR_INVALID, "atp_attn_core_fwd: NULL buffer");
+  if (const char* m = atp::attn_check(T, seq, heads, head_dim, ld_qkv, ld_ctx)) return fail(ATP_ERR_SHAPE, m);
+  if (!aligned16(qkv) || !aligned16(ctx) || !aligned16(lse)) return fail(ATP_ERR_SHAPE, "atp_attn_core_fwd: alignment");
+  atp::count_launch(1);
+  cudaError_t e = atp::attn_fwd_launch(qkv, ld_qkv, static_cast<int>(T), static_cast<int>(seq), heads, causal, ctx,
+                                       ld_ctx, lse, as_stream(stream));
+  if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("atp_attn_core_fwd: ") + cudaGetErrorString(e));
   return ATP_OK;
 }
 

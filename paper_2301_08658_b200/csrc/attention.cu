@@ -1,0 +1,312 @@
+// Attention core: O = softmax(Q K^T / sqrt(d)) V per
+// sequence and head (Eq. 1), causal (reading G30), head dim 128,
+// on tcgen05 tensor cores with TMEM accumulators.
+//
+// Input: one rank's head block of the QKV activations, token-major
+// [T, 3 * heads * 128] with head-interleaved columns (head j: q at 3j*128,
+// k at 3j*128 + 128, v at 3j*128 + 256; reading G19).  Rows are whole
+// sequences of `seq` tokens (seq % 128 == 0).
+//
+// Forward: one CTA per (128-query block, head, sequence), heaviest causal
+// blocks first.  Warp roles:
+//   warp 0     TMA: Q once, then K_j / V_j double-buffered (one tensor map over
+//              the QKV block, 64 x 128 boxes, 128B swizzle)
+//   warp 1     MMA issuer: S_{j+1} = Q K_{j+1}^T into the other TMEM S buffer
+//              while the softmax works on S_j, then O += P_j V_j (V as an
+//              MN-major B operand, P from shared memory)
+//   warps 4-7  softmax, one thread per query row (TMEM lane = row): online
+//              softmax in the log2 domain with LAZY rescaling — O (in TMEM)
+//              is corrected only when the running row max grows by more than
+//              8 (a factor 256), so p = exp2(s - m) stays <= 256 and the
+//              correction pass is rare; P (bf16) goes to shared memory in the
+//              SW128 K-major layout the MMA reads.
+// TMEM: S0 [0,128) S1 [128,256) O [256,384) of a 512-column allocation.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "atp_internal.h"
+#include "attention.h"
+#include "sm100_ptx.cuh"
+
+namespace atp {
+
+namespace {
+
+constexpr int HD = 128;                  // head dim
+constexpr int BQ = 128;                  // query rows per CTA
+constexpr int BKV = 128;                 // keys per block
+constexpr uint32_t kHalf = 128 * 128;    // one 64-column SW128 box of 128 rows (bytes)
+constexpr uint32_t kTile = 2 * kHalf;    // [128 rows][128 cols] bf16
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// Byte offset of the 16-byte chunk `c16` (8 bf16 columns) of row r in a
+// [128 rows][128 cols] tile stored as two SW128 boxes of 64 columns.
+__device__ __forceinline__ uint32_t sw128_off(int r, int c16) {
+  return static_cast<uint32_t>((c16 >> 3) * kHalf + r * 128 + (((c16 & 7) ^ (r & 7)) << 4));
+}
+
+// K-major operand descriptor for K-step kk (16 columns) of a 128x128 tile.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t tile, int kk) {
+  return ptx::smem_desc_sw128(tile + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
+}
+// MN-major operand descriptor (MN = the 128 tile columns, K = the 128 tile rows).
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile, int kk) {
+  return ptx::smem_desc_sw128(tile + kk * 2048, kHalf, 1024);
+}
+
+struct FwdParams {
+  int T, seq, heads, causal;
+  float scale_log2;  // log2(e) / sqrt(d)
+  __nv_bfloat16* ctx;
+  int64_t ld_ctx;
+  float* lse;  // [heads][T], natural log
+};
+
+// Block index -> (query block, head, sequence); causal: heaviest query blocks first.
+__device__ __forceinline__ void fwd_coords(const FwdParams& p, int& qb, int& head, int& sq) {
+  const int nqb = p.seq / BQ, nseq = p.T / p.seq;
+  const int per = p.heads * nseq;
+  qb = static_cast<int>(blockIdx.x) / per;
+  if (p.causal) qb = nqb - 1 - qb;
+  const int rest = static_cast<int>(blockIdx.x) % per;
+  head = rest % p.heads;
+  sq = rest / p.heads;
+}
+
+__global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sQ = base, sP = base + 5 * kTile;
+  auto sK = [&](int s) { return base + kTile + s * 2 * kTile; };
+  auto sV = [&](int s) { return base + 2 * kTile + s * 2 * kTile; };
+  const uint32_t bars = base + 6 * kTile;
+  const uint32_t q_full = bars, p_full = bars + 8, o_done = bars + 16;
+  auto kv_full = [&](int s) { return bars + 24 + 8 * s; };
+  auto kv_empty = [&](int s) { return bars + 40 + 8 * s; };
+  auto s_full = [&](int s) { return bars + 56 + 8 * s; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 72 - raw));
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int qb, head, sq;
+  fwd_coords(p, qb, head, sq);
+  const int row0 = sq * p.seq, qrow = row0 + qb * BQ;
+  const int nkv = p.causal ? qb + 1 : p.seq / BKV;
+  const int qcol = head * 3 * HD;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(o_done, 1);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(kv_full(s), 1);
+      ptx::mbar_init(kv_empty(s), 1);
+      ptx::mbar_init(s_full(s), 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      ptx::prefetch_tmap(&tm_qkv);
+      ptx::mbar_arrive_expect_tx(q_full, kTile);
+      ptx::tma_load_2d(sQ, &tm_qkv, q_full, qcol, qrow);
+      ptx::tma_load_2d(sQ + kHalf, &tm_qkv, q_full, qcol + 64, qrow);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j & 1;
+        ptx::mbar_wait(kv_empty(s), ((j >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(kv_full(s), 2 * kTile);
+        const int kr = row0 + j * BKV;
+        ptx::tma_load_2d(sK(s), &tm_qkv, kv_full(s), qcol + HD, kr);
+        ptx::tma_load_2d(sK(s) + kHalf, &tm_qkv, kv_full(s), qcol + HD + 64, kr);
+        ptx::tma_load_2d(sV(s), &tm_qkv, kv_full(s), qcol + 2 * HD, kr);
+        ptx::tma_load_2d(sV(s) + kHalf, &tm_qkv, kv_full(s), qcol + 2 * HD + 64, kr);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, 128, 0, 1);
+      ptx::mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int s = j & 1;
+        ptx::mbar_wait(kv_full(s), (j >> 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ptx::mma_bf16_ss(tmem + s * 128, desc_kmajor(sQ, kk), desc_kmajor(sK(s), kk), idesc_s, kk > 0 ? 1u : 0u);
+        ptx::mma_commit(s_full(s));
+      };
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_s(j + 1);  // its S buffer was released with P_{j-1}
+        ptx::mbar_wait(p_full, j & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          ptx::mma_bf16_ss(tmem + 256, desc_kmajor(sP, kk), desc_mnmajor(sV(j & 1), kk), idesc_o,
+                           (j | kk) != 0 ? 1u : 0u);
+        ptx::mma_commit(o_done);
+        ptx::mma_commit(kv_empty(j & 1));
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax (row r of the query block)
+    const int q4 = warp - 4;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    float m_run = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int s = j & 1;
+      ptx::mbar_wait(s_full(s), (j >> 1) & 1);
+      ptx::tc_fence_after();
+      float sv[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + s * 128 + c * 32, u);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(u[i]) * p.scale_log2;
+      }
+      if (p.causal && j == qb) {
+#pragma unroll
+        for (int c = 0; c < BKV; ++c)
+          if (c > r) sv[c] = -INFINITY;
+      }
+      float mb = sv[0];
+#pragma unroll
+      for (int c = 1; c < BKV; ++c) mb = fmaxf(mb, sv[c]);
+      const bool need = mb > m_run + 8.f;
+      if (j > 0) {
+        ptx::mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: O stable, P buffer free
+        ptx::tc_fence_after();
+      }
+      if (__any_sync(0xffffffffu, need)) {  // warp-uniform: tcgen05.ld/st are warp-collective
+        const float m_new = fmaxf(m_run, mb);
+        const float f = exp2f(m_run - m_new);
+        l *= f;
+        if (j > 0) {
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t u[32];
+            const uint32_t ta = tmem + lane_off + 256 + c * 32;
+            ptx::tmem_ld_32x32b_x32(ta, u);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * f);
+            ptx::tmem_st_32x32b_x32(ta, u);
+          }
+          ptx::tmem_wait_st();
+        }
+        m_run = m_new;
+      }
+      float rs = 0.f;
+#pragma unroll
+      for (int c16 = 0; c16 < BKV / 8; ++c16) {
+        float e[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          e[i] = exp2f(sv[c16 * 8 + i] - m_run);
+          rs += e[i];
+        }
+        st_shared_v4(sP + sw128_off(r, c16), pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]), pack_bf16(e[4], e[5]),
+                     pack_bf16(e[6], e[7]));
+      }
+      l += rs;
+      ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+    }
+    // ---- epilogue: O / l -> ctx (bf16), log-sum-exp -> lse
+    ptx::mbar_wait(o_done, (nkv - 1) & 1);
+    ptx::tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = p.ctx + static_cast<int64_t>(qrow + r) * p.ld_ctx + head * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t u[32];
+      ptx::tmem_ld_32x32b_x32(tmem + lane_off + 256 + c * 32, u);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+        w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+        w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+        w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * v) = w;
+      }
+    }
+    p.lse[static_cast<int64_t>(head) * p.T + qrow + r] = (m_run + log2f(l)) * kLn2;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+constexpr int kFwdSmem = 6 * kTile + 128 + 1024;
+
+}  // namespace
+
+const char* attn_check(int64_t T, int64_t seq, int heads, int head_dim, int64_t ld_qkv, int64_t ld_ctx) {
+  if (head_dim != HD) return "attention: head_dim must be 128";
+  if (heads <= 0 || T <= 0 || seq <= 0) return "attention: T, seq, heads must be positive";
+  if (seq % BQ) return "attention: seq must be a multiple of 128";
+  if (T % seq) return "attention: T must be whole sequences (T % seq == 0)";
+  if (ld_qkv < 3 * heads * HD || ld_ctx < heads * HD) return "attention: leading dimension too small";
+  if ((ld_qkv % 8) || (ld_ctx % 8)) return "attention: leading dimensions must be multiples of 8 elements";
+  if (T > (int64_t(1) << 30)) return "attention: T too large";
+  return nullptr;
+}
+
+cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int heads, int causal, void* ctx,
+                            int64_t ld_ctx, float* lse, cudaStream_t st) {
+  alignas(64) CUtensorMap tm;
+  if (!tmap_bf16_2d(&tm, qkv, T, 3 * heads * HD, ld_qkv, 128, 64)) return cudaErrorInvalidValue;
+  static bool attr = [] {
+    return cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem) ==
+           cudaSuccess;
+  }();
+  (void)attr;
+  FwdParams p;
+  p.T = T;
+  p.seq = seq;
+  p.heads = heads;
+  p.causal = causal ? 1 : 0;
+  p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  p.ctx = static_cast<__nv_bfloat16*>(ctx);
+  p.ld_ctx = ld_ctx;
+  p.lse = lse;
+  const int grid = (seq / BQ) * heads * (T / seq);
+  attn_fwd_kernel<<<grid, 256, kFwdSmem, st>>>(tm, p);
+  return cudaGetLastError();
+}
+
+}  // namespace atp

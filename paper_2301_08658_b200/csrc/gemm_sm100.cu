@@ -534,6 +534,11 @@ int gemm_mode() {
 
 }  // namespace
 
+bool tmap_bf16_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                  int box_cols) {
+  return make_tmap(m, ptr, rows, cols, ld, box_rows, box_cols);
+}
+
 int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;

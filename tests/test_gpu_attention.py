@@ -1,0 +1,69 @@
+"""GPU parity of the attention core against the fp64
+oracle (oracle/gpt.py: Eq. 1), through the C ABI."""
+import numpy as np
+import pytest
+
+from gpu_util import rel
+from paper_2301_08658_b200._abi import AtpError
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2  # bf16 inputs / P, fp32 accumulation (north_star bf16 bar)
+
+
+def _qkv(T, heads, seed, scale=1.0):
+    rng = np.random.default_rng(seed)
+    import datagen
+
+    return datagen.round_bf16((rng.standard_normal((T, 3 * heads * 128)) * scale).astype(np.float32))
+
+
+@pytest.mark.parametrize("T,seq,heads,causal", [
+    (256, 128, 1, True), (512, 256, 3, True), (768, 384, 2, True), (1024, 512, 2, False),
+    (2048, 2048, 1, True), (256, 256, 2, False)])
+def test_attn_fwd_matches_oracle(T, seq, heads, causal):
+    import torch
+    import paper_2301_08658_b200 as atp
+    from oracle import gpt
+
+    q = _qkv(T, heads, seed=T + heads, scale=1.5)
+    qd = torch.from_numpy(q).to("cuda", torch.bfloat16)
+    ctx = torch.zeros(T, heads * 128, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, T, device="cuda", dtype=torch.float32)
+    atp.atp_attn_core_fwd(qd, ctx, lse, seq, heads, causal)
+    torch.cuda.synchronize()
+    ref, ref_lse = gpt.core_softmax_fwd(q.astype(np.float64), heads, seq, causal)
+    got = ctx.float().cpu().numpy()
+    assert rel(got, ref) < TOL
+    assert np.abs(lse.cpu().numpy() - ref_lse).max() < 2e-2
+
+
+def test_attn_fwd_peaked_scores():
+    """Large logits (one key dominates): exercises the lazy rescaling path."""
+    import torch
+    import paper_2301_08658_b200 as atp
+    from oracle import gpt
+
+    T, seq, heads = 1024, 1024, 2
+    q = _qkv(T, heads, seed=7, scale=4.0)
+    qd = torch.from_numpy(q).to("cuda", torch.bfloat16)
+    ctx = torch.zeros(T, heads * 128, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, T, device="cuda", dtype=torch.float32)
+    atp.atp_attn_core_fwd(qd, ctx, lse, seq, heads, True)
+    torch.cuda.synchronize()
+    ref, ref_lse = gpt.core_softmax_fwd(q.astype(np.float64), heads, seq, True)
+    assert rel(ctx.float().cpu().numpy(), ref) < TOL
+    assert np.abs(lse.cpu().numpy() - ref_lse).max() < 5e-2
+
+
+def test_attn_shape_errors():
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    qd = torch.zeros(256, 3 * 128, device="cuda", dtype=torch.bfloat16)
+    ctx = torch.zeros(256, 128, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(1, 256, device="cuda", dtype=torch.float32)
+    with pytest.raises(AtpError):
+        atp.atp_attn_core_fwd(qd, ctx, lse, 100, 1)   # seq not a multiple of 128
+    with pytest.raises(AtpError):
+        atp.atp_attn_core_fwd(qd[:200], ctx, lse, 128, 1)  # T not whole sequences
