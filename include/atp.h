@@ -175,6 +175,19 @@ atp_status atp_gemm(const void* A, int64_t lda, int a_mn, const void* B, int64_t
 atp_status atp_attn_core_fwd(const void* qkv, int64_t ld_qkv, int64_t T, int64_t seq, int heads, int head_dim,
                              int causal, void* ctx, int64_t ld_ctx, float* lse, void* stream);
 
+/* Backward of atp_attn_core_fwd (dV = P^T dO, dP = dO V^T, dS = P*(dP - D),
+ * D = rowsum(dO*O), dQ = dS K/sqrt(d), dK = dS^T Q/sqrt(d)): dqkv [T,
+ * 3*heads*d] bf16 (pitch ld_dqkv, same column order as qkv) from the forward's
+ * qkv, ctx (= O) and lse and the upstream dctx [T, heads*d] (pitch ld_dctx).
+ * `workspace` (device, caller-owned) must hold atp_attn_core_workspace(T,
+ * heads) bytes (fp32 dQ accumulator and D); its contents are scratch.
+ * Same shape requirements as the forward; ATP_ERR_SHAPE otherwise. */
+atp_status atp_attn_core_bwd(const void* qkv, int64_t ld_qkv, const void* ctx, int64_t ld_ctx, const float* lse,
+                             const void* dctx, int64_t ld_dctx, int64_t T, int64_t seq, int heads, int head_dim,
+                             int causal, void* dqkv, int64_t ld_dqkv, void* workspace, size_t workspace_bytes,
+                             void* stream);
+size_t atp_attn_core_workspace(int64_t T, int heads);
+
 /* ------------------------------------------------------------------ linears
  * Column-first TP linear (Fig. 5 right): x [M, K/d2] ([Replicate,
  * Shard(1)]), w [K/d2, N/d1] ([Shard(1), Shard(0)]), bias [N/d1] or NULL;

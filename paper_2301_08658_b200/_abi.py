@@ -116,6 +116,9 @@ SIGNATURES = {
     "atp_profile_end": (C.c_int, [vp, C.POINTER(Profile)]),
     "atp_launch_count": (C.c_int, [C.POINTER(C.c_uint64)]),
     "atp_attn_core_fwd": (C.c_int, [vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64, vp, vp]),
+    "atp_attn_core_bwd": (C.c_int, [vp, i64, vp, i64, vp, vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64,
+                                    vp, C.c_size_t, vp]),
+    "atp_attn_core_workspace": (C.c_size_t, [i64, C.c_int]),
     "atp_gemm": (C.c_int, [vp, i64, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int, vp, i64, i64, i64, C.c_int, vp]),
     "atp_linear_colfirst_fwd": (C.c_int, [vp, C.POINTER(LinearFwdArgs), i64, i64, i64, C.c_int, C.c_int, vp]),
     "atp_linear_rowfirst_fwd": (C.c_int, [vp, C.POINTER(LinearFwdArgs), i64, i64, i64, C.c_int, C.c_int, vp]),

@@ -121,6 +121,21 @@ def atp_attn_core_fwd(qkv, ctx, lse, seq: int, heads: int, causal: bool = True, 
                                   ctx.data_ptr(), ctx.stride(0), lse.data_ptr(), _stream(stream)))
 
 
+def atp_attn_core_bwd(qkv, ctx, lse, dctx, dqkv, seq: int, heads: int, causal: bool = True, workspace=None,
+                      head_dim: int = 128, stream=None):
+    """dqkv = d(attention)/d(qkv) for upstream dctx (forward's qkv, ctx, lse)."""
+    import torch
+
+    T = qkv.shape[0]
+    nbytes = lib().atp_attn_core_workspace(T, heads)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=qkv.device)
+    check(lib().atp_attn_core_bwd(qkv.data_ptr(), qkv.stride(0), ctx.data_ptr(), ctx.stride(0), lse.data_ptr(),
+                                  dctx.data_ptr(), dctx.stride(0), T, seq, heads, head_dim, int(causal),
+                                  dqkv.data_ptr(), dqkv.stride(0), workspace.data_ptr(), workspace.numel(),
+                                  _stream(stream)))
+
+
 # ------------------------------------------------------------------ linears
 def _arr(struct_cls, items):
     arr = (struct_cls * len(items))()

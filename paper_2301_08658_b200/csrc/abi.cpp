@@ -212,6 +212,26 @@ atp_status atp_attn_core_fwd(const void* qkv, int64_t ld_qkv, int64_t T, int64_t
   return ATP_OK;
 }
 
+size_t atp_attn_core_workspace(int64_t T, int heads) { return atp::attn_workspace_bytes(T, heads); }
+
+atp_status atp_attn_core_bwd(const void* qkv, int64_t ld_qkv, const void* ctx, int64_t ld_ctx, const float* lse,
+                             const void* dctx, int64_t ld_dctx, int64_t T, int64_t seq, int heads, int head_dim,
+                             int causal, void* dqkv, int64_t ld_dqkv, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  if (!qkv || !ctx || !lse || !dctx || !dqkv || !workspace) return fail(ATP_ERR_INVALID, "atp_attn_core_bwd: NULL buffer");
+  if (const char* m = atp::attn_check(T, seq, heads, head_dim, ld_qkv, ld_ctx)) return fail(ATP_ERR_SHAPE, m);
+  if (ld_dctx < heads * 128 || ld_dctx % 8 || ld_dqkv < 3 * heads * 128 || ld_dqkv % 8)
+    return fail(ATP_ERR_SHAPE, "atp_attn_core_bwd: dctx / dqkv pitch");
+  if (workspace_bytes < atp::attn_workspace_bytes(T, heads)) return fail(ATP_ERR_SHAPE, "atp_attn_core_bwd: workspace too small");
+  if (!aligned16(qkv) || !aligned16(ctx) || !aligned16(dctx) || !aligned16(dqkv) || !aligned16(workspace))
+    return fail(ATP_ERR_SHAPE, "atp_attn_core_bwd: alignment");
+  atp::count_launch(3);
+  cudaError_t e = atp::attn_bwd_launch(qkv, ld_qkv, ctx, ld_ctx, lse, dctx, ld_dctx, static_cast<int>(T),
+                                       static_cast<int>(seq), heads, causal, dqkv, ld_dqkv, workspace, as_stream(stream));
+  if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("atp_attn_core_bwd: ") + cudaGetErrorString(e));
+  return ATP_OK;
+}
+
 // ---------------------------------------------------------------- linears
 static atp_status linear_fwd(atp_mesh* mesh, const atp_linear_fwd_args* args, int64_t M, int64_t K, int64_t N,
                              int chunks, atp_dtype dtype, void* stream, bool colfirst) {

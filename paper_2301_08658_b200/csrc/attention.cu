@@ -273,6 +273,269 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const __grid_constant_
 
 constexpr int kFwdSmem = 6 * kTile + 128 + 1024;
 
+// ================================================================ backward
+// dV = P^T dO, dP = dO V^T, dS = P * (dP - D) with D = rowsum(dO * O),
+// dQ = dS K / sqrt(d), dK = dS^T Q / sqrt(d)   (FlashAttention-2 order).
+// One CTA per (128-key block, head, sequence) loops over the query blocks that
+// see it; TMEM: S (reused for the dQ tile) [0,128), dP [128,256), dV
+// [256,384), dK [384,512).  P and dS (bf16) are written once to shared memory
+// in the SW128 layout [query rows][key cols]: the same bytes are the K-major A
+// operand of dQ = dS K and the MN-major A operand of dV = P^T dO / dK = dS^T Q.
+// dQ tiles are added to an fp32 accumulator with vector atomics; a finalize
+// kernel scales and converts them.
+struct BwdParams {
+  int T, seq, heads, causal;
+  float scale_log2;  // log2(e) / sqrt(d)
+  float scale;       // 1 / sqrt(d)
+  const float* lse;  // [heads][T] natural log (forward output)
+  const float* D;    // [heads][T] rowsum(dO * O)
+  float* dq_acc;     // [T][heads*128] fp32
+  __nv_bfloat16* dqkv;
+  int64_t ld_dqkv;
+};
+
+__global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                          const __grid_constant__ CUtensorMap tm_do, BwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t sK = base, sV = base + kTile, sQ = base + 2 * kTile, sdO = base + 3 * kTile;
+  const uint32_t sP = base + 4 * kTile, sdS = base + 5 * kTile;
+  const uint32_t bars = base + 6 * kTile;
+  const uint32_t kv_full = bars, qdo_full = bars + 8, qdo_empty = bars + 16, s_full = bars + 24;
+  const uint32_t ds_full = bars + 32, dq_full = bars + 40, s_free = bars + 48, done = bars + 56;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 64 - raw));
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nkb = p.seq / BKV, nseq = p.T / p.seq, per = p.heads * nseq;
+  const int jb = static_cast<int>(blockIdx.x) / per;  // causal: key block 0 sees the most query blocks
+  const int rest = static_cast<int>(blockIdx.x) % per;
+  const int head = rest % p.heads, sq = rest / p.heads;
+  const int row0 = sq * p.seq, kvrow = row0 + jb * BKV;
+  const int i0 = p.causal ? jb : 0, n = nkb - i0;
+  const int qcol = head * 3 * HD;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(kv_full, 1);
+    ptx::mbar_init(qdo_full, 1);
+    ptx::mbar_init(qdo_empty, 1);
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(ds_full, 128);
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(s_free, 128);
+    ptx::mbar_init(done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tm_qkv);
+      ptx::prefetch_tmap(&tm_do);
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * kTile);
+      ptx::tma_load_2d(sK, &tm_qkv, kv_full, qcol + HD, kvrow);
+      ptx::tma_load_2d(sK + kHalf, &tm_qkv, kv_full, qcol + HD + 64, kvrow);
+      ptx::tma_load_2d(sV, &tm_qkv, kv_full, qcol + 2 * HD, kvrow);
+      ptx::tma_load_2d(sV + kHalf, &tm_qkv, kv_full, qcol + 2 * HD + 64, kvrow);
+      for (int t = 0; t < n; ++t) {
+        const int qr = row0 + (i0 + t) * BQ;
+        ptx::mbar_wait(qdo_empty, (t & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(qdo_full, 2 * kTile);
+        ptx::tma_load_2d(sQ, &tm_qkv, qdo_full, qcol, qr);
+        ptx::tma_load_2d(sQ + kHalf, &tm_qkv, qdo_full, qcol + 64, qr);
+        ptx::tma_load_2d(sdO, &tm_do, qdo_full, head * HD, qr);
+        ptx::tma_load_2d(sdO + kHalf, &tm_do, qdo_full, head * HD + 64, qr);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_kk = ptx::idesc_bf16_f32(128, 128, 0, 0);  // both K-major
+      constexpr uint32_t id_mm = ptx::idesc_bf16_f32(128, 128, 1, 1);  // both MN-major
+      constexpr uint32_t id_km = ptx::idesc_bf16_f32(128, 128, 0, 1);  // A K-major, B MN-major
+      ptx::mbar_wait(kv_full, 0);
+      for (int t = 0; t < n; ++t) {
+        ptx::mbar_wait(qdo_full, t & 1);
+        if (t > 0) ptx::mbar_wait(s_free, (t - 1) & 1);  // dQ tile of t-1 read out of TMEM
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ptx::mma_bf16_ss(tmem, desc_kmajor(sQ, kk), desc_kmajor(sK, kk), id_kk, kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ptx::mma_bf16_ss(tmem + 128, desc_kmajor(sdO, kk), desc_kmajor(sV, kk), id_kk, kk > 0 ? 1u : 0u);
+        ptx::mma_commit(s_full);
+        ptx::mbar_wait(ds_full, t & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO
+          ptx::mma_bf16_ss(tmem + 256, desc_mnmajor(sP, kk), desc_mnmajor(sdO, kk), id_mm, (t | kk) != 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk)  // dK += dS^T Q
+          ptx::mma_bf16_ss(tmem + 384, desc_mnmajor(sdS, kk), desc_mnmajor(sQ, kk), id_mm, (t | kk) != 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)  // dQ tile = dS K
+          ptx::mma_bf16_ss(tmem, desc_kmajor(sdS, kk), desc_mnmajor(sK, kk), id_km, kk > 0 ? 1u : 0u);
+        ptx::mma_commit(dq_full);
+        ptx::mma_commit(qdo_empty);
+      }
+      ptx::mma_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int q4 = warp - 4;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const int ldq = p.heads * HD;
+    for (int t = 0; t < n; ++t) {
+      const int i = i0 + t;
+      const int qrow = row0 + i * BQ + r;
+      const float lse2 = p.lse[static_cast<int64_t>(head) * p.T + qrow] * 1.4426950408889634f;
+      const float Dr = p.D[static_cast<int64_t>(head) * p.T + qrow];
+      ptx::mbar_wait(s_full, t & 1);
+      ptx::tc_fence_after();
+      float pv[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + c * 32, u);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) pv[c * 32 + k] = exp2f(__uint_as_float(u[k]) * p.scale_log2 - lse2);
+      }
+      if (p.causal && i == jb) {
+#pragma unroll
+        for (int c = 0; c < BKV; ++c)
+          if (c > r) pv[c] = 0.f;
+      }
+#pragma unroll
+      for (int c16 = 0; c16 < BKV / 8; ++c16)
+        st_shared_v4(sP + sw128_off(r, c16), pack_bf16(pv[8 * c16], pv[8 * c16 + 1]),
+                     pack_bf16(pv[8 * c16 + 2], pv[8 * c16 + 3]), pack_bf16(pv[8 * c16 + 4], pv[8 * c16 + 5]),
+                     pack_bf16(pv[8 * c16 + 6], pv[8 * c16 + 7]));
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + 128 + c * 32, u);
+        ptx::tmem_wait_ld();
+        float ds[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) ds[k] = pv[c * 32 + k] * (__uint_as_float(u[k]) - Dr);
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          st_shared_v4(sdS + sw128_off(r, c * 4 + v), pack_bf16(ds[8 * v], ds[8 * v + 1]),
+                       pack_bf16(ds[8 * v + 2], ds[8 * v + 3]), pack_bf16(ds[8 * v + 4], ds[8 * v + 5]),
+                       pack_bf16(ds[8 * v + 6], ds[8 * v + 7]));
+      }
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(ds_full);
+      // dQ tile (unscaled) -> fp32 accumulator
+      ptx::mbar_wait(dq_full, t & 1);
+      ptx::tc_fence_after();
+      float* dst = p.dq_acc + static_cast<int64_t>(qrow) * ldq + head * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + c * 32, u);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          atomicAdd(reinterpret_cast<float4*>(dst + c * 32 + 4 * v),
+                    make_float4(__uint_as_float(u[4 * v]), __uint_as_float(u[4 * v + 1]),
+                                __uint_as_float(u[4 * v + 2]), __uint_as_float(u[4 * v + 3])));
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(s_free);
+    }
+    // ---- dK (scaled), dV -> dqkv rows of this key block (TMEM lane = key row)
+    ptx::mbar_wait(done, 0);
+    ptx::tc_fence_after();
+    __nv_bfloat16* drow = p.dqkv + static_cast<int64_t>(kvrow + r) * p.ld_dqkv + qcol;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {  // 0: dK, 1: dV
+      const float f = which == 0 ? p.scale : 1.f;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + (which == 0 ? 384 : 256) + c * 32, u);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * f, __uint_as_float(u[8 * v + 1]) * f);
+          w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * f, __uint_as_float(u[8 * v + 3]) * f);
+          w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * f, __uint_as_float(u[8 * v + 5]) * f);
+          w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * f, __uint_as_float(u[8 * v + 7]) * f);
+          *reinterpret_cast<uint4*>(drow + (which == 0 ? HD : 2 * HD) + c * 32 + 8 * v) = w;
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// D[h][t] = sum_c dO[t, h*128 + c] * O[t, h*128 + c] (fp32); zero the dQ accumulator.
+// One warp per (row, head).
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o,
+                                     const __nv_bfloat16* __restrict__ dO, int64_t ld_do, int T, int heads,
+                                     float* __restrict__ D, float* __restrict__ dq_acc) {
+  const int lane = threadIdx.x % 32;
+  const int64_t nw = static_cast<int64_t>(T) * heads;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; w < nw;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    const int t = static_cast<int>(w / heads), h = static_cast<int>(w % heads);
+    const uint2 a = *reinterpret_cast<const uint2*>(o + t * ld_o + h * HD + 4 * lane);
+    const uint2 b = *reinterpret_cast<const uint2*>(dO + t * ld_do + h * HD + 4 * lane);
+    const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&b);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float2 x = __bfloat1622float2(ah[i]), y = __bfloat1622float2(bh[i]);
+      acc += x.x * y.x + x.y * y.y;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) D[static_cast<int64_t>(h) * T + t] = acc;
+    *reinterpret_cast<float4*>(dq_acc + static_cast<int64_t>(t) * heads * HD + h * HD + 4 * lane) =
+        make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// dqkv[t, 3h*128 + c] = bf16(dq_acc[t, h*128 + c] / sqrt(d)).
+__global__ void attn_bwd_dq_kernel(const float* __restrict__ dq_acc, int T, int heads, float scale,
+                                   __nv_bfloat16* __restrict__ dqkv, int64_t ld) {
+  const int64_t n8 = static_cast<int64_t>(T) * heads * HD / 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = i * 8;
+    const int t = static_cast<int>(e / (heads * HD));
+    const int rem = static_cast<int>(e % (heads * HD));
+    const int h = rem / HD, c = rem % HD;
+    const float4 a = *reinterpret_cast<const float4*>(dq_acc + e);
+    const float4 b = *reinterpret_cast<const float4*>(dq_acc + e + 4);
+    uint4 w;
+    w.x = pack_bf16(a.x * scale, a.y * scale);
+    w.y = pack_bf16(a.z * scale, a.w * scale);
+    w.z = pack_bf16(b.x * scale, b.y * scale);
+    w.w = pack_bf16(b.z * scale, b.w * scale);
+    *reinterpret_cast<uint4*>(dqkv + t * ld + h * 3 * HD + c) = w;
+  }
+}
+
+constexpr int kBwdSmem = 6 * kTile + 128 + 1024;
+
 }  // namespace
 
 const char* attn_check(int64_t T, int64_t seq, int heads, int head_dim, int64_t ld_qkv, int64_t ld_ctx) {
@@ -306,6 +569,44 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
   p.lse = lse;
   const int grid = (seq / BQ) * heads * (T / seq);
   attn_fwd_kernel<<<grid, 256, kFwdSmem, st>>>(tm, p);
+  return cudaGetLastError();
+}
+
+size_t attn_workspace_bytes(int64_t T, int heads) {
+  return static_cast<size_t>(T) * heads * HD * 4 + static_cast<size_t>(T) * heads * 4;
+}
+
+cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, int64_t ld_ctx, const float* lse,
+                            const void* dctx, int64_t ld_dctx, int T, int seq, int heads, int causal, void* dqkv,
+                            int64_t ld_dqkv, void* workspace, cudaStream_t st) {
+  alignas(64) CUtensorMap tq, td;
+  if (!tmap_bf16_2d(&tq, qkv, T, 3 * heads * HD, ld_qkv, 128, 64)) return cudaErrorInvalidValue;
+  if (!tmap_bf16_2d(&td, dctx, T, heads * HD, ld_dctx, 128, 64)) return cudaErrorInvalidValue;
+  static bool attr = [] {
+    return cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem) ==
+           cudaSuccess;
+  }();
+  (void)attr;
+  float* dq_acc = static_cast<float*>(workspace);
+  float* D = dq_acc + static_cast<int64_t>(T) * heads * HD;
+  const int sms = num_sms();
+  attn_bwd_prep_kernel<<<sms * 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(ctx), ld_ctx,
+                                                static_cast<const __nv_bfloat16*>(dctx), ld_dctx, T, heads, D, dq_acc);
+  BwdParams p;
+  p.T = T;
+  p.seq = seq;
+  p.heads = heads;
+  p.causal = causal ? 1 : 0;
+  p.scale = 1.f / sqrtf(static_cast<float>(HD));
+  p.scale_log2 = 1.4426950408889634f * p.scale;
+  p.lse = lse;
+  p.D = D;
+  p.dq_acc = dq_acc;
+  p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  p.ld_dqkv = ld_dqkv;
+  const int grid = (seq / BKV) * heads * (T / seq);
+  attn_bwd_kernel<<<grid, 256, kBwdSmem, st>>>(tq, td, p);
+  attn_bwd_dq_kernel<<<sms * 8, 256, 0, st>>>(dq_acc, T, heads, p.scale, static_cast<__nv_bfloat16*>(dqkv), ld_dqkv);
   return cudaGetLastError();
 }
 

@@ -12,4 +12,12 @@ const char* attn_check(int64_t T, int64_t seq, int heads, int head_dim, int64_t 
 cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int heads, int causal, void* ctx,
                             int64_t ld_ctx, float* lse, cudaStream_t st);
 
+// Bytes of workspace attn_bwd_launch needs: dQ accumulator [T][heads*128] fp32 + D [heads][T].
+size_t attn_workspace_bytes(int64_t T, int heads);
+// dqkv[T, 3*heads*128] (pitch ld_dqkv) = d(attention)/d(qkv) for upstream dctx, given the
+// forward's qkv, ctx (O) and lse.  Three launches (prep, main, dQ finalize).
+cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, int64_t ld_ctx, const float* lse,
+                            const void* dctx, int64_t ld_dctx, int T, int seq, int heads, int causal, void* dqkv,
+                            int64_t ld_dqkv, void* workspace, cudaStream_t st);
+
 }  // namespace atp

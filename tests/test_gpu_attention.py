@@ -67,3 +67,31 @@ def test_attn_shape_errors():
         atp.atp_attn_core_fwd(qd, ctx, lse, 100, 1)   # seq not a multiple of 128
     with pytest.raises(AtpError):
         atp.atp_attn_core_fwd(qd[:200], ctx, lse, 128, 1)  # T not whole sequences
+
+
+@pytest.mark.parametrize("T,seq,heads,causal", [
+    (256, 128, 1, True), (512, 256, 3, True), (768, 384, 2, True), (1024, 512, 2, False), (2048, 1024, 1, True)])
+def test_attn_bwd_matches_oracle(T, seq, heads, causal):
+    import torch
+    import paper_2301_08658_b200 as atp
+    from oracle import gpt
+
+    q = _qkv(T, heads, seed=3 * T + heads, scale=1.5)
+    rng = np.random.default_rng(T)
+    import datagen
+
+    do = datagen.round_bf16(rng.standard_normal((T, heads * 128)).astype(np.float32))
+    qd = torch.from_numpy(q).to("cuda", torch.bfloat16)
+    dod = torch.from_numpy(do).to("cuda", torch.bfloat16)
+    ctx = torch.zeros(T, heads * 128, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(heads, T, device="cuda", dtype=torch.float32)
+    dqkv = torch.full((T, 3 * heads * 128), float("nan"), device="cuda", dtype=torch.bfloat16)
+    atp.atp_attn_core_fwd(qd, ctx, lse, seq, heads, causal)
+    atp.atp_attn_core_bwd(qd, ctx, lse, dod, dqkv, seq, heads, causal)
+    torch.cuda.synchronize()
+    ref = gpt.core_softmax_bwd(do.astype(np.float64), q.astype(np.float64), heads, seq, causal)
+    got = dqkv.float().cpu().numpy()
+    assert np.isfinite(got).all()
+    for part in range(3):  # q, k, v columns of every head
+        cols = np.concatenate([np.arange(128) + (3 * j + part) * 128 for j in range(heads)])
+        assert rel(got[:, cols], ref[:, cols]) < TOL, ("qkv"[part], rel(got[:, cols], ref[:, cols]))
