@@ -126,16 +126,19 @@ atp_status atp_mesh_enable_fused_ar(atp_mesh* mesh, size_t part_bytes);
  * are then wrong by construction.  atp_profile_begin(mesh) makes the executor
  * bracket every kernel / all-reduce it enqueues with CUDA timing events on the
  * stream it is launched on; atp_profile_end synchronises on those events and
- * returns, per class (0 = tcgen05 GEMM, 1 = elementwise, 2 = all-reduce),
- * the launch count, summed device milliseconds, and the algorithmic FLOPs
- * (GEMM: 2MNK) and bytes (GEMM: A+B+C; elementwise: reads+writes; all-reduce:
- * ring bytes sent 2(p-1)/p*n*2) of those launches.  atp_launch_count() is a
+ * returns, per class (0 = tcgen05 GEMM, 1 = elementwise / LayerNorm,
+ * 2 = collective, 3 = attention core), the launch count, summed device
+ * milliseconds, and the algorithmic FLOPs (GEMM: 2MNK; attention: 4 d per
+ * visible (query, key) pair forward, 2.5x that backward) and bytes (GEMM:
+ * A+B+C; elementwise: reads+writes; all-reduce: ring bytes sent
+ * 2(p-1)/p*n*esz; reduce-scatter / all-gather: (p-1)*block*esz) of those
+ * launches.  atp_launch_count() is a
  * process-wide count of kernels libatp has launched (NCCL's not included). */
 typedef struct {
-  int64_t launches[3];
-  double ms[3];
-  double flops[3];
-  double bytes[3];
+  int64_t launches[4];
+  double ms[4];
+  double flops[4];
+  double bytes[4];
 } atp_profile;
 
 atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled);
@@ -302,6 +305,49 @@ typedef struct {
 atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t T, int64_t h,
                              int64_t F, int64_t heads, int chunks, int do_backward,
                              atp_dtype dtype, void* stream);
+
+/* ------------------------------------------------------------------ full GPT layer
+ * One pre-LN GPT layer, forward then backward, on DeviceMesh(d1, d2) (SURVEY
+ * §8(f) NEXT #1; readings G29-G35 in DESIGN.md):
+ *   A = LN1(X); QKV = A Wqkv + bqkv; ctx = softmax-attention(QKV) (Eq. 1,
+ *   P:83, causal); Y1 = X + ctx Wo + bo; B = LN2(Y1); U = B W1 + b1;
+ *   H = GeLU(U); Z = Y1 + H W2 + b2; then the backward for upstream dZ.
+ * The attention core is fully sharded (Fig. 6(a)): the QKV partial
+ * sums are reduce-scattered over mesh dim 2 so rank (i1, i2) holds heads
+ * [(i1*d2 + i2)*hl, +hl), hl = heads/(d1*d2); ctx is all-gathered over dim 2
+ * before Out; backward reduce-scatters dctx and all-gathers dQKV on dim 2.
+ * LayerNorm statistics are all-reduced over dim 2 ([rows, 2] fp32).  Chunks
+ * are whole sequences: T = b*seq, T % (chunks*seq) == 0 (reading G34).
+ * Local shapes (hc = h/d2, h1 = h/d1, q1 = 3h/d1, F1 = F/d1, ql = q1/d2,
+ * cl = h1/d2), bf16 unless noted:
+ *   inputs   x, dz [T, hc]; g1, be1, g2, be2 [hc]; wqkv [hc, q1]; bqkv [q1];
+ *            wo [h1, hc]; bo [hc]; w1 [hc, F1]; b1 [F1]; w2 [F1, hc]; b2 [hc]
+ *   saved    a, y1, bn [T, hc]; sv1, sv2 fp32 [T, 2] (mean, rstd);
+ *            qkv [T, ql]; ctx_loc [T, cl]; lse fp32 [T*hl]; ctx [T, h1];
+ *            u, h [T, F1]
+ *   outputs  z, dx [T, hc]; fp32 grads dwqkv [hc, q1], dbqkv [q1],
+ *            dwo [h1, hc], dbo [hc], dw1 [hc, F1], db1 [F1], dw2 [F1, hc],
+ *            db2 [hc], dg1, dbe1, dg2, dbe2 [hc]
+ *   workspace  atp_gpt_workspace(...) bytes (device, caller-owned scratch).
+ * With d2 == 1, ctx_loc may equal ctx.  bf16 only.  Requirements: head dim
+ * h/heads == 128, heads % (d1*d2) == 0, seq % 128 == 0, T % (chunks*seq) ==
+ * 0, h % d2 == 0, widths multiples of 8; else ATP_ERR_SHAPE. */
+typedef struct {
+  const void* x; const void* dz;
+  const void* g1; const void* be1; const void* g2; const void* be2;
+  const void* wqkv; const void* bqkv; const void* wo; const void* bo;
+  const void* w1; const void* b1; const void* w2; const void* b2;
+  void* a; float* sv1; void* qkv; void* ctx_loc; float* lse; void* ctx;
+  void* y1; void* bn; float* sv2; void* u; void* h;
+  void* z; void* dx;
+  float* dwqkv; float* dbqkv; float* dwo; float* dbo; float* dw1; float* db1; float* dw2; float* db2;
+  float* dg1; float* dbe1; float* dg2; float* dbe2;
+} atp_gpt_args;
+
+size_t atp_gpt_workspace(int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq, int chunks);
+atp_status atp_gpt_layer_fwd_bwd(atp_mesh* mesh, const atp_gpt_args* args, int64_t T, int64_t h, int64_t F,
+                                 int64_t heads, int64_t seq, int chunks, int causal, void* workspace,
+                                 size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------ cost model
  * Hierarchical communication matrix (§3.4): layers outermost

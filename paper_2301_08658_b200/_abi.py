@@ -87,8 +87,17 @@ class Plan(C.Structure):
                 ("rejected_d2", C.c_int * ATP_MAX_PLAN)]
 
 
+GPT_FIELDS = ("x", "dz", "g1", "be1", "g2", "be2", "wqkv", "bqkv", "wo", "bo", "w1", "b1", "w2", "b2",
+              "a", "sv1", "qkv", "ctx_loc", "lse", "ctx", "y1", "bn", "sv2", "u", "h", "z", "dx",
+              "dwqkv", "dbqkv", "dwo", "dbo", "dw1", "db1", "dw2", "db2", "dg1", "dbe1", "dg2", "dbe2")
+
+
+class GptArgs(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in GPT_FIELDS]
+
+
 class Profile(C.Structure):
-    _fields_ = [("launches", i64 * 3), ("ms", C.c_double * 3), ("flops", C.c_double * 3), ("bytes", C.c_double * 3)]
+    _fields_ = [("launches", i64 * 4), ("ms", C.c_double * 4), ("flops", C.c_double * 4), ("bytes", C.c_double * 4)]
 
 
 class Call(C.Structure):
@@ -119,6 +128,9 @@ SIGNATURES = {
     "atp_attn_core_bwd": (C.c_int, [vp, i64, vp, i64, vp, vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64,
                                     vp, C.c_size_t, vp]),
     "atp_attn_core_workspace": (C.c_size_t, [i64, C.c_int]),
+    "atp_gpt_workspace": (C.c_size_t, [C.c_int, C.c_int, i64, i64, i64, i64, i64, C.c_int]),
+    "atp_gpt_layer_fwd_bwd": (C.c_int, [vp, C.POINTER(GptArgs), i64, i64, i64, i64, i64, C.c_int, C.c_int, vp,
+                                        C.c_size_t, vp]),
     "atp_gemm": (C.c_int, [vp, i64, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int, vp, i64, i64, i64, C.c_int, vp]),
     "atp_linear_colfirst_fwd": (C.c_int, [vp, C.POINTER(LinearFwdArgs), i64, i64, i64, C.c_int, C.c_int, vp]),
     "atp_linear_rowfirst_fwd": (C.c_int, [vp, C.POINTER(LinearFwdArgs), i64, i64, i64, C.c_int, C.c_int, vp]),

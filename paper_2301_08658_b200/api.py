@@ -263,6 +263,60 @@ def atp_layer_fwd_bwd(mesh, bufs, T, h, F, heads, chunks=1, backward=True, strea
     LayerCall(mesh, bufs, T, h, F, heads, chunks, backward)(stream)
 
 
+# ------------------------------------------------------------------ full GPT layer
+def gpt_boxes(d1: int, d2: int, rank: int, T: int, h: int, F: int) -> dict:
+    """(row0, nrows, col0, ncols) of rank's shard of every global input (oracle/gpt.shard_gpt
+    layout; bqkv is the whole d1 block: the GPU adds it on i2 == 0 before the reduce-scatter)."""
+    box = layout.shard_boxes(d1, d2, rank, T, h, F)
+    out = {k: box[k] for k in ("x", "dz", "wqkv", "bqkv", "wo", "bo", "w1", "b1", "w2", "b2")}
+    for k in ("g1", "be1", "g2", "be2"):
+        out[k] = box["bo"]
+    return out
+
+
+def alloc_gpt_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, heads: int, device, seed: int,
+                   inputs: bool = True) -> dict:
+    """One rank's full-layer buffers (inputs from the seeded generator, on the device)."""
+    import torch
+    import datagen
+
+    hc, h1, q1, F1 = h // d2, h // d1, 3 * h // d1, F // d1
+    ql, cl, hl = q1 // d2, h1 // d2, heads // (d1 * d2)
+    shapes = datagen.gpt_shapes(T, h, F)
+    b = {}
+    for name, (r0, nr, c0, nc) in gpt_boxes(d1, d2, rank, T, h, F).items():
+        t = (datagen.torch_block(name, shapes[name], r0, nr, c0, nc, device, seed=seed) if inputs
+             else torch.empty((nr, nc), dtype=torch.bfloat16, device=device))
+        b[name] = t.reshape(-1) if len(shapes[name]) == 1 else t
+    bf, f32 = torch.bfloat16, torch.float32
+    E = lambda *s, dt=bf: torch.empty(s, dtype=dt, device=device)
+    b.update(a=E(T, hc), sv1=E(T, 2, dt=f32), qkv=E(T, ql), ctx_loc=E(T, cl), lse=E(T * hl, dt=f32), ctx=E(T, h1),
+             y1=E(T, hc), bn=E(T, hc), sv2=E(T, 2, dt=f32), u=E(T, F1), h=E(T, F1), z=E(T, hc), dx=E(T, hc),
+             dwqkv=E(hc, q1, dt=f32), dbqkv=E(q1, dt=f32), dwo=E(h1, hc, dt=f32), dbo=E(hc, dt=f32),
+             dw1=E(hc, F1, dt=f32), db1=E(F1, dt=f32), dw2=E(F1, hc, dt=f32), db2=E(hc, dt=f32),
+             dg1=E(hc, dt=f32), dbe1=E(hc, dt=f32), dg2=E(hc, dt=f32), dbe2=E(hc, dt=f32))
+    return b
+
+
+class GptCall:
+    """Pre-marshalled atp_gpt_layer_fwd_bwd call (one args entry per local rank) with its workspace."""
+
+    def __init__(self, mesh, bufs, T, h, F, heads, seq, chunks=1, causal=True):
+        import torch
+
+        self.mesh = mesh
+        self.args = _arr(_abi.GptArgs, [_abi.GptArgs(*[bb[n].data_ptr() for n in _abi.GPT_FIELDS]) for bb in bufs])
+        self.dims = (T, h, F, heads, seq, chunks, int(causal))
+        per = lib().atp_gpt_workspace(mesh.d1, mesh.d2, T, h, F, heads, seq, chunks)
+        self.ws = torch.empty(per * len(bufs), dtype=torch.uint8, device=bufs[0]["x"].device)
+        self._f = lib().atp_gpt_layer_fwd_bwd
+
+    def __call__(self, stream=None):
+        T, h, F, heads, seq, chunks, causal = self.dims
+        check(self._f(self.mesh.handle, self.args, T, h, F, heads, seq, chunks, causal, self.ws.data_ptr(),
+                      self.ws.numel(), _stream(stream)))
+
+
 # ------------------------------------------------------------------ cost model
 @dataclass
 class HcmLayer:

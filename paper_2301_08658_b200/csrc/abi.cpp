@@ -394,6 +394,43 @@ atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t
   });
 }
 
+// ---------------------------------------------------------------- full GPT layer
+size_t atp_gpt_workspace(int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq, int chunks) {
+  if (d1 < 1 || d2 < 1 || chunks < 1 || T < 1) return 0;
+  return atp::gpt_workspace_bytes(d1, d2, T, h, F, heads, seq, chunks);
+}
+
+atp_status atp_gpt_layer_fwd_bwd(atp_mesh* mesh, const atp_gpt_args* args, int64_t T, int64_t h, int64_t F,
+                                 int64_t heads, int64_t seq, int chunks, int causal, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  const int d1 = mesh->d1, d2 = mesh->d2;
+  if (heads < 1 || h % heads || h / heads != 128) return fail(ATP_ERR_SHAPE, "gpt layer: head dim h/heads must be 128");
+  if (heads % (d1 * d2)) return fail(ATP_ERR_SHAPE, "gpt layer: heads % (d1*d2) != 0 (heads are sharded over both dims)");
+  if (h % d2 || (3 * h) % d1 || F % d1 || (F / d1) % 8 || (h / d2) % 8)
+    return fail(ATP_ERR_SHAPE, "gpt layer: h % d2, F % d1 and 8-element local widths required");
+  if (seq < 128 || seq % 128) return fail(ATP_ERR_SHAPE, "gpt layer: seq must be a multiple of 128");
+  if (chunks < 1 || chunks > atp::kMaxChunks || T % (static_cast<int64_t>(chunks) * seq))
+    return fail(ATP_ERR_SHAPE, "gpt layer: T % (chunks * seq) != 0 (chunks are whole sequences) or chunks > 16");
+  const size_t per = atp::gpt_workspace_bytes(d1, d2, T, h, F, heads, seq, chunks);
+  const int n = n_ranks(mesh);
+  if (workspace == nullptr || workspace_bytes < per * n) return fail(ATP_ERR_SHAPE, "gpt layer: workspace too small");
+  for (int r = 0; r < n; ++r) {
+    const atp_gpt_args& a = args[r];
+    const void* req[] = {a.x, a.dz, a.g1, a.be1, a.g2, a.be2, a.wqkv, a.bqkv, a.wo, a.bo, a.w1, a.b1, a.w2, a.b2,
+                         a.a, a.sv1, a.qkv, a.lse, a.ctx, a.y1, a.bn, a.sv2, a.u, a.h, a.z, a.dx,
+                         a.dwqkv, a.dbqkv, a.dwo, a.dbo, a.dw1, a.db1, a.dw2, a.db2, a.dg1, a.dbe1, a.dg2, a.dbe2};
+    for (const void* p : req)
+      if (p == nullptr) return fail(ATP_ERR_INVALID, "gpt layer: NULL buffer");
+    if (d2 > 1 && a.ctx_loc == nullptr) return fail(ATP_ERR_INVALID, "gpt layer: ctx_loc required when d2 > 1");
+  }
+  char* ws = static_cast<char*>(workspace);
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    return atp::build_gpt_layer(rv, args[r], T, h, F, heads, seq, chunks, causal, ws + per * r, out);
+  });
+}
+
 // ---------------------------------------------------------------- probe
 atp_status atp_probe_allreduce(atp_mesh* mesh, int dim, size_t msg_bytes, int iters, void* buf, double* busbw_gbps,
                                double* algbw_gbps, double* seconds) {

@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "atp_internal.h"
+#include "attention.h"
 #include "elementwise.h"
 
 namespace atp {
@@ -277,6 +278,13 @@ cudaError_t ew_launch_t(const EwDesc& e, cudaStream_t st) {
 }
 
 cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
+  if (e.kind == EW_ATTN_FWD)
+    return attn_fwd_launch(e.a, e.lda, static_cast<int>(e.rows), e.seq, e.heads, e.causal, e.out, e.ldo,
+                           static_cast<float*>(e.out2), st);
+  if (e.kind == EW_ATTN_BWD)
+    return attn_bwd_launch(e.a, e.lda, e.b, e.ldb, static_cast<const float*>(e.out2), e.res, e.ldres,
+                           static_cast<int>(e.rows), e.seq, e.heads, e.causal, e.out, e.ldo, e.ws, st);
+  if (e.kind >= EW_LN_STATS) return gpt_ew_launch(e, st);
   return e.dtype == 1 ? ew_launch_t<float>(e, st) : ew_launch_t<__nv_bfloat16>(e, st);
 }
 

@@ -1,0 +1,265 @@
+// Full-layer memory-bound kernels: LayerNorm with the
+// hidden dimension sharded over mesh dim 2 (reading G33), and the block
+// pack / unpack around the dim-2 reduce-scatter / all-gather of the attention
+// heads (Fig. 6(a); reading G32).
+//
+// LayerNorm rows are split in two passes around a [rows, 2] fp32 all-reduce:
+//   ln_stats        s = (sum x, sum x^2) over the local columns
+//   ln_apply        mean = s0/n, rstd = 1/sqrt(s1/n - mean^2 + eps);
+//                   y = (x - mean) * rstd * gamma + beta; saves (mean, rstd)
+//   ln_bwd_stats    s = (sum g, sum g*xhat), g = dy * gamma
+//   ln_bwd_apply    out = res + rstd * (g - s0/n - xhat * s1/n)
+//   ln_param_grad   dgamma = sum_rows dy*xhat, dbeta = sum_rows dy (fp32,
+//                   deterministic: fixed row segments, then a fixed-order sum)
+// One warp per row, 16-byte vectors; grids are multiples of the SM count.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "atp_internal.h"
+#include "elementwise.h"
+
+namespace atp {
+
+namespace {
+
+constexpr float kLnEps = 1e-5f;  // reading G29 (Megatron / PyTorch default)
+constexpr int kSegs = 32;        // row segments of ln_param_grad
+
+struct F8 {
+  float v[8];
+};
+__device__ __forceinline__ F8 ld8(const __nv_bfloat16* p) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  F8 r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    r.v[2 * i] = f.x;
+    r.v[2 * i + 1] = f.y;
+  }
+  return r;
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const F8& f) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f.v[2 * i], f.v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+int grid_for(int64_t warps_needed) {
+  const int64_t blocks = (warps_needed + 7) / 8;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+__global__ void ln_stats_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t rows, int64_t cols,
+                                float* __restrict__ out) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    float s = 0.f, q = 0.f;
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 v = ld8(x + r * ldx + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s += v.v[i];
+        q += v.v[i] * v.v[i];
+      }
+    }
+    s = warp_sum(s);
+    q = warp_sum(q);
+    if (lane == 0) {
+      out[2 * r] = s;
+      out[2 * r + 1] = q;
+    }
+  }
+}
+
+__global__ void ln_apply_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t rows, int64_t cols,
+                                const float* __restrict__ stats, float n_total, const __nv_bfloat16* __restrict__ gamma,
+                                const __nv_bfloat16* __restrict__ beta, __nv_bfloat16* __restrict__ y, int64_t ldy,
+                                float* __restrict__ saved) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    const float mean = stats[2 * r] / n_total;
+    const float var = fmaxf(stats[2 * r + 1] / n_total - mean * mean, 0.f);
+    const float rstd = rsqrtf(var + kLnEps);
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 v = ld8(x + r * ldx + c), g = ld8(gamma + c), b = ld8(beta + c);
+      F8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o.v[i] = (v.v[i] - mean) * rstd * g.v[i] + b.v[i];
+      st8(y + r * ldy + c, o);
+    }
+    if (lane == 0) {
+      saved[2 * r] = mean;
+      saved[2 * r + 1] = rstd;
+    }
+  }
+}
+
+__global__ void ln_bwd_stats_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy, const __nv_bfloat16* __restrict__ x,
+                                    int64_t ldx, int64_t rows, int64_t cols, const __nv_bfloat16* __restrict__ gamma,
+                                    const float* __restrict__ saved, float* __restrict__ out) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    const float mean = saved[2 * r], rstd = saved[2 * r + 1];
+    float s = 0.f, q = 0.f;
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 d = ld8(dy + r * lddy + c), v = ld8(x + r * ldx + c), g = ld8(gamma + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gg = d.v[i] * g.v[i];
+        s += gg;
+        q += gg * (v.v[i] - mean) * rstd;
+      }
+    }
+    s = warp_sum(s);
+    q = warp_sum(q);
+    if (lane == 0) {
+      out[2 * r] = s;
+      out[2 * r + 1] = q;
+    }
+  }
+}
+
+__global__ void ln_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy, const __nv_bfloat16* __restrict__ x,
+                                    int64_t ldx, int64_t rows, int64_t cols, const __nv_bfloat16* __restrict__ gamma,
+                                    const float* __restrict__ saved, const float* __restrict__ sums, float n_total,
+                                    const __nv_bfloat16* res, int64_t ldres, __nv_bfloat16* out, int64_t ldo) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    const float mean = saved[2 * r], rstd = saved[2 * r + 1];
+    const float m1 = sums[2 * r] / n_total, m2 = sums[2 * r + 1] / n_total;
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 d = ld8(dy + r * lddy + c), v = ld8(x + r * ldx + c), g = ld8(gamma + c);
+      const F8 rr = ld8(res + r * ldres + c);
+      F8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (v.v[i] - mean) * rstd;
+        o.v[i] = rr.v[i] + rstd * (d.v[i] * g.v[i] - m1 - xh * m2);
+      }
+      st8(out + r * ldo + c, o);
+    }
+  }
+}
+
+// Partial column sums over row segment blockIdx.y: part[0][seg][c] = sum dy*xhat,
+// part[1][seg][c] = sum dy.  One thread per column.
+__global__ void ln_param_part_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
+                                     const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t rows, int64_t cols,
+                                     const float* __restrict__ saved, float* __restrict__ part) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= cols) return;
+  const int64_t per = (rows + kSegs - 1) / kSegs;
+  const int64_t r0 = blockIdx.y * per, r1 = r0 + per < rows ? r0 + per : rows;
+  float sg = 0.f, sb = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float d = __bfloat162float(dy[r * lddy + c]);
+    const float xh = (__bfloat162float(x[r * ldx + c]) - saved[2 * r]) * saved[2 * r + 1];
+    sg += d * xh;
+    sb += d;
+  }
+  part[static_cast<int64_t>(blockIdx.y) * cols + c] = sg;
+  part[(kSegs + static_cast<int64_t>(blockIdx.y)) * cols + c] = sb;
+}
+
+__global__ void ln_param_final_kernel(const float* __restrict__ part, int64_t cols, float* __restrict__ dgamma,
+                                      float* __restrict__ dbeta) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= cols) return;
+  float sg = 0.f, sb = 0.f;
+  for (int s = 0; s < kSegs; ++s) {
+    sg += part[s * cols + c];
+    sb += part[(kSegs + s) * cols + c];
+  }
+  dgamma[c] = sg;
+  dbeta[c] = sb;
+}
+
+// [rows, p*w] (pitch ld) -> [p][rows][w]   (pack = 1), or back (pack = 0).
+__global__ void block_pack_kernel(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t rows,
+                                  int64_t w, int p, int64_t ld, int pack) {
+  const int64_t w8 = w / 8, n = rows * p * w8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c8 = i % w8, t = i / w8;
+    const int64_t r = t % rows, j = t / rows;
+    const int64_t blk = (j * rows + r) * w + 8 * c8, flat = r * ld + j * w + 8 * c8;
+    if (pack)
+      *reinterpret_cast<uint4*>(out + blk) = *reinterpret_cast<const uint4*>(in + flat);
+    else
+      *reinterpret_cast<uint4*>(out + flat) = *reinterpret_cast<const uint4*>(in + blk);
+  }
+}
+
+}  // namespace
+
+size_t ln_param_workspace_bytes(int64_t cols) { return static_cast<size_t>(2 * kSegs) * cols * sizeof(float); }
+
+cudaError_t gpt_ew_launch(const EwDesc& e, cudaStream_t st) {
+  using bf = __nv_bfloat16;
+  const int64_t lda = e.lda > 0 ? e.lda : e.cols;
+  const int64_t ldo = e.ldo > 0 ? e.ldo : e.cols;
+  switch (e.kind) {
+    case EW_LN_STATS:
+      ln_stats_kernel<<<grid_for(e.rows), 256, 0, st>>>(static_cast<const bf*>(e.a), lda, e.rows, e.cols,
+                                                        static_cast<float*>(e.out2));
+      break;
+    case EW_LN_APPLY:
+      ln_apply_kernel<<<grid_for(e.rows), 256, 0, st>>>(
+          static_cast<const bf*>(e.a), lda, e.rows, e.cols, static_cast<const float*>(e.out2),
+          static_cast<float>(e.n_total), static_cast<const bf*>(e.b), static_cast<const bf*>(e.c),
+          static_cast<bf*>(e.out), ldo, static_cast<float*>(e.ws));
+      break;
+    case EW_LN_BWD_STATS:
+      ln_bwd_stats_kernel<<<grid_for(e.rows), 256, 0, st>>>(
+          static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b), e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
+          static_cast<const bf*>(e.c), static_cast<const float*>(e.ws), static_cast<float*>(e.out2));
+      break;
+    case EW_LN_BWD_APPLY:
+      ln_bwd_apply_kernel<<<grid_for(e.rows), 256, 0, st>>>(
+          static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b), e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
+          static_cast<const bf*>(e.c), static_cast<const float*>(e.ws), static_cast<const float*>(e.out2),
+          static_cast<float>(e.n_total), static_cast<const bf*>(e.res), e.ldres > 0 ? e.ldres : e.cols,
+          static_cast<bf*>(e.out), ldo);
+      break;
+    case EW_LN_PARAM_GRAD: {
+      float* part = static_cast<float*>(e.out2);  // workspace: ln_param_workspace_bytes(cols)
+      dim3 grid(static_cast<unsigned>((e.cols + 255) / 256), kSegs);
+      ln_param_part_kernel<<<grid, 256, 0, st>>>(static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b),
+                                                 e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
+                                                 static_cast<const float*>(e.ws), part);
+      ln_param_final_kernel<<<static_cast<unsigned>((e.cols + 255) / 256), 256, 0, st>>>(
+          part, e.cols, static_cast<float*>(e.out), static_cast<float*>(e.res_out));
+      break;
+    }
+    case EW_PACK:
+    case EW_UNPACK: {
+      const int64_t n = e.rows * e.cols / 8;  // cols = p * w
+      const int64_t blocks = (n + 255) / 256, cap = static_cast<int64_t>(num_sms()) * 8;
+      block_pack_kernel<<<static_cast<int>(blocks < cap ? blocks : cap), 256, 0, st>>>(
+          static_cast<const bf*>(e.a), static_cast<bf*>(e.out), e.rows, e.cols / e.p, e.p,
+          e.kind == EW_PACK ? lda : ldo, e.kind == EW_PACK ? 1 : 0);
+      break;
+    }
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace atp

@@ -120,6 +120,15 @@ void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes) {
     double out = op.g.epi == EPI_F32 ? 4.0 : 2.0;
     double extra = (op.g.epi == EPI_RESID || op.g.epi == EPI_DGELU || op.g.epi == EPI_BIAS_GELU) ? 2.0 : 0.0;
     *bytes = 2.0 * (M * K + N * K) + M * N * (out + extra);
+  } else if (op.kind == OP_EW && (op.e.kind == EW_ATTN_FWD || op.e.kind == EW_ATTN_BWD)) {
+    // attention core: 4 d s_visible FLOPs per query row and head forward (QK^T and PV),
+    // 2.5x that backward (5 products); causal rows see (s+1)/2 keys on average
+    *cls = 3;
+    const double s = op.e.seq, rows = static_cast<double>(op.e.rows), d = 128.0;
+    const double keys = op.e.causal ? (s + 1.0) / 2.0 : s;
+    const double f = 4.0 * d * keys * rows * op.e.heads;
+    *flops = op.e.kind == EW_ATTN_FWD ? f : 2.5 * f;
+    *bytes = (op.e.kind == EW_ATTN_FWD ? 8.0 : 20.0) * rows * op.e.heads * d;
   } else if (op.kind == OP_EW) {
     *cls = 1;
     const double n = static_cast<double>(op.e.rows) * op.e.cols;
@@ -128,10 +137,18 @@ void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes) {
       case EW_DGELU: case EW_ADD: *bytes = 6.0 * n; break;
       case EW_CORE_FWD: case EW_CORE_BWD: *bytes = 8.0 * n; break;
       case EW_COLSUM: *bytes = 2.0 * n + 4.0 * op.e.cols; break;
+      case EW_LN_STATS: case EW_PACK: case EW_UNPACK: *bytes = (op.e.kind == EW_LN_STATS ? 2.0 : 4.0) * n; break;
+      case EW_LN_APPLY: case EW_LN_BWD_STATS: *bytes = 4.0 * n; break;
+      case EW_LN_BWD_APPLY: *bytes = 8.0 * n; break;
+      case EW_LN_PARAM_GRAD: *bytes = 4.0 * n; break;
+      default: break;
     }
   } else {
     *cls = 2;
-    *bytes = p > 1 ? 2.0 * (p - 1) / p * op.ar_count * (op.ar_dtype == 1 ? 4.0 : 2.0) : 0.0;
+    const double esz = op.ar_dtype == 1 ? 4.0 : 2.0;
+    if (p <= 1) *bytes = 0.0;
+    else if (op.coll == 0) *bytes = 2.0 * (p - 1) / p * op.ar_count * esz;
+    else *bytes = (p - 1.0) * op.ar_count * esz;  // reduce-scatter / all-gather ring
   }
 }
 
@@ -206,8 +223,32 @@ static cudaError_t launch_local(const Op& op, cudaStream_t st) {
     count_launch(1);
     return gemm_launch(op.g, st);
   }
-  count_launch(1);
+  count_launch(op.e.kind == EW_ATTN_BWD ? 3 : (op.e.kind == EW_LN_PARAM_GRAD ? 2 : 1));
   return ew_launch(op.e, st);
+}
+
+// One grouped NCCL collective of a distributed mesh.
+static int nccl_coll(atp_mesh* m, const Op& op, cudaStream_t st) {
+  ncclComm_t comm = op.ar_dim == 1 ? m->dim1 : m->dim2;
+  const ncclDataType_t dt = op.ar_dtype == 1 ? ncclFloat32 : ncclBfloat16;
+  const size_t n = static_cast<size_t>(op.ar_count);
+  ncclResult_t nr;
+  const char* what;
+  if (op.coll == 1) {
+    nr = ncclReduceScatter(op.ar_ptr, op.ar_out, n, dt, ncclSum, comm, st);
+    what = "ncclReduceScatter: ";
+  } else if (op.coll == 2) {
+    nr = ncclAllGather(op.ar_ptr, op.ar_out, n, dt, comm, st);
+    what = "ncclAllGather: ";
+  } else {
+    nr = ncclAllReduce(op.ar_ptr, op.ar_ptr, n, dt, ncclSum, comm, st);
+    what = "ncclAllReduce: ";
+  }
+  if (nr != ncclSuccess) {
+    set_error(std::string(what) + ncclGetErrorString(nr));
+    return 4;
+  }
+  return 0;
 }
 
 static cudaError_t wait_all(const Op& op, RankState& s, cudaStream_t st) {
@@ -262,13 +303,8 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
         if ((e = launch_fused(m, s, op, st)) != cudaSuccess) return cuda_fail(e, "fused all-reduce launch");
       } else if (op.kind == OP_AR) {
         if (m->comm_enabled) {
-          ncclComm_t comm = op.ar_dim == 1 ? m->dim1 : m->dim2;
-          ncclResult_t nr = ncclAllReduce(op.ar_ptr, op.ar_ptr, static_cast<size_t>(op.ar_count),
-                                          op.ar_dtype == 1 ? ncclFloat32 : ncclBfloat16, ncclSum, comm, st);
-          if (nr != ncclSuccess) {
-            set_error(std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
-            return 4;
-          }
+          const int rc = nccl_coll(m, op, st);
+          if (rc) return rc;
         }
       } else if ((e = launch_local(op, st)) != cudaSuccess) {
         return cuda_fail(e, op.kind == OP_GEMM ? "gemm launch" : "elementwise launch");
@@ -346,11 +382,27 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
         }
       }
       ProfRec* pr = prof_begin(m, sch[leader].ops[i], m->rs[leader].comm);
-      if (m->comm_enabled) {
-        if ((e = group_sum_launch(ga, sch[leader].ops[i].ar_count, sch[leader].ops[i].ar_dtype,
-                                  m->rs[leader].comm)) != cudaSuccess)
-          return cuda_fail(e, "group_sum launch");
+      const Op& lop = sch[leader].ops[i];
+      const size_t esz = lop.ar_dtype == 1 ? 4 : 2;
+      cudaStream_t ls = m->rs[leader].comm;
+      if (m->comm_enabled && lop.coll == 2) {
+        // all-gather: member i's block -> block i of every member's output
+        for (int jo = 0; jo < p; ++jo)
+          for (int ji = 0; ji < p; ++ji)
+            if ((e = cudaMemcpyAsync(static_cast<char*>(sch[members[jo]].ops[i].ar_out) + ji * lop.ar_count * esz,
+                                     sch[members[ji]].ops[i].ar_ptr, lop.ar_count * esz, cudaMemcpyDeviceToDevice,
+                                     ls)) != cudaSuccess)
+              return cuda_fail(e, "virtual all-gather copy");
+      } else if (m->comm_enabled) {
+        const int64_t n_sum = lop.coll == 1 ? lop.ar_count * p : lop.ar_count;
+        if ((e = group_sum_launch(ga, n_sum, lop.ar_dtype, ls)) != cudaSuccess) return cuda_fail(e, "group_sum launch");
         count_launch(1);
+        if (lop.coll == 1)  // reduce-scatter: member j keeps block j of the sum
+          for (int j = 0; j < p; ++j)
+            if ((e = cudaMemcpyAsync(sch[members[j]].ops[i].ar_out,
+                                     static_cast<char*>(sch[members[j]].ops[i].ar_ptr) + j * lop.ar_count * esz,
+                                     lop.ar_count * esz, cudaMemcpyDeviceToDevice, ls)) != cudaSuccess)
+              return cuda_fail(e, "virtual reduce-scatter copy");
       }
       prof_end(pr, m->rs[leader].comm);
       cudaEventRecord(m->rs[leader].done, m->rs[leader].comm);

@@ -31,9 +31,14 @@ struct Op {
   int record = -1;
   GemmDesc g;
   EwDesc e;
-  int ar_dim = 0;  // mesh dimension of the grouped all-reduce (1 or 2)
+  int ar_dim = 0;  // mesh dimension of the grouped collective (1 or 2)
+  // OP_AR collective: 0 all-reduce (in place on ar_ptr, ar_count elements),
+  // 1 reduce-scatter (ar_ptr [p][ar_count] -> ar_out [ar_count], member j keeps block j),
+  // 2 all-gather (ar_ptr [ar_count] -> ar_out [p][ar_count], blocks in member order)
+  int coll = 0;
   void* ar_ptr = nullptr;
-  int64_t ar_count = 0;  // elements, in place
+  void* ar_out = nullptr;
+  int64_t ar_count = 0;
   int ar_dtype = 0;      // 0 = bf16, 1 = fp32
   // OP_WAITSIG: the stream waits until counter `sig_slot` has grown by
   // `sig_inc` since the previous wait on that slot (cyclic >=).

@@ -41,6 +41,7 @@
 
 #include "runtime.h"
 #include "schedule.h"
+#include "attention.h"
 
 namespace atp {
 
@@ -534,6 +535,303 @@ int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, i
                  [&]() { return b.dw(a.x, hc, a.ws_dqkv, q1, a.dwqkv, a.dbqkv); }))
       return fail();
   }
+  b.flush();
+  out = std::move(b.s);
+  return 0;
+}
+
+
+// ---------------------------------------------------------------- full GPT layer
+namespace {
+
+// Per-rank workspace of the full layer (bytes, 256-aligned pieces).
+struct GptWs {
+  size_t part, packed, ctxb, dctxp, dctxl, dqkvl, dqkvb, dqkv, dh, dbn, dy1, da, st1, st2, bs1, bs2, lnws, attn, total;
+  GptWs(int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq, int chunks) {
+    (void)seq;
+    const int64_t hc = h / d2, h1 = h / d1, q1 = 3 * h / d1, F1 = F / d1, ql = q1 / d2, cl = h1 / d2;
+    const int64_t hl = heads / (d1 * d2), Mc = T / chunks;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t o = off;
+      off += (bytes + 255) & ~static_cast<size_t>(255);
+      return o;
+    };
+    part = take(T * q1 * 2);
+    packed = take(T * q1 * 2);
+    ctxb = take(T * h1 * 2);
+    dctxp = take(T * h1 * 2);
+    dctxl = take(T * cl * 2);
+    dqkvl = take(T * ql * 2);
+    dqkvb = take(T * q1 * 2);
+    dqkv = take(T * q1 * 2);
+    dh = take(T * F1 * 2);
+    dbn = take(T * hc * 2);
+    dy1 = take(T * hc * 2);
+    da = take(T * hc * 2);
+    st1 = take(T * 8);
+    st2 = take(T * 8);
+    bs1 = take(T * 8);
+    bs2 = take(T * 8);
+    lnws = take(ln_param_workspace_bytes(hc));
+    attn = take(attn_workspace_bytes(Mc, static_cast<int>(hl)));
+    total = off;
+  }
+};
+
+}  // namespace
+
+size_t gpt_workspace_bytes(int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq, int chunks) {
+  return GptWs(d1, d2, T, h, F, heads, seq, chunks).total;
+}
+
+// Stages breadth-first over chunks (Fig. 7; reading G14): a chunk's op
+// on the compute stream waits only for that chunk's previous collective; the
+// elementwise step that follows a collective is deferred into the next
+// stage's chunk prologue, so chunk k's collective overlaps the compute of the
+// chunks before it.  dW GEMMs run on all T rows after their stage's chunks.
+int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_t h, int64_t F, int64_t heads,
+                    int64_t seq, int chunks, int causal, char* ws, Sched& out) {
+  Builder b(rv, T, chunks, 0);
+  const int d1 = rv.d1, d2 = rv.d2;
+  const int64_t hc = h / d2, h1 = h / d1, q1 = 3 * h / d1, F1 = F / d1, ql = q1 / d2, cl = h1 / d2;
+  const int hl = static_cast<int>(heads / (d1 * d2));
+  const int64_t Mc = T / chunks;
+  const GptWs L(d1, d2, T, h, F, heads, seq, chunks);
+  auto W = [&](size_t off) { return static_cast<void*>(ws + off); };
+  auto R = [&](const void* base, int k, int64_t w, int esz = 2) {  // chunk k's rows of a [T, w] buffer
+    return static_cast<void*>(static_cast<char*>(const_cast<void*>(base)) + static_cast<int64_t>(k) * Mc * w * esz);
+  };
+  using E = Builder;
+  auto fail = [&]() {
+    set_error(b.err);
+    return 2;
+  };
+  // compute-stream op of chunk k after its prologue (pending wait + deferred steps)
+  auto gemm_k = [&](int k, const void* A, int64_t lda, const void* Wt, int64_t ldw, bool b_mn, int64_t N, int64_t K,
+                    void* C, const void* bias, int epi, const void* aux, void* C2) {
+    const int w = b.prologue(k);
+    EpiParams ep;
+    ep.C = C;
+    ep.ldc = N;
+    ep.bias = bias;
+    ep.aux = aux;
+    ep.ldaux = N;
+    ep.C2 = C2;
+    ep.ldc2 = N;
+    return b.gemm(A, lda, false, Wt, ldw, b_mn, Mc, N, K, epi, ep, {w}, -1) != nullptr;
+  };
+  auto ew_k = [&](int k, const EwDesc& e) {
+    const int w = b.prologue(k);
+    b.ew(e, 0, w);
+  };
+  // collective of chunk k on the communication stream after the last compute op;
+  // `post` runs in chunk k's next prologue
+  auto coll_k = [&](int k, int dim, int coll, void* ptr, void* outp, int64_t count, int dtype, const EwList& post) {
+    const int e = b.ev();
+    b.s.ops.back().record = e;
+    Op& o = b.push(OP_AR, 1);
+    o.ar_dim = dim;
+    o.coll = coll;
+    o.ar_ptr = ptr;
+    o.ar_out = outp;
+    o.ar_count = count;
+    o.ar_dtype = dtype;
+    Builder::add_wait(o, e);
+    const int r = b.ev();
+    o.record = r;
+    b.pend[k] = r;
+    for (const EwDesc& d : post) b.def[k].push_back(d);
+  };
+  auto ln_stats = [&](const void* x, int64_t rows, float* st) {
+    EwDesc e = E::ewd(EW_LN_STATS, nullptr, x, rows, hc);
+    e.out2 = st;
+    return e;
+  };
+  auto ln_apply = [&](const void* x, const void* g, const void* be, float* st, float* sv, void* y, int64_t rows) {
+    EwDesc e = E::ewd(EW_LN_APPLY, y, x, rows, hc);
+    e.b = g;
+    e.c = be;
+    e.out2 = st;
+    e.ws = sv;
+    e.n_total = h;
+    return e;
+  };
+  auto ln_bstats = [&](const void* dy, const void* x, const void* g, float* sv, float* bs, int64_t rows) {
+    EwDesc e = E::ewd(EW_LN_BWD_STATS, nullptr, dy, rows, hc);
+    e.b = x;
+    e.c = g;
+    e.ws = sv;
+    e.out2 = bs;
+    return e;
+  };
+  auto ln_bapply = [&](const void* dy, const void* x, const void* g, float* sv, float* bs, const void* res, void* o,
+                       int64_t rows) {
+    EwDesc e = E::ewd(EW_LN_BWD_APPLY, o, dy, rows, hc);
+    e.b = x;
+    e.c = g;
+    e.ws = sv;
+    e.out2 = bs;
+    e.res = res;
+    e.n_total = h;
+    return e;
+  };
+  auto ln_params = [&](const void* dy, const void* x, float* sv, float* dg, float* dbe) {
+    EwDesc e = E::ewd(EW_LN_PARAM_GRAD, dg, dy, T, hc);
+    e.b = x;
+    e.ws = sv;
+    e.res_out = dbe;
+    e.out2 = W(L.lnws);
+    b.ew(e, aux_colsum() ? 2 : 0, b.mark_compute());
+  };
+  // LayerNorm of every chunk: row statistics, dim-2 all-reduce (G33), apply (deferred)
+  auto layernorm = [&](const void* x, const void* g, const void* be, size_t st_off, float* sv, void* y) {
+    for (int k = 0; k < chunks; ++k) {
+      float* st = static_cast<float*>(R(W(st_off), k, 2, 4));
+      ew_k(k, ln_stats(R(x, k, hc), Mc, st));
+      const EwDesc ap = ln_apply(R(x, k, hc), g, be, st, static_cast<float*>(R(sv, k, 2, 4)), R(y, k, hc), Mc);
+      if (d2 > 1)
+        coll_k(k, 2, 0, st, nullptr, 2 * Mc, 1, {ap});
+      else
+        b.def[k].push_back(ap);
+    }
+  };
+  auto ln_backward = [&](const void* dy, const void* x, const void* g, float* sv, size_t bs_off, const void* res,
+                         void* o) {
+    for (int k = 0; k < chunks; ++k) {
+      float* bs = static_cast<float*>(R(W(bs_off), k, 2, 4));
+      float* svk = static_cast<float*>(R(sv, k, 2, 4));
+      ew_k(k, ln_bstats(R(dy, k, hc), R(x, k, hc), g, svk, bs, Mc));
+      const EwDesc ap = ln_bapply(R(dy, k, hc), R(x, k, hc), g, svk, bs, R(res, k, hc), R(o, k, hc), Mc);
+      if (d2 > 1)
+        coll_k(k, 2, 0, bs, nullptr, 2 * Mc, 1, {ap});
+      else
+        b.def[k].push_back(ap);
+    }
+  };
+  auto attn_desc = [&](int kind, int k) {
+    EwDesc e;
+    e.kind = kind;
+    e.rows = Mc;
+    e.heads = hl;
+    e.seq = static_cast<int>(seq);
+    e.causal = causal;
+    e.out2 = R(a.lse, k, hl, 4);  // per-chunk [hl][Mc] block
+    return e;
+  };
+  void* ctx_loc = d2 > 1 ? a.ctx_loc : a.ctx;
+  const bool c1 = (d1 == 1), c2 = (d2 == 1);
+  const void* bqkv_here = rv.i2 == 0 ? a.bqkv : nullptr;  // added once before the dim-2 reduction (G16)
+  const void* b1_here = rv.i2 == 0 ? a.b1 : nullptr;
+  const void* bo_here = rv.i1 == 0 ? a.bo : nullptr;
+  const void* b2_here = rv.i1 == 0 ? a.b2 : nullptr;
+
+  // ================= forward
+  layernorm(a.x, a.g1, a.be1, L.st1, a.sv1, a.a);
+  for (int k = 0; k < chunks; ++k) {  // QKV column-first; reduce-scatter of the head blocks on dim 2 (f1)
+    void* dst = c2 ? R(a.qkv, k, ql) : R(W(L.part), k, q1);
+    if (!gemm_k(k, R(a.a, k, hc), hc, a.wqkv, q1, true, q1, hc, dst, bqkv_here, EPI_BF16, nullptr, nullptr)) return fail();
+    if (!c2) {
+      EwDesc pk = E::ewd(EW_PACK, R(W(L.packed), k, q1), dst, Mc, q1);
+      pk.p = d2;
+      b.ew(pk, 0);
+      coll_k(k, 2, 1, R(W(L.packed), k, q1), R(a.qkv, k, ql), Mc * ql, 0, {});
+    }
+  }
+  for (int k = 0; k < chunks; ++k) {  // attention core on the local heads; all-gather ctx on dim 2 (f1 conjugate)
+    EwDesc at = attn_desc(EW_ATTN_FWD, k);
+    at.a = R(a.qkv, k, ql);
+    at.lda = ql;
+    at.out = R(ctx_loc, k, cl);
+    at.ldo = cl;
+    ew_k(k, at);
+    if (!c2) {
+      EwDesc un = E::ewd(EW_UNPACK, R(a.ctx, k, h1), R(W(L.ctxb), k, h1), Mc, h1);
+      un.p = d2;
+      coll_k(k, 2, 2, R(ctx_loc, k, cl), R(W(L.ctxb), k, h1), Mc * cl, 0, {un});
+    }
+  }
+  for (int k = 0; k < chunks; ++k) {  // Out row-first, all-reduce on dim 1 (f2), residual
+    if (!gemm_k(k, R(a.ctx, k, h1), h1, a.wo, hc, true, hc, h1, R(a.y1, k, hc), bo_here, c1 ? EPI_RESID : EPI_BF16,
+                R(a.x, k, hc), nullptr))
+      return fail();
+    if (!c1) coll_k(k, 1, 0, R(a.y1, k, hc), nullptr, Mc * hc, 0, {E::ewd(EW_ADD, R(a.y1, k, hc), R(a.x, k, hc), Mc, hc)});
+  }
+  layernorm(a.y1, a.g2, a.be2, L.st2, a.sv2, a.bn);
+  for (int k = 0; k < chunks; ++k) {  // FC1 column-first, all-reduce on dim 2 (f3), GeLU
+    if (!gemm_k(k, R(a.bn, k, hc), hc, a.w1, F1, true, F1, hc, R(a.u, k, F1), b1_here, c2 ? EPI_BIAS_GELU : EPI_BF16,
+                nullptr, R(a.h, k, F1)))
+      return fail();
+    if (!c2) coll_k(k, 2, 0, R(a.u, k, F1), nullptr, Mc * F1, 0, {E::ewd(EW_GELU, R(a.h, k, F1), R(a.u, k, F1), Mc, F1)});
+  }
+  for (int k = 0; k < chunks; ++k) {  // FC2 row-first, all-reduce on dim 1 (f4), residual
+    if (!gemm_k(k, R(a.h, k, F1), F1, a.w2, hc, true, hc, F1, R(a.z, k, hc), b2_here, c1 ? EPI_RESID : EPI_BF16,
+                R(a.y1, k, hc), nullptr))
+      return fail();
+    if (!c1) coll_k(k, 1, 0, R(a.z, k, hc), nullptr, Mc * hc, 0, {E::ewd(EW_ADD, R(a.z, k, hc), R(a.y1, k, hc), Mc, hc)});
+  }
+
+  // ================= backward
+  void* dh = W(L.dh);
+  for (int k = 0; k < chunks; ++k) {  // FC2-dX, all-reduce on dim 2; dGeLU
+    if (!gemm_k(k, R(a.dz, k, hc), hc, a.w2, hc, false, F1, hc, R(dh, k, F1), nullptr, c2 ? EPI_DGELU : EPI_BF16,
+                R(a.u, k, F1), nullptr))
+      return fail();
+    if (!c2) coll_k(k, 2, 0, R(dh, k, F1), nullptr, Mc * F1, 0, {E::ewd(EW_DGELU, R(dh, k, F1), R(a.u, k, F1), Mc, F1)});
+  }
+  if (!b.dw(a.h, F1, a.dz, hc, a.dw2, a.db2)) return fail();
+  void* dbn = W(L.dbn);
+  for (int k = 0; k < chunks; ++k) {  // FC1-dX, all-reduce on dim 1
+    if (!gemm_k(k, R(dh, k, F1), F1, a.w1, F1, false, hc, F1, R(dbn, k, hc), nullptr, EPI_BF16, nullptr, nullptr))
+      return fail();
+    if (!c1) coll_k(k, 1, 0, R(dbn, k, hc), nullptr, Mc * hc, 0, {});
+  }
+  if (!b.dw(a.bn, hc, dh, F1, a.dw1, a.db1)) return fail();
+  void* dy1 = W(L.dy1);
+  ln_backward(dbn, a.y1, a.g2, a.sv2, L.bs2, a.dz, dy1);  // dY1 = dZ + LN2'(dB)
+  for (int k = 0; k < chunks; ++k) b.prologue(k);        // dY1 complete before dWo / LN2 params
+  ln_params(dbn, a.y1, a.sv2, a.dg2, a.dbe2);
+  void* dctxl = W(L.dctxl);
+  for (int k = 0; k < chunks; ++k) {  // Out-dX, reduce-scatter of the head blocks on dim 2 (f2 conjugate)
+    void* dst = c2 ? R(dctxl, k, cl) : R(W(L.dctxp), k, h1);
+    if (!gemm_k(k, R(dy1, k, hc), hc, a.wo, hc, false, h1, hc, dst, nullptr, EPI_BF16, nullptr, nullptr)) return fail();
+    if (!c2) {
+      EwDesc pk = E::ewd(EW_PACK, R(W(L.packed), k, h1), dst, Mc, h1);
+      pk.p = d2;
+      b.ew(pk, 0);
+      coll_k(k, 2, 1, R(W(L.packed), k, h1), R(dctxl, k, cl), Mc * cl, 0, {});
+    }
+  }
+  if (!b.dw(a.ctx, h1, dy1, hc, a.dwo, a.dbo)) return fail();
+  void* dqkv = W(L.dqkv);
+  for (int k = 0; k < chunks; ++k) {  // attention backward on the local heads; all-gather dQKV on dim 2 (f1)
+    EwDesc at = attn_desc(EW_ATTN_BWD, k);
+    at.a = R(a.qkv, k, ql);
+    at.lda = ql;
+    at.b = R(ctx_loc, k, cl);
+    at.ldb = cl;
+    at.res = R(dctxl, k, cl);
+    at.ldres = cl;
+    at.out = c2 ? R(dqkv, k, q1) : R(W(L.dqkvl), k, ql);
+    at.ldo = c2 ? q1 : ql;
+    at.ws = W(L.attn);
+    ew_k(k, at);
+    if (!c2) {
+      EwDesc un = E::ewd(EW_UNPACK, R(dqkv, k, q1), R(W(L.dqkvb), k, q1), Mc, q1);
+      un.p = d2;
+      coll_k(k, 2, 2, R(W(L.dqkvl), k, ql), R(W(L.dqkvb), k, q1), Mc * ql, 0, {un});
+    }
+  }
+  void* da = W(L.da);
+  for (int k = 0; k < chunks; ++k) {  // QKV-dX, all-reduce on dim 1
+    if (!gemm_k(k, R(dqkv, k, q1), q1, a.wqkv, q1, false, hc, q1, R(da, k, hc), nullptr, EPI_BF16, nullptr, nullptr))
+      return fail();
+    if (!c1) coll_k(k, 1, 0, R(da, k, hc), nullptr, Mc * hc, 0, {});
+  }
+  if (!b.dw(a.a, hc, dqkv, q1, a.dwqkv, a.dbqkv)) return fail();
+  ln_backward(da, a.x, a.g1, a.sv1, L.bs1, dy1, a.dx);  // dX = dY1 + LN1'(dA)
+  for (int k = 0; k < chunks; ++k) b.prologue(k);
+  ln_params(da, a.x, a.sv1, a.dg1, a.dbe1);
   b.flush();
   out = std::move(b.s);
   return 0;

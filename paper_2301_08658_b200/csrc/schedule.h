@@ -23,6 +23,11 @@ int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int6
 int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
                 int chunks, int dtype, Sched& out);
 
+// Full pre-LN GPT layer: per-rank workspace bytes and schedule.
+size_t gpt_workspace_bytes(int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq, int chunks);
+int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_t h, int64_t F, int64_t heads,
+                    int64_t seq, int chunks, int causal, char* ws, Sched& out);
+
 const char* last_error();
 int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, bool is_virtual, atp_mesh** out);
 int mesh_destroy(atp_mesh* m);

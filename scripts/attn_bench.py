@@ -35,9 +35,20 @@ def main():
         q, k, vv = (v[:, :, :, i].transpose(1, 2) for i in range(3))
         q, k, vv = q.contiguous(), k.contiguous(), vv.contiguous()
         ms_ref = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, vv, is_causal=causal))
+        dctx = torch.randn_like(ctx)
+        dqkv = torch.empty_like(qkv)
+        ws = torch.empty(atp._abi.lib().atp_attn_core_workspace(T, heads), dtype=torch.uint8, device="cuda")
+        atp.atp_attn_core_fwd(qkv, ctx, lse, s, heads, causal)
+        msb = timeit(lambda: atp.atp_attn_core_bwd(qkv, ctx, lse, dctx, dqkv, s, heads, causal, ws))
+        qg, kg, vg = (t.detach().requires_grad_() for t in (q, k, vv))
+        o = torch.nn.functional.scaled_dot_product_attention(qg, kg, vg, is_causal=causal)
+        go = torch.randn_like(o)
+        msb_ref = timeit(lambda: torch.autograd.grad(o, (qg, kg, vg), go, retain_graph=True))
         print(json.dumps({"b": b, "s": s, "heads": heads, "causal": causal, "fwd_ms": round(ms, 4),
                           "fwd_tflops": round(fl / ms / 1e9, 1), "sdpa_ms": round(ms_ref, 4),
-                          "sdpa_tflops": round(fl / ms_ref / 1e9, 1)}), flush=True)
+                          "sdpa_tflops": round(fl / ms_ref / 1e9, 1), "bwd_ms": round(msb, 4),
+                          "bwd_tflops": round(2.5 * fl / msb / 1e9, 1), "sdpa_bwd_ms": round(msb_ref, 4),
+                          "sdpa_bwd_tflops": round(2.5 * fl / msb_ref / 1e9, 1)}), flush=True)
 
 
 if __name__ == "__main__":

@@ -23,7 +23,7 @@ def built():
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "atp.h")).read()
-    return sorted(set(re.findall(r"^(?:atp_status|const char\*)\s+(atp_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:atp_status|const char\*|size_t)\s+(atp_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_library_exports_every_declared_symbol():
