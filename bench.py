@@ -54,6 +54,9 @@ def parse():
     p.add_argument("--ffn", type=int, default=0, help="default 4*hidden")
     p.add_argument("--batch", type=int, default=4)
     p.add_argument("--seq", type=int, default=2048)
+    p.add_argument("--layer", default="linear", choices=["linear", "gpt"],
+                   help="linear: the north_star linear block (default); gpt: the full pre-LN layer "
+                        "(LayerNorm + causal softmax attention core, SURVEY NEXT #1)")
     p.add_argument("--mesh", default="", help="d1xd2; default: atp_search (uniform NVSwitch HCM, or --probe)")
     p.add_argument("--fused-ar", action="store_true",
                    help="N>1: fused peer-memory all-reduce (CUDA IPC) instead of NCCL on the data path")
@@ -191,6 +194,57 @@ def cpu_baseline(h: int, F: int, heads: int, seed: int, target_s: float) -> dict
                       f"DeviceMesh(1,1), {t:.1f} s", "seconds": t, "tokens": T_s}
 
 
+def traffic_for(peaks_path: str, h: int, T: int):
+    """Measured DRAM bytes (read + write) per GEMM launch of this workload's step,
+    from the committed ncu --set full capture (profiles/*_gemm_traffic.json,
+    written by scripts/ncu_traffic.py); None when there is none for (h, T)."""
+    import glob
+
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_gemm_traffic.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:  # noqa: BLE001
+            continue
+        if d.get("hidden") == h and d.get("tokens") == T and d.get("gemm_launches"):
+            best = {"dram_bytes_per_gemm_launch": d["gemm_dram_bytes"] / d["gemm_launches"],
+                    "algorithmic_bytes_per_gemm_launch": d.get("gemm_algorithmic_bytes", 0) / d["gemm_launches"],
+                    "source": os.path.relpath(f, ROOT)}
+    return best
+
+
+def gpt_flops(T: int, h: int, F: int, seq: int) -> float:
+    """FLOPs the full causal layer performs fwd+bwd: the linear block plus the
+    attention core (forward 4*d per visible (query, key) pair and head = 2(s+1)Th
+    for causal rows; backward 2.5x)."""
+    return layer_flops(T, h, F) + 7.0 * (seq + 1) * T * h
+
+
+def gpt_flops_paper(T: int, h: int, seq: int) -> float:
+    """The paper's per-layer count 72bsh^2 + 12bs^2h (non-causal core, F = 4h)."""
+    return 72.0 * T * h * h + 12.0 * T * seq * h
+
+
+def cpu_baseline_gpt(h: int, F: int, heads: int, seq: int, seed: int) -> dict:
+    """The full-layer oracle (fp64 NumPy, oracle/gpt.py) on one whole sequence."""
+    import datagen
+    from oracle import gpt
+
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        threads = os.cpu_count()
+    g = {k: v.astype("float64") for k, v in datagen.gpt_globals(seq, h, F, seed).items()}
+    t0 = time.time()
+    fw = gpt.dense_forward(g, heads, seq)
+    gpt.dense_backward(g, fw, g["dz"], heads, seq)
+    t = time.time() - t0
+    return {"value": gpt_flops(seq, h, F, seq) / t / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": f"1 sequence ({seq} tokens) of the full layer (h={h}, F={F}, {heads} heads, causal), "
+                      f"fp64 NumPy dense oracle, {t:.1f} s", "seconds": t, "tokens": seq}
+
+
 def _quiet(fn):
     """Run fn with fd 1 redirected to stderr (NCCL prints its version banner on
     stdout at communicator init; stdout carries only the JSON line)."""
@@ -324,7 +378,19 @@ def main() -> None:
         # one stage's partial sums [T, widest local output] in bf16
         mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
 
-    bufs = atp.alloc_layer_rank(d1, d2, rank, T, h, F, dev, a.seed)
+    gpt_mode = a.layer == "gpt"
+    if gpt_mode:
+        bufs = atp.alloc_gpt_rank(d1, d2, rank, T, h, F, heads, dev, a.seed)
+        if a.chunks == 0:
+            chunks = 1 if world == 1 else min(4, a.batch)  # whole sequences; the paper's "2 or 4"
+
+        def make_call(bb, c):
+            return atp.GptCall(mesh, [bb], T, h, F, heads, a.seq, c, True)
+    else:
+        bufs = atp.alloc_layer_rank(d1, d2, rank, T, h, F, dev, a.seed)
+
+        def make_call(bb, c):
+            return atp.LayerCall(mesh, [bb], T, h, F, heads, c, True)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -354,7 +420,7 @@ def main() -> None:
     # model (planner.py, §4.1/§4.2) at --busbw, take the fastest (same on every
     # rank: the timings are max-reduced over ranks before the choice).
     chunk_choice = None
-    if world > 1 and a.chunks == 0 and (d1 > 1 or d2 > 1):
+    if world > 1 and a.chunks == 0 and (d1 > 1 or d2 > 1) and not gpt_mode:
         from paper_2301_08658_b200 import planner
 
         comp = {}
@@ -369,7 +435,7 @@ def main() -> None:
         _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 1))
         chunks, pred = planner.choose_chunks(T, h, F, d1, d2, comp, a.busbw)
         chunk_choice = {"compute_ms": comp, "predicted_ms": pred, "busbw_gbs": a.busbw, "chosen": chunks}
-    call = atp.LayerCall(mesh, [bufs], T, h, F, heads, chunks, True)
+    call = make_call(bufs, chunks)
 
     for _ in range(max(3, a.warmup)):
         call(stream)
@@ -389,7 +455,7 @@ def main() -> None:
     clocks = sampler.stop(t0, t1)
     launches = int(n1.value - n0.value)
 
-    fl = layer_flops(T, h, F)
+    fl = gpt_flops(T, h, F, a.seq) if gpt_mode else layer_flops(T, h, F)
     value = fl / (ms * 1e-3) / 1e12
     per_gpu = value / world
 
@@ -414,7 +480,7 @@ def main() -> None:
     gemm_tflops = (prof.flops[0] / n_prof) / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     peak_tc = pk["bf16_tflops_sustained"] or pk["bf16_tflops"]
     roofline = {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_tc, "unit": "TFLOP/s",
-                "frac": gemm_tflops / peak_tc, "traffic": None,
+                "frac": gemm_tflops / peak_tc, "traffic": traffic_for(a.peaks, h, T),
                 "kernel": "gemm_sm100_kernel (tcgen05, all GEMM launches of the step)",
                 "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside a long step)",
                 "gemm_share_of_step": gemm_ms / ms_prof if ms_prof > 0 else None,
@@ -425,6 +491,14 @@ def main() -> None:
                 "allreduce_busbw_gbs": (prof.bytes[2] / max(prof.ms[2], 1e-9)) / 1e6 if prof.ms[2] > 0 else None,
                 "profiled_ms_per_step": ms_prof,
                 "layer_roofline_frac": (fl / world / (peak_tc * 1e12)) / (ms * 1e-3)}
+    if gpt_mode:
+        att_ms = prof.ms[3] / n_prof
+        roofline.update({
+            "attention_ms_per_step": att_ms,
+            "attention_tflops": (prof.flops[3] / n_prof) / (att_ms * 1e-3) / 1e12 if att_ms > 0 else None,
+            "attention_share_of_step": att_ms / ms_prof if ms_prof > 0 else None,
+            "tensor_achieved_gemm_plus_attention": ((prof.flops[0] + prof.flops[3]) / n_prof)
+            / ((gemm_ms + att_ms) * 1e-3) / 1e12})
 
     # ---- e2e: every step's inputs (X, dZ) H2D from pinned host memory and its
     # result (the bias gradients) D2H, through the public API.  Inputs are
@@ -438,7 +512,7 @@ def main() -> None:
         h2d = hx.numel() * hx.element_size() + hdz.numel() * hdz.element_size()
         d2h = sum(r.numel() * r.element_size() for r in res)
         bufs_b = dict(bufs, x=torch.empty_like(bufs["x"]), dz=torch.empty_like(bufs["dz"]))
-        sets = [(bufs, call), (bufs_b, atp.LayerCall(mesh, [bufs_b], T, h, F, heads, chunks, True))]
+        sets = [(bufs, call), (bufs_b, make_call(bufs_b, chunks))]
         copy_stream = torch.cuda.Stream()
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -479,12 +553,14 @@ def main() -> None:
             ms_e2e = float(t.item())
         e2e = {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-               "api": "paper_2301_08658_b200.LayerCall -> atp_layer_fwd_bwd (C ABI)",
+               "api": ("paper_2301_08658_b200.GptCall -> atp_gpt_layer_fwd_bwd (C ABI)" if gpt_mode else
+                       "paper_2301_08658_b200.LayerCall -> atp_layer_fwd_bwd (C ABI)"),
                "note": "X, dZ copied H2D every step (double-buffered on a copy stream), bias grads read D2H"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(h, F, heads, a.seed, a.cpu_seconds)
+        cpu = (cpu_baseline_gpt(h, F, heads, a.seq, a.seed) if gpt_mode
+               else cpu_baseline(h, F, heads, a.seed, a.cpu_seconds))
 
     mesh.destroy()
     if rank == 0:
@@ -492,8 +568,11 @@ def main() -> None:
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
             "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"gpt-layer linear block (QKV/Out/FC1/FC2 fwd+bwd) h{h} a{heads} ffn{F} "
-                                   f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}",
+            "config": {"workload": (f"full pre-LN GPT layer (LN + QKV + causal softmax attention + Out + LN + MLP, "
+                                    f"fwd+bwd) h{h} a{heads} ffn{F} s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), "
+                                    f"chunks {chunks}") if gpt_mode else
+                                   (f"gpt-layer linear block (QKV/Out/FC1/FC2 fwd+bwd) h{h} a{heads} ffn{F} "
+                                    f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}"),
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
                        "allreduce": "fused peer-memory kernel" if (a.fused_ar and world > 1) else "nccl",
@@ -505,6 +584,10 @@ def main() -> None:
         }
         if chunk_choice is not None:
             out["chunk_choice"] = chunk_choice
+        if gpt_mode:
+            out["tflops_paper_formula"] = gpt_flops_paper(T, h, a.seq) / (ms * 1e-3) / 1e12
+            out["flops_note"] = ("value counts the FLOPs performed (linear 72Th^2 + causal core 7(s+1)Th); "
+                                 "tflops_paper_formula uses P:375's 72bsh^2 + 12bs^2h (non-causal core)")
         if plan is not None:
             out["search"] = {"chosen": plan["chosen"], "ranked": [(r["d1"], r["d2"], r["t_comm"], r["calibrated"])
                                                                    for r in plan["ranked"]]}
