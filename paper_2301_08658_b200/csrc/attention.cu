@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 
 #include "atp_internal.h"
@@ -46,6 +47,13 @@ constexpr float kLn2 = 0.6931471805599453f;
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// 2^x (MUFU.EX2, flush-to-zero; 2^-inf = 0)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -272,6 +280,227 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const __grid_constant_
 }
 
 constexpr int kFwdSmem = 6 * kTile + 128 + 1024;
+
+// ---------------------------------------------------------------- forward v2
+// Two 128-row query tiles per CTA (query blocks 2m and 2m+1 of a sequence)
+// share each K/V block; each tile has its own softmax warpgroup (warps 2-5:
+// tile 0, warps 6-9: tile 1).  P goes back into TMEM over its S columns
+// (bf16 pairs) and is the A operand of O += P V straight from TMEM, so the
+// MMA warp ping-pongs: PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) — the tensor core
+// works on one tile while the other tile's softmax runs.  The score row is
+// read from TMEM twice (max pass, then exp pass) in 32-column slices to keep
+// register pressure low.  TMEM: tile t at [256t, 256t+256): S/P [0,128),
+// O [128,256).  Shared memory: Q0, Q1, and two K/V stages (192 KB).
+__global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant__ CUtensorMap tm_qkv, FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  auto sQ = [&](int t) { return base + t * kTile; };
+  auto sK = [&](int s) { return base + 2 * kTile + s * 2 * kTile; };
+  auto sV = [&](int s) { return base + 3 * kTile + s * 2 * kTile; };
+  const uint32_t bars = base + 6 * kTile;
+  const uint32_t q_full = bars;
+  auto kv_full = [&](int s) { return bars + 8 + 8 * s; };
+  auto kv_empty = [&](int s) { return bars + 24 + 8 * s; };
+  auto s_full = [&](int t) { return bars + 40 + 8 * t; };
+  auto p_full = [&](int t) { return bars + 56 + 8 * t; };
+  auto o_done = [&](int t) { return bars + 72 + 8 * t; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 88 - raw));
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nq = p.seq / BQ, nm = (nq + 1) / 2, nseq = p.T / p.seq;
+  const int per = p.heads * nseq;
+  int m = static_cast<int>(blockIdx.x) / per;
+  if (p.causal) m = nm - 1 - m;  // heaviest first
+  const int rest = static_cast<int>(blockIdx.x) % per;
+  const int head = rest % p.heads, sq = rest / p.heads;
+  const int row0 = sq * p.seq;
+  int qblk[2], n[2];
+  for (int t = 0; t < 2; ++t) {
+    qblk[t] = 2 * m + t;
+    n[t] = qblk[t] < nq ? (p.causal ? qblk[t] + 1 : nq) : 0;
+  }
+  const int nkv = n[0] > n[1] ? n[0] : n[1];
+  const int qcol = head * 3 * HD;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(kv_full(s), 1);
+      ptx::mbar_init(kv_empty(s), 1);
+      ptx::mbar_init(s_full(s), 1);
+      ptx::mbar_init(p_full(s), 128);
+      ptx::mbar_init(o_done(s), 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tm_qkv);
+      ptx::mbar_arrive_expect_tx(q_full, (n[1] > 0 ? 2 : 1) * kTile);
+      for (int t = 0; t < 2; ++t) {
+        if (n[t] == 0) continue;
+        const int qr = row0 + qblk[t] * BQ;
+        ptx::tma_load_2d(sQ(t), &tm_qkv, q_full, qcol, qr);
+        ptx::tma_load_2d(sQ(t) + kHalf, &tm_qkv, q_full, qcol + 64, qr);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j & 1;
+        ptx::mbar_wait(kv_empty(s), ((j >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(kv_full(s), 2 * kTile);
+        const int kr = row0 + j * BKV;
+        ptx::tma_load_2d(sK(s), &tm_qkv, kv_full(s), qcol + HD, kr);
+        ptx::tma_load_2d(sK(s) + kHalf, &tm_qkv, kv_full(s), qcol + HD + 64, kr);
+        ptx::tma_load_2d(sV(s), &tm_qkv, kv_full(s), qcol + 2 * HD, kr);
+        ptx::tma_load_2d(sV(s) + kHalf, &tm_qkv, kv_full(s), qcol + 2 * HD + 64, kr);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, 128, 0, 1);
+      int kv_seen = -1;
+      auto need_kv = [&](int j) {
+        if (j > kv_seen) {
+          ptx::mbar_wait(kv_full(j & 1), (j >> 1) & 1);
+          ptx::tc_fence_after();
+          kv_seen = j;
+        }
+      };
+      auto issue_s = [&](int t, int j) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ptx::mma_bf16_ss(tmem + 256 * t, desc_kmajor(sQ(t), kk), desc_kmajor(sK(j & 1), kk), idesc_s,
+                           kk > 0 ? 1u : 0u);
+        ptx::mma_commit(s_full(t));
+      };
+      ptx::mbar_wait(q_full, 0);
+      need_kv(0);
+      for (int t = 0; t < 2; ++t)
+        if (n[t] > 0) issue_s(t, 0);
+      for (int j = 0; j < nkv; ++j) {
+        for (int t = 0; t < 2; ++t) {
+          if (j >= n[t]) continue;
+          ptx::mbar_wait(p_full(t), j & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            ptx::mma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, desc_mnmajor(sV(j & 1), kk), idesc_o,
+                             (j | kk) != 0 ? 1u : 0u);
+          ptx::mma_commit(o_done(t));
+          if (j + 1 < n[t]) {
+            need_kv(j + 1);
+            issue_s(t, j + 1);
+          }
+        }
+        ptx::mma_commit(kv_empty(j & 1));
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax of tile t, row r
+    const int t = (warp - 2) / 4;
+    const int nt = t ? n[1] : n[0], qbt = t ? qblk[1] : qblk[0];
+    const int q4 = warp % 4;  // TMEM lane quarter this warp may access
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t tS = tmem + lane_off + 256 * t, tO = tS + 128;
+    float m_run = -INFINITY, l = 0.f;
+    for (int j = 0; j < nt; ++j) {
+      ptx::mbar_wait(s_full(t), j & 1);
+      ptx::tc_fence_after();
+      uint32_t u[BKV / 32][32];  // the whole score row: four loads, one wait
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) ptx::tmem_ld_32x32b_x32(tS + c * 32, u[c]);
+      ptx::tmem_wait_ld();
+      if (p.causal && j == qbt) {  // diagonal block: keys after the query row are masked
+#pragma unroll
+        for (int c = 0; c < BKV; ++c)
+          if (c > r) u[c / 32][c % 32] = __float_as_uint(-INFINITY);
+      }
+      float mb = __uint_as_float(u[0][0]);
+#pragma unroll
+      for (int c = 1; c < BKV; ++c) mb = fmaxf(mb, __uint_as_float(u[c / 32][c % 32]));
+      mb *= p.scale_log2;
+      // Lazy rescale (warp-uniform: tcgen05.ld/st are warp-collective).  P is
+      // written with the new max first; O is corrected afterwards, once the
+      // score row is dead, still before p_full releases PV(j).  PV(j-1) is
+      // complete here: S(j) was issued after it.
+      const bool rescale = __any_sync(0xffffffffu, mb > m_run + 8.f);
+      float f = 1.f;
+      if (rescale) {
+        const float m_new = fmaxf(m_run, mb);
+        f = ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float e0 = ex2(fmaf(__uint_as_float(u[c][2 * i]), p.scale_log2, -m_run));
+          const float e1 = ex2(fmaf(__uint_as_float(u[c][2 * i + 1]), p.scale_log2, -m_run));
+          rs += e0 + e1;
+          pk[i] = pack_bf16(e0, e1);
+        }
+        ptx::tmem_st_32x32b_x16(tS + c * 16, pk);  // P (bf16 pairs) over the S columns
+      }
+      l = l * f + rs;
+      if (rescale && j > 0) {
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          ptx::tmem_ld_32x32b_x32(tO + c * 32, o);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+          ptx::tmem_st_32x32b_x32(tO + c * 32, o);
+        }
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full(t));
+    }
+    if (nt > 0) {
+      ptx::mbar_wait(o_done(t), (nt - 1) & 1);
+      ptx::tc_fence_after();
+      const float inv = 1.f / l;
+      const int qrow = row0 + qbt * BQ + r;
+      __nv_bfloat16* orow = p.ctx + static_cast<int64_t>(qrow) * p.ld_ctx + head * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tO + c * 32, u);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + 8 * v) = w;
+        }
+      }
+      p.lse[static_cast<int64_t>(head) * p.T + qrow] = (m_run + log2f(l)) * kLn2;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
 
 // ================================================================ backward
 // dV = P^T dO, dP = dO V^T, dS = P * (dP - D) with D = rowsum(dO * O),
@@ -553,9 +782,15 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
                             int64_t ld_ctx, float* lse, cudaStream_t st) {
   alignas(64) CUtensorMap tm;
   if (!tmap_bf16_2d(&tm, qkv, T, 3 * heads * HD, ld_qkv, 128, 64)) return cudaErrorInvalidValue;
+  static const bool v1 = [] {
+    const char* e = getenv("ATP_ATTN_FWD");
+    return e && e[0] == '1';
+  }();
   static bool attr = [] {
     return cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem) ==
-           cudaSuccess;
+               cudaSuccess &&
+           cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem) ==
+               cudaSuccess;
   }();
   (void)attr;
   FwdParams p;
@@ -567,8 +802,11 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
   p.ctx = static_cast<__nv_bfloat16*>(ctx);
   p.ld_ctx = ld_ctx;
   p.lse = lse;
-  const int grid = (seq / BQ) * heads * (T / seq);
-  attn_fwd_kernel<<<grid, 256, kFwdSmem, st>>>(tm, p);
+  if (v1) {
+    attn_fwd_kernel<<<(seq / BQ) * heads * (T / seq), 256, kFwdSmem, st>>>(tm, p);
+  } else {
+    attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwdSmem, st>>>(tm, p);
+  }
   return cudaGetLastError();
 }
 
