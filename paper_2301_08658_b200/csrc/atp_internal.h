@@ -71,5 +71,8 @@ int num_sms();
 // box [box_rows, box_cols], 128B swizzle, out-of-bounds reads as zero.
 bool tmap_bf16_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                   int box_cols);
+// Same for fp32 (box_cols * 4 <= 128 bytes).
+bool tmap_f32_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                 int box_cols);
 
 }  // namespace atp

@@ -519,12 +519,14 @@ struct BwdParams {
   const float* lse;  // [heads][T] natural log (forward output)
   const float* D;    // [heads][T] rowsum(dO * O)
   float* dq_acc;     // [T][heads*128] fp32
+  int skip_dq;       // timing experiments only (ATP_ATTN_NO_DQ=1): results wrong
   __nv_bfloat16* dqkv;
   int64_t ld_dqkv;
 };
 
-__global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
-                                                          const __grid_constant__ CUtensorMap tm_do, BwdParams p) {
+__global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                                                          const __grid_constant__ CUtensorMap tm_do,
+                                                          const __grid_constant__ CUtensorMap tm_dq, BwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -549,13 +551,13 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant_
     ptx::mbar_init(qdo_full, 1);
     ptx::mbar_init(qdo_empty, 1);
     ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(ds_full, 128);
+    ptx::mbar_init(ds_full, 256);
     ptx::mbar_init(dq_full, 1);
-    ptx::mbar_init(s_free, 128);
+    ptx::mbar_init(s_free, 256);
     ptx::mbar_init(done, 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 2) {
+  if (warp == 1) {
     ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
     ptx::tmem_relinquish();
   }
@@ -591,13 +593,16 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant_
       ptx::mbar_wait(kv_full, 0);
       for (int t = 0; t < n; ++t) {
         ptx::mbar_wait(qdo_full, t & 1);
-        if (t > 0) ptx::mbar_wait(s_free, (t - 1) & 1);  // dQ tile of t-1 read out of TMEM
         ptx::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
+        for (int kk = 0; kk < HD / 16; ++kk)  // S = Q K^T
           ptx::mma_bf16_ss(tmem, desc_kmajor(sQ, kk), desc_kmajor(sK, kk), id_kk, kk > 0 ? 1u : 0u);
+        if (t > 0) {
+          ptx::mbar_wait(s_free, (t - 1) & 1);  // dQ tile of t-1 read out of the dP columns
+          ptx::tc_fence_after();
+        }
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
+        for (int kk = 0; kk < HD / 16; ++kk)  // dP = dO V^T
           ptx::mma_bf16_ss(tmem + 128, desc_kmajor(sdO, kk), desc_kmajor(sV, kk), id_kk, kk > 0 ? 1u : 0u);
         ptx::mma_commit(s_full);
         ptx::mbar_wait(ds_full, t & 1);
@@ -608,17 +613,18 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant_
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk)  // dK += dS^T Q
           ptx::mma_bf16_ss(tmem + 384, desc_mnmajor(sdS, kk), desc_mnmajor(sQ, kk), id_mm, (t | kk) != 0 ? 1u : 0u);
+        ptx::mma_commit(qdo_empty);  // Q and dO of t are no longer read: the next load can start
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)  // dQ tile = dS K
-          ptx::mma_bf16_ss(tmem, desc_kmajor(sdS, kk), desc_mnmajor(sK, kk), id_km, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < BKV / 16; ++kk)  // dQ tile = dS K (into the dP columns)
+          ptx::mma_bf16_ss(tmem + 128, desc_kmajor(sdS, kk), desc_mnmajor(sK, kk), id_km, kk > 0 ? 1u : 0u);
         ptx::mma_commit(dq_full);
-        ptx::mma_commit(qdo_empty);
       }
       ptx::mma_commit(done);
     }
-  } else if (warp >= 4) {
-    const int q4 = warp - 4;
-    const int r = q4 * 32 + lane;
+  } else {
+    // ---- warps 2-9: two threads per query row, columns [64*half, 64*half + 64)
+    const int half = (warp - 2) / 4, q4 = warp % 4;
+    const int r = q4 * 32 + lane, c0 = 64 * half;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const int ldq = p.heads * HD;
     for (int t = 0; t < n; ++t) {
@@ -628,60 +634,69 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant_
       const float Dr = p.D[static_cast<int64_t>(head) * p.T + qrow];
       ptx::mbar_wait(s_full, t & 1);
       ptx::tc_fence_after();
-      float pv[BKV];
+      uint32_t su[2][32], du[2][32];
 #pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t u[32];
-        ptx::tmem_ld_32x32b_x32(tmem + lane_off + c * 32, u);
-        ptx::tmem_wait_ld();
-#pragma unroll
-        for (int k = 0; k < 32; ++k) pv[c * 32 + k] = exp2f(__uint_as_float(u[k]) * p.scale_log2 - lse2);
+      for (int c = 0; c < 2; ++c) {
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + c0 + 32 * c, su[c]);
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + 128 + c0 + 32 * c, du[c]);
       }
-      if (p.causal && i == jb) {
+      ptx::tmem_wait_ld();
+      const bool diag = p.causal && i == jb;
 #pragma unroll
-        for (int c = 0; c < BKV; ++c)
-          if (c > r) pv[c] = 0.f;
-      }
+      for (int c = 0; c < 2; ++c) {
+        float pv[32], ds[32];
 #pragma unroll
-      for (int c16 = 0; c16 < BKV / 8; ++c16)
-        st_shared_v4(sP + sw128_off(r, c16), pack_bf16(pv[8 * c16], pv[8 * c16 + 1]),
-                     pack_bf16(pv[8 * c16 + 2], pv[8 * c16 + 3]), pack_bf16(pv[8 * c16 + 4], pv[8 * c16 + 5]),
-                     pack_bf16(pv[8 * c16 + 6], pv[8 * c16 + 7]));
+        for (int k = 0; k < 32; ++k) {
+          const float e = ex2(fmaf(__uint_as_float(su[c][k]), p.scale_log2, -lse2));
+          pv[k] = (diag && c0 + 32 * c + k > r) ? 0.f : e;
+          ds[k] = pv[k] * (__uint_as_float(du[c][k]) - Dr);
+        }
 #pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t u[32];
-        ptx::tmem_ld_32x32b_x32(tmem + lane_off + 128 + c * 32, u);
-        ptx::tmem_wait_ld();
-        float ds[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) ds[k] = pv[c * 32 + k] * (__uint_as_float(u[k]) - Dr);
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-          st_shared_v4(sdS + sw128_off(r, c * 4 + v), pack_bf16(ds[8 * v], ds[8 * v + 1]),
-                       pack_bf16(ds[8 * v + 2], ds[8 * v + 3]), pack_bf16(ds[8 * v + 4], ds[8 * v + 5]),
-                       pack_bf16(ds[8 * v + 6], ds[8 * v + 7]));
+        for (int v = 0; v < 4; ++v) {
+          const int c16 = (c0 + 32 * c) / 8 + v;
+          st_shared_v4(sP + sw128_off(r, c16), pack_bf16(pv[8 * v], pv[8 * v + 1]), pack_bf16(pv[8 * v + 2], pv[8 * v + 3]),
+                       pack_bf16(pv[8 * v + 4], pv[8 * v + 5]), pack_bf16(pv[8 * v + 6], pv[8 * v + 7]));
+          st_shared_v4(sdS + sw128_off(r, c16), pack_bf16(ds[8 * v], ds[8 * v + 1]), pack_bf16(ds[8 * v + 2], ds[8 * v + 3]),
+                       pack_bf16(ds[8 * v + 4], ds[8 * v + 5]), pack_bf16(ds[8 * v + 6], ds[8 * v + 7]));
+        }
       }
       ptx::fence_proxy_async();
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full);
-      // dQ tile (unscaled) -> fp32 accumulator
+      // dQ tile (unscaled) -> fp32 accumulator with one TMA bulk reduce-add per
+      // 32-column box: the tile is staged (SW128, conflict-free) in the P/dS
+      // region, free once the dQ MMA that read it has completed.
       ptx::mbar_wait(dq_full, t & 1);
       ptx::tc_fence_after();
-      float* dst = p.dq_acc + static_cast<int64_t>(qrow) * ldq + head * HD;
+      uint32_t qu[2][32];
 #pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t u[32];
-        ptx::tmem_ld_32x32b_x32(tmem + lane_off + c * 32, u);
-        ptx::tmem_wait_ld();
+      for (int c = 0; c < 2; ++c) ptx::tmem_ld_32x32b_x32(tmem + lane_off + 128 + c0 + 32 * c, qu[c]);
+      ptx::tmem_wait_ld();
+      if (p.skip_dq) {
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(s_free);
+        continue;
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t box = sP + static_cast<uint32_t>((c0 + 32 * c) / 32) * kHalf;  // [128 rows][32 fp32]
 #pragma unroll
         for (int v = 0; v < 8; ++v)
-          atomicAdd(reinterpret_cast<float4*>(dst + c * 32 + 4 * v),
-                    make_float4(__uint_as_float(u[4 * v]), __uint_as_float(u[4 * v + 1]),
-                                __uint_as_float(u[4 * v + 2]), __uint_as_float(u[4 * v + 3])));
+          st_shared_v4(box + r * 128 + ((v ^ (r & 7)) << 4), qu[c][4 * v], qu[c][4 * v + 1], qu[c][4 * v + 2],
+                       qu[c][4 * v + 3]);
+      }
+      ptx::fence_proxy_async();
+      ptx::named_bar_sync(1, 256);
+      if (warp == 2 && lane == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) ptx::tma_reduce_add_2d(&tm_dq, sP + b * kHalf, head * HD + 32 * b, row0 + i * BQ);
+        ptx::bulk_commit();
+        ptx::bulk_wait_read0();  // staging may be overwritten (next P/dS) only after the reads
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(s_free);
     }
+    if (warp == 2 && lane == 0) ptx::bulk_wait0();  // reductions complete before the dQ finalize kernel
     // ---- dK (scaled), dV -> dqkv rows of this key block (TMEM lane = key row)
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
@@ -690,9 +705,9 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant_
     for (int which = 0; which < 2; ++which) {  // 0: dK, 1: dV
       const float f = which == 0 ? p.scale : 1.f;
 #pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        ptx::tmem_ld_32x32b_x32(tmem + lane_off + (which == 0 ? 384 : 256) + c * 32, u);
+        ptx::tmem_ld_32x32b_x32(tmem + lane_off + (which == 0 ? 384 : 256) + c0 + 32 * c, u);
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
@@ -701,14 +716,14 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_kernel(const __grid_constant_
           w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * f, __uint_as_float(u[8 * v + 3]) * f);
           w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * f, __uint_as_float(u[8 * v + 5]) * f);
           w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * f, __uint_as_float(u[8 * v + 7]) * f);
-          *reinterpret_cast<uint4*>(drow + (which == 0 ? HD : 2 * HD) + c * 32 + 8 * v) = w;
+          *reinterpret_cast<uint4*>(drow + (which == 0 ? HD : 2 * HD) + c0 + 32 * c + 8 * v) = w;
         }
       }
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
@@ -817,9 +832,10 @@ size_t attn_workspace_bytes(int64_t T, int heads) {
 cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, int64_t ld_ctx, const float* lse,
                             const void* dctx, int64_t ld_dctx, int T, int seq, int heads, int causal, void* dqkv,
                             int64_t ld_dqkv, void* workspace, cudaStream_t st) {
-  alignas(64) CUtensorMap tq, td;
+  alignas(64) CUtensorMap tq, td, tdq;
   if (!tmap_bf16_2d(&tq, qkv, T, 3 * heads * HD, ld_qkv, 128, 64)) return cudaErrorInvalidValue;
   if (!tmap_bf16_2d(&td, dctx, T, heads * HD, ld_dctx, 128, 64)) return cudaErrorInvalidValue;
+  if (!tmap_f32_2d(&tdq, workspace, T, heads * HD, heads * HD, 128, 32)) return cudaErrorInvalidValue;
   static bool attr = [] {
     return cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem) ==
            cudaSuccess;
@@ -840,10 +856,15 @@ cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, in
   p.lse = lse;
   p.D = D;
   p.dq_acc = dq_acc;
+  static const int skip_dq = [] {
+    const char* e = getenv("ATP_ATTN_NO_DQ");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  p.skip_dq = skip_dq;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dqkv = ld_dqkv;
   const int grid = (seq / BKV) * heads * (T / seq);
-  attn_bwd_kernel<<<grid, 256, kBwdSmem, st>>>(tq, td, p);
+  attn_bwd_kernel<<<grid, 320, kBwdSmem, st>>>(tq, td, tdq, p);
   attn_bwd_dq_kernel<<<sms * 8, 256, 0, st>>>(dq_acc, T, heads, p.scale, static_cast<__nv_bfloat16*>(dqkv), ld_dqkv);
   return cudaGetLastError();
 }
