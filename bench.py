@@ -382,7 +382,7 @@ def main() -> None:
     if gpt_mode:
         bufs = atp.alloc_gpt_rank(d1, d2, rank, T, h, F, heads, dev, a.seed)
         if a.chunks == 0:
-            chunks = 1 if world == 1 else min(4, a.batch)  # whole sequences; the paper's "2 or 4"
+            chunks = 1 if world == 1 else min(2, a.batch)  # whole sequences; "2 or 4" (2: attention occupancy)
 
         def make_call(bb, c):
             return atp.GptCall(mesh, [bb], T, h, F, heads, a.seq, c, True)
