@@ -35,6 +35,7 @@ struct GemmDesc {
   int bn = 0;        // 128 or 256 (0 = choose)
   int cg = 0;        // 1 = single CTA (128 x bn tile), 2 = CTA pair (256 x bn); 0 = choose
   int max_ctas = 0;  // persistent grid cap (0 = all SMs)
+  int group_m = 16;  // M-tiles per raster group (raster_group_m)
   int epi = EPI_BF16;
   EpiParams ep;
   // Chunk signalling (schedule.cpp "signalled stages"): tiles run chunk by
@@ -67,6 +68,7 @@ cudaError_t gemm_launch_f32(const GemmDesc& d, cudaStream_t st);
 void gemm_plan_tile(int M, int N, int* bn, int* cg);
 int gemm_tiles(const GemmDesc& d);
 int num_sms();
+int raster_group_m(int rows_per_mtile, int K);
 // 2-D bf16 TMA map over a row-major [rows, cols] matrix (pitch ld elements),
 // box [box_rows, box_cols], 128B swizzle, out-of-bounds reads as zero.
 bool tmap_bf16_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,

@@ -87,15 +87,15 @@ struct SmemLayout {
 // not signalling), and inside a chunk groups of kGroupM M-tiles sweep all
 // N-tiles, so the ~148 tiles in flight share a few A row-blocks and B
 // column-blocks in L2.
-constexpr int kGroupM = 16;
-__device__ __forceinline__ void tile_coords(int tile, int mt_chunk, int num_n, int& mt, int& nt, int& chunk) {
+__device__ __forceinline__ void tile_coords(int tile, int mt_chunk, int num_n, int group_m, int& mt, int& nt,
+                                            int& chunk) {
   const int per_chunk = mt_chunk * num_n;
   chunk = tile / per_chunk;
   const int r0 = tile - chunk * per_chunk;
-  const int per_group = kGroupM * num_n;
+  const int per_group = group_m * num_n;
   const int g = r0 / per_group;
-  const int first = g * kGroupM;
-  const int gm = min(kGroupM, mt_chunk - first);
+  const int first = g * group_m;
+  const int gm = min(group_m, mt_chunk - first);
   const int r = r0 - g * per_group;
   mt = chunk * mt_chunk + first + r % gm;
   nt = r / gm;
@@ -211,7 +211,7 @@ template <int CG, int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows, const uint32_t* gate,
-                      uint32_t gate_target) {
+                      uint32_t gate_target, int group_m) {
   using L = SmemLayout<CG, BN, STAGES>;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr int BNC = BN / CG;  // B rows loaded by this CTA
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int gated_chunk = -1;
       for (int tile = unit; tile < num_tiles; tile += n_units) {
         int mt, nt, chunk;
-        tile_coords(tile, mt_chunk, num_n, mt, nt, chunk);
+        tile_coords(tile, mt_chunk, num_n, group_m, mt, nt, chunk);
         const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
         const int nb = nt * BN + BNC * static_cast<int>(cta_rank);
         if (gate != nullptr && chunk > gated_chunk) {  // tiles are chunk-major: chunk only grows
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = unit; tile < num_tiles; tile += n_units) {
       int mt, nt, chunk;
-      tile_coords(tile, mt_chunk, num_n, mt, nt, chunk);
+      tile_coords(tile, mt_chunk, num_n, group_m, mt, nt, chunk);
       const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
       const int n0 = nt * BN;
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
@@ -497,8 +497,8 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate,
-                            d.gate_target);
+  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate, d.gate_target,
+                            d.group_m > 0 ? d.group_m : 16);
 }
 
 template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>
@@ -533,6 +533,22 @@ int gemm_mode() {
 }
 
 }  // namespace
+
+// M-tiles per raster group (tiles sweep all N-tiles of a group before the next
+// group).  Default: the largest g <= 16 whose A panel (g M-tiles x K, bf16)
+// stays within ~40 MB of L2, so the group's A rows are read from HBM once
+// (K = 16384 -> 4... 16 for K <= 4096).  ATP_GROUP_M=g > 0 fixes it (A/B runs:
+// profiles/r01_raster_ab.log; +0.8% step throughput over a fixed 16).
+int raster_group_m(int rows_per_mtile, int K) {
+  static const int env = [] {
+    const char* e = getenv("ATP_GROUP_M");
+    return e ? atoi(e) : -1;
+  }();
+  if (env > 0) return env;
+  const double panel = static_cast<double>(rows_per_mtile) * K * 2.0;
+  int g = static_cast<int>(40e6 / panel);
+  return g < 1 ? 1 : (g > 16 ? 16 : g);
+}
 
 bool tmap_bf16_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                   int box_cols) {
@@ -586,6 +602,7 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
   d.a_mn = a_mn;
   d.b_mn = b_mn;
   if (d.bn != 128 && d.bn != 256) gemm_plan_tile(M, N, &d.bn, &d.cg);
+  d.group_m = raster_group_m(d.cg == 2 ? 256 : BM, K);
   if (d.cg != 1 && d.cg != 2) d.cg = (d.bn == 256 && M >= 256 && gemm_mode() != 1) ? 2 : 1;
   if (d.cg == 2 && d.bn != 256) d.cg = 1;
   bool ok;
