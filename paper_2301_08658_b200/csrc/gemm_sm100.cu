@@ -537,7 +537,8 @@ int gemm_mode() {
 // M-tiles per raster group (tiles sweep all N-tiles of a group before the next
 // group).  Default: the largest g <= 16 whose A panel (g M-tiles x K, bf16)
 // stays within ~40 MB of L2, so the group's A rows are read from HBM once
-// (K = 16384 -> 4... 16 for K <= 4096).  ATP_GROUP_M=g > 0 fixes it (A/B runs:
+// (256-row M-tiles: K = 16384 -> 4, 12288 -> 6, 8192 -> 9, <= 4096 -> 16).
+// ATP_GROUP_M=g > 0 fixes it (A/B runs:
 // profiles/r01_raster_ab.log; +0.8% step throughput over a fixed 16).
 int raster_group_m(int rows_per_mtile, int K) {
   static const int env = [] {
