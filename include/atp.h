@@ -80,6 +80,16 @@ atp_status atp_get_unique_id(uint8_t uid_out[128]);
 atp_status atp_mesh_init(int d1, int d2, int world_rank, const uint8_t uid[128], int cuda_device,
                          atp_mesh** out);
 /* All d1*d2 ranks of a mesh in this process on `cuda_device` (see header). */
+/* Borrow the caller's communicators (SURVEY §8(b) variant): dim1_comm holds
+ * the d1 ranks sharing this rank's i2 (this rank at position i1), dim2_comm
+ * the d2 ranks sharing i1 (at position i2), with rank = i1*d2 + i2;
+ * ncclComm_t values passed as void*.  A comm of a size-1 dimension may be
+ * NULL.  The mesh never destroys borrowed comms; features that need a world
+ * communicator (atp_mesh_enable_fused_ar on a multi-rank mesh, probes) return
+ * an error.  Errors: ATP_ERR_INVALID (NULL comm of a dimension > 1, comm size
+ * or rank position not matching). */
+atp_status atp_mesh_init_from_comms(int d1, int d2, int world_rank, void* dim1_comm, void* dim2_comm,
+                                    int cuda_device, atp_mesh** out);
 atp_status atp_vmesh_init(int d1, int d2, int cuda_device, atp_mesh** out);
 /* Dry-run handle for ONE rank `rank` of DeviceMesh(d1, d2) on `cuda_device`
  * without communicators: every all-reduce of its schedule is elided (results
@@ -305,6 +315,19 @@ typedef struct {
 atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t T, int64_t h,
                              int64_t F, int64_t heads, int chunks, int do_backward,
                              atp_dtype dtype, void* stream);
+
+/* ------------------------------------------------------------------ workspace sizes
+ * Bytes of every caller-allocated workspace buffer of an op, in the order the
+ * op's argument struct names them (the library makes no hidden allocations):
+ *   ATP_OP_MLP_BWD   [ws_dh]                       (T x F/d1 bf16)
+ *   ATP_OP_ATTN_BWD  [ws_dctx, ws_dqkv]            (T x h/d1, T x 3h/d1 bf16)
+ *   ATP_OP_LAYER     [ws_dh, ws_dctx, ws_dqkv]
+ *   ATP_OP_GPT_LAYER [workspace of atp_gpt_layer_fwd_bwd, per rank]
+ * Unused entries are 0.  heads/seq/chunks matter only for ATP_OP_GPT_LAYER.
+ * Pure host computation.  Errors: ATP_ERR_INVALID. */
+typedef enum { ATP_OP_MLP_BWD = 0, ATP_OP_ATTN_BWD = 1, ATP_OP_LAYER = 2, ATP_OP_GPT_LAYER = 3 } atp_op;
+atp_status atp_workspace_size(int op, int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq,
+                              int chunks, size_t bytes[4]);
 
 /* ------------------------------------------------------------------ full GPT layer
  * One pre-LN GPT layer, forward then backward, on DeviceMesh(d1, d2) (SURVEY

@@ -128,6 +128,9 @@ SIGNATURES = {
     "atp_attn_core_bwd": (C.c_int, [vp, i64, vp, i64, vp, vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64,
                                     vp, C.c_size_t, vp]),
     "atp_attn_core_workspace": (C.c_size_t, [i64, C.c_int]),
+    "atp_mesh_init_from_comms": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(vp)]),
+    "atp_workspace_size": (C.c_int, [C.c_int, C.c_int, C.c_int, i64, i64, i64, i64, i64, C.c_int,
+                                     C.POINTER(C.c_size_t)]),
     "atp_gpt_workspace": (C.c_size_t, [C.c_int, C.c_int, i64, i64, i64, i64, i64, C.c_int]),
     "atp_gpt_layer_fwd_bwd": (C.c_int, [vp, C.POINTER(GptArgs), i64, i64, i64, i64, i64, C.c_int, C.c_int, vp,
                                         C.c_size_t, vp]),

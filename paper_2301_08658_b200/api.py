@@ -61,6 +61,13 @@ class Mesh:
         check(lib().atp_mesh_init(d1, d2, rank, uid, device, C.byref(h)))
         return cls(h, d1, d2, False, rank)
 
+    @classmethod
+    def from_comms(cls, d1: int, d2: int, rank: int, dim1_comm: int, dim2_comm: int, device: int) -> "Mesh":
+        """Mesh over the caller's NCCL communicators (ncclComm_t values as ints; borrowed, not destroyed)."""
+        h = C.c_void_p()
+        check(lib().atp_mesh_init_from_comms(d1, d2, rank, dim1_comm, dim2_comm, device, C.byref(h)))
+        return cls(h, d1, d2, False, rank)
+
     @property
     def n_local_ranks(self) -> int:
         return self.d1 * self.d2 if self.is_virtual else 1
@@ -261,6 +268,18 @@ class LayerCall:
 
 def atp_layer_fwd_bwd(mesh, bufs, T, h, F, heads, chunks=1, backward=True, stream=None):
     LayerCall(mesh, bufs, T, h, F, heads, chunks, backward)(stream)
+
+
+# ------------------------------------------------------------------ workspace sizes
+ATP_OP_MLP_BWD, ATP_OP_ATTN_BWD, ATP_OP_LAYER, ATP_OP_GPT_LAYER = 0, 1, 2, 3
+
+
+def atp_workspace_size(op: int, d1: int, d2: int, T: int, h: int, F: int, heads: int = 0, seq: int = 0,
+                       chunks: int = 1) -> list[int]:
+    """Bytes of each caller-allocated workspace buffer of `op` (struct order; unused = 0)."""
+    out = (C.c_size_t * 4)()
+    check(lib().atp_workspace_size(op, d1, d2, T, h, F, heads, seq, chunks, out))
+    return [int(v) for v in out]
 
 
 # ------------------------------------------------------------------ full GPT layer

@@ -73,6 +73,33 @@ atp_status atp_mesh_init_local(int d1, int d2, int rank, int cuda_device, atp_me
   return static_cast<atp_status>(atp::mesh_create(d1, d2, rank, nullptr, cuda_device, false, out));
 }
 
+atp_status atp_mesh_init_from_comms(int d1, int d2, int world_rank, void* dim1_comm, void* dim2_comm,
+                                    int cuda_device, atp_mesh** out) {
+  if ((d1 > 1 && dim1_comm == nullptr) || (d2 > 1 && dim2_comm == nullptr))
+    return fail(ATP_ERR_INVALID, "atp_mesh_init_from_comms: a communicator of a dimension of size > 1 is NULL");
+  atp_status s = static_cast<atp_status>(atp::mesh_create(d1, d2, world_rank, nullptr, cuda_device, false, out));
+  if (s) return s;
+  atp_mesh* m = *out;
+  auto check_comm = [&](void* c, int size, int pos) {
+    if (c == nullptr) return true;
+    int cnt = 0, rk = -1;
+    return ncclCommCount(static_cast<ncclComm_t>(c), &cnt) == ncclSuccess &&
+           ncclCommUserRank(static_cast<ncclComm_t>(c), &rk) == ncclSuccess && cnt == size && rk == pos;
+  };
+  if (!check_comm(dim1_comm, d1, m->i1) || !check_comm(dim2_comm, d2, m->i2)) {
+    atp::mesh_destroy(m);
+    *out = nullptr;
+    return fail(ATP_ERR_INVALID,
+                "atp_mesh_init_from_comms: dim-1 comm must have d1 ranks with this rank at i1, dim-2 comm d2 ranks at i2");
+  }
+  m->dim1 = static_cast<ncclComm_t>(dim1_comm);
+  m->dim2 = static_cast<ncclComm_t>(dim2_comm);
+  m->comms_borrowed = true;
+  m->local_only = false;
+  m->comm_enabled = true;
+  return ATP_OK;
+}
+
 atp_status atp_vmesh_init(int d1, int d2, int cuda_device, atp_mesh** out) {
   return static_cast<atp_status>(atp::mesh_create(d1, d2, 0, nullptr, cuda_device, true, out));
 }
@@ -392,6 +419,26 @@ atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t
     }
     return atp::build_layer(rv, p, T, h, F, heads, chunks, dtype, out);
   });
+}
+
+// ---------------------------------------------------------------- workspace sizes
+atp_status atp_workspace_size(int op, int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq,
+                              int chunks, size_t bytes[4]) {
+  if (bytes == nullptr || d1 < 1 || d2 < 1 || T < 1 || h < 1 || F < 1) return fail(ATP_ERR_INVALID, "atp_workspace_size: bad arguments");
+  bytes[0] = bytes[1] = bytes[2] = bytes[3] = 0;
+  const size_t t = static_cast<size_t>(T);
+  const size_t dh = t * (F / d1) * 2, dctx = t * (h / d1) * 2, dqkv = t * (3 * h / d1) * 2;
+  switch (op) {
+    case ATP_OP_MLP_BWD: bytes[0] = dh; break;
+    case ATP_OP_ATTN_BWD: bytes[0] = dctx; bytes[1] = dqkv; break;
+    case ATP_OP_LAYER: bytes[0] = dh; bytes[1] = dctx; bytes[2] = dqkv; break;
+    case ATP_OP_GPT_LAYER:
+      if (heads < 1 || seq < 1 || chunks < 1) return fail(ATP_ERR_INVALID, "atp_workspace_size: heads, seq, chunks");
+      bytes[0] = atp::gpt_workspace_bytes(d1, d2, T, h, F, heads, seq, chunks);
+      break;
+    default: return fail(ATP_ERR_INVALID, "atp_workspace_size: unknown op");
+  }
+  return ATP_OK;
 }
 
 // ---------------------------------------------------------------- full GPT layer

@@ -484,6 +484,10 @@ int enable_fused_ar(atp_mesh* m, size_t part_bytes) {
   const int n = d1 * d2;
   std::vector<cudaIpcMemHandle_t> all(n);
   if (!m->local_only && n > 1) {
+    if (m->world == nullptr) {
+      set_error("fused all-reduce: needs the world communicator (not available with borrowed communicators)");
+      return 1;
+    }
     cudaIpcMemHandle_t h;
     if ((e = cudaIpcGetMemHandle(&h, s.sym_base)) != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
     uint8_t* dbuf = nullptr;
@@ -628,8 +632,10 @@ int mesh_destroy(atp_mesh* m) {
     if (s.compute) cudaStreamSynchronize(s.compute);
     if (s.aux) cudaStreamSynchronize(s.aux);
   }
-  if (m->dim2) ncclCommDestroy(m->dim2);
-  if (m->dim1) ncclCommDestroy(m->dim1);
+  if (!m->comms_borrowed) {
+    if (m->dim2) ncclCommDestroy(m->dim2);
+    if (m->dim1) ncclCommDestroy(m->dim1);
+  }
   if (m->world) ncclCommDestroy(m->world);
   for (auto& s : m->rs) free_rank_state(s);
   for (auto& r : m->prof) {

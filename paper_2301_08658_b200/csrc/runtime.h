@@ -102,6 +102,7 @@ struct atp_mesh {
   int d1 = 1, d2 = 1;
   bool comm_enabled = true;
   bool local_only = false;  // atp_mesh_init_local: no communicators
+  bool comms_borrowed = false;  // atp_mesh_init_from_comms: dim1/dim2 belong to the caller, no world
   bool signalled = true;    // signalled stages (ATP_SIGNALLED=0 disables, for A/B runs)
   bool gated = false;       // chunk-gated GEMMs (atp_mesh_set_gating; ATP_GATED=1 initial value)
   bool profiling = false;

@@ -118,3 +118,20 @@ def test_comm_volume_matches_oracle(d1, d2, chunks):
     assert calls == cm.comm_volume(d1, d2, T, h, chunks)
     assert e1 == sum(c[4] for c in calls if c[2] == 1)
     assert e2 == sum(c[4] for c in calls if c[2] == 2)
+
+
+def test_workspace_size_matches_argument_shapes():
+    """atp_workspace_size reports exactly the bf16 workspace buffers the op structs name."""
+    import paper_2301_08658_b200 as atp
+    from paper_2301_08658_b200 import api
+
+    T, h, F = 512, 256, 1024
+    for d1, d2 in ((1, 1), (2, 1), (2, 4), (4, 2)):
+        assert api.atp_workspace_size(api.ATP_OP_MLP_BWD, d1, d2, T, h, F) == [T * F // d1 * 2, 0, 0, 0]
+        assert api.atp_workspace_size(api.ATP_OP_ATTN_BWD, d1, d2, T, h, F) == [T * h // d1 * 2, T * 3 * h // d1 * 2, 0, 0]
+        assert api.atp_workspace_size(api.ATP_OP_LAYER, d1, d2, T, h, F) == [T * F // d1 * 2, T * h // d1 * 2,
+                                                                             T * 3 * h // d1 * 2, 0]
+        g = api.atp_workspace_size(api.ATP_OP_GPT_LAYER, d1, d2, T, h, F, 8, 256, 2)
+        assert g[0] == atp._abi.lib().atp_gpt_workspace(d1, d2, T, h, F, 8, 256, 2) > 0 and g[1:] == [0, 0, 0]
+    with pytest.raises(atp._abi.AtpError):
+        api.atp_workspace_size(9, 1, 1, T, h, F)

@@ -314,3 +314,45 @@ def test_layer_gated_chunk_count_changes(fused):
             compare(bufs, fw, bw, d1, d2)
     finally:
         mesh.destroy()
+
+
+@pytest.mark.gpu
+def test_mesh_from_borrowed_comms():
+    """atp_mesh_init_from_comms: a mesh over caller-created NCCL
+    communicators (here 1-rank ones from the same libnccl libatp links) runs
+    the linear block like atp_mesh_init, and is destroyed without touching them."""
+    import ctypes as C
+    import os
+    import torch
+    import paper_2301_08658_b200 as atp
+    from paper_2301_08658_b200 import build as B
+
+    class UniqueId(C.Structure):  # ncclUniqueId, passed by value
+        _fields_ = [("internal", C.c_char * 128)]
+
+    nccl = C.CDLL(os.path.join(B.nccl_dir(), "lib", "libnccl.so.2"))
+    nccl.ncclGetUniqueId.argtypes = [C.POINTER(UniqueId)]
+    nccl.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, UniqueId, C.c_int]
+    nccl.ncclCommCount.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
+    nccl.ncclCommDestroy.argtypes = [C.c_void_p]
+    torch.cuda.set_device(0)
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+    comm = C.c_void_p()
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    T, h, F, heads, seed = 512, 256, 1024, 2, 3
+    g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, 1, 1, 1, seed)
+    mesh = atp.Mesh.from_comms(1, 1, 0, comm.value, comm.value, 0)
+    try:
+        bufs = atp.alloc_layer_rank(1, 1, 0, T, h, F, "cuda", seed)
+        atp.LayerCall(mesh, [bufs], T, h, F, heads, 1, True)()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    compare([bufs], fw, bw, 1, 1)
+    cnt = C.c_int()
+    assert nccl.ncclCommCount(comm, C.byref(cnt)) == 0 and cnt.value == 1  # still alive
+    nccl.ncclCommDestroy(comm)
+    from paper_2301_08658_b200._abi import AtpError
+    with pytest.raises(AtpError):
+        atp.Mesh.from_comms(2, 1, 0, None, None, 0)
