@@ -610,6 +610,7 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
   // compute-stream op of chunk k after its prologue (pending wait + deferred steps)
   auto gemm_k = [&](int k, const void* A, int64_t lda, const void* Wt, int64_t ldw, bool b_mn, int64_t N, int64_t K,
                     void* C, const void* bias, int epi, const void* aux, void* C2) {
+    b.gate_slot = -1;  // custom ops in between: the next stage must not gate on older chunk gates
     const int w = b.prologue(k);
     EpiParams ep;
     ep.C = C;
@@ -622,6 +623,7 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
     return b.gemm(A, lda, false, Wt, ldw, b_mn, Mc, N, K, epi, ep, {w}, -1) != nullptr;
   };
   auto ew_k = [&](int k, const EwDesc& e) {
+    b.gate_slot = -1;
     const int w = b.prologue(k);
     b.ew(e, 0, w);
   };
@@ -722,9 +724,6 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
   void* ctx_loc = d2 > 1 ? a.ctx_loc : a.ctx;
   const bool c1 = (d1 == 1), c2 = (d2 == 1);
   const void* bqkv_here = rv.i2 == 0 ? a.bqkv : nullptr;  // added once before the dim-2 reduction (G16)
-  const void* b1_here = rv.i2 == 0 ? a.b1 : nullptr;
-  const void* bo_here = rv.i1 == 0 ? a.bo : nullptr;
-  const void* b2_here = rv.i1 == 0 ? a.b2 : nullptr;
 
   // ================= forward
   layernorm(a.x, a.g1, a.be1, L.st1, a.sv1, a.a);
@@ -751,42 +750,62 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
       coll_k(k, 2, 2, R(ctx_loc, k, cl), R(W(L.ctxb), k, h1), Mc * cl, 0, {un});
     }
   }
-  for (int k = 0; k < chunks; ++k) {  // Out row-first, all-reduce on dim 1 (f2), residual
-    if (!gemm_k(k, R(a.ctx, k, h1), h1, a.wo, hc, true, hc, h1, R(a.y1, k, hc), bo_here, c1 ? EPI_RESID : EPI_BF16,
-                R(a.x, k, hc), nullptr))
-      return fail();
-    if (!c1) coll_k(k, 1, 0, R(a.y1, k, hc), nullptr, Mc * hc, 0, {E::ewd(EW_ADD, R(a.y1, k, hc), R(a.x, k, hc), Mc, hc)});
-  }
+  // Out row-first, all-reduce on dim 1 (f2), residual Y1 = X + .  (Builder::stage: one
+  // signalled GEMM over all T rows when chunked and communicating, §6)
+  if (!b.stage(1, a.ctx, h1, a.wo, hc, true, hc, a.bo, a.y1, EPI_RESID,
+               [&](EpiParams& ep, int64_t, int64_t) {
+                 ep.aux = a.x;
+                 ep.ldaux = hc;
+               },
+               [&](int, int64_t r0, int64_t n) {
+                 return EwList{E::ewd(EW_ADD, mptr(a.y1, r0 * hc), cptr(a.x, r0 * hc), n, hc)};
+               },
+               [] { return true; }))
+    return fail();
   layernorm(a.y1, a.g2, a.be2, L.st2, a.sv2, a.bn);
-  for (int k = 0; k < chunks; ++k) {  // FC1 column-first, all-reduce on dim 2 (f3), GeLU
-    if (!gemm_k(k, R(a.bn, k, hc), hc, a.w1, F1, true, F1, hc, R(a.u, k, F1), b1_here, c2 ? EPI_BIAS_GELU : EPI_BF16,
-                nullptr, R(a.h, k, F1)))
-      return fail();
-    if (!c2) coll_k(k, 2, 0, R(a.u, k, F1), nullptr, Mc * F1, 0, {E::ewd(EW_GELU, R(a.h, k, F1), R(a.u, k, F1), Mc, F1)});
-  }
-  for (int k = 0; k < chunks; ++k) {  // FC2 row-first, all-reduce on dim 1 (f4), residual
-    if (!gemm_k(k, R(a.h, k, F1), F1, a.w2, hc, true, hc, F1, R(a.z, k, hc), b2_here, c1 ? EPI_RESID : EPI_BF16,
-                R(a.y1, k, hc), nullptr))
-      return fail();
-    if (!c1) coll_k(k, 1, 0, R(a.z, k, hc), nullptr, Mc * hc, 0, {E::ewd(EW_ADD, R(a.z, k, hc), R(a.y1, k, hc), Mc, hc)});
-  }
+  // FC1 column-first, all-reduce on dim 2 (f3), GeLU
+  if (!b.stage(2, a.bn, hc, a.w1, F1, true, F1, a.b1, a.u, EPI_BIAS_GELU,
+               [&](EpiParams& ep, int64_t, int64_t) {
+                 ep.C2 = a.h;
+                 ep.ldc2 = F1;
+               },
+               [&](int, int64_t r0, int64_t n) {
+                 return EwList{E::ewd(EW_GELU, mptr(a.h, r0 * F1), cptr(a.u, r0 * F1), n, F1)};
+               },
+               [] { return true; }))
+    return fail();
+  // FC2 row-first, all-reduce on dim 1 (f4), residual Z = Y1 + .
+  if (!b.stage(1, a.h, F1, a.w2, hc, true, hc, a.b2, a.z, EPI_RESID,
+               [&](EpiParams& ep, int64_t, int64_t) {
+                 ep.aux = a.y1;
+                 ep.ldaux = hc;
+               },
+               [&](int, int64_t r0, int64_t n) {
+                 return EwList{E::ewd(EW_ADD, mptr(a.z, r0 * hc), cptr(a.y1, r0 * hc), n, hc)};
+               },
+               [] { return true; }))
+    return fail();
 
   // ================= backward
   void* dh = W(L.dh);
-  for (int k = 0; k < chunks; ++k) {  // FC2-dX, all-reduce on dim 2; dGeLU
-    if (!gemm_k(k, R(a.dz, k, hc), hc, a.w2, hc, false, F1, hc, R(dh, k, F1), nullptr, c2 ? EPI_DGELU : EPI_BF16,
-                R(a.u, k, F1), nullptr))
-      return fail();
-    if (!c2) coll_k(k, 2, 0, R(dh, k, F1), nullptr, Mc * F1, 0, {E::ewd(EW_DGELU, R(dh, k, F1), R(a.u, k, F1), Mc, F1)});
-  }
-  if (!b.dw(a.h, F1, a.dz, hc, a.dw2, a.db2)) return fail();
+  b.next_independent = true;  // FC2-dX reads dZ and the saved U only
+  // FC2-dX, all-reduce on dim 2, dGeLU; || dW2, db2
+  if (!b.stage(2, a.dz, hc, a.w2, hc, false, F1, nullptr, dh, EPI_DGELU,
+               [&](EpiParams& ep, int64_t, int64_t) {
+                 ep.aux = a.u;
+                 ep.ldaux = F1;
+               },
+               [&](int, int64_t r0, int64_t n) {
+                 return EwList{E::ewd(EW_DGELU, mptr(dh, r0 * F1), cptr(a.u, r0 * F1), n, F1)};
+               },
+               [&]() { return b.dw(a.h, F1, a.dz, hc, a.dw2, a.db2); }))
+    return fail();
   void* dbn = W(L.dbn);
-  for (int k = 0; k < chunks; ++k) {  // FC1-dX, all-reduce on dim 1
-    if (!gemm_k(k, R(dh, k, F1), F1, a.w1, F1, false, hc, F1, R(dbn, k, hc), nullptr, EPI_BF16, nullptr, nullptr))
-      return fail();
-    if (!c1) coll_k(k, 1, 0, R(dbn, k, hc), nullptr, Mc * hc, 0, {});
-  }
-  if (!b.dw(a.bn, hc, dh, F1, a.dw1, a.db1)) return fail();
+  // FC1-dX, all-reduce on dim 1 (LayerNorm-2 backward follows); || dW1, db1
+  if (!b.stage(1, dh, F1, a.w1, F1, false, hc, nullptr, dbn, EPI_BF16, [](EpiParams&, int64_t, int64_t) {},
+               [](int, int64_t, int64_t) { return EwList{}; },
+               [&]() { return b.dw(a.bn, hc, dh, F1, a.dw1, a.db1); }))
+    return fail();
   void* dy1 = W(L.dy1);
   ln_backward(dbn, a.y1, a.g2, a.sv2, L.bs2, a.dz, dy1);  // dY1 = dZ + LN2'(dB)
   for (int k = 0; k < chunks; ++k) b.prologue(k);        // dY1 complete before dWo / LN2 params
@@ -823,12 +842,11 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
     }
   }
   void* da = W(L.da);
-  for (int k = 0; k < chunks; ++k) {  // QKV-dX, all-reduce on dim 1
-    if (!gemm_k(k, R(dqkv, k, q1), q1, a.wqkv, q1, false, hc, q1, R(da, k, hc), nullptr, EPI_BF16, nullptr, nullptr))
-      return fail();
-    if (!c1) coll_k(k, 1, 0, R(da, k, hc), nullptr, Mc * hc, 0, {});
-  }
-  if (!b.dw(a.a, hc, dqkv, q1, a.dwqkv, a.dbqkv)) return fail();
+  // QKV-dX, all-reduce on dim 1 (LayerNorm-1 backward follows); || dWqkv, dbqkv
+  if (!b.stage(1, dqkv, q1, a.wqkv, q1, false, hc, nullptr, da, EPI_BF16, [](EpiParams&, int64_t, int64_t) {},
+               [](int, int64_t, int64_t) { return EwList{}; },
+               [&]() { return b.dw(a.a, hc, dqkv, q1, a.dwqkv, a.dbqkv); }))
+    return fail();
   ln_backward(da, a.x, a.g1, a.sv1, L.bs1, dy1, a.dx);  // dX = dY1 + LN1'(dA)
   for (int k = 0; k < chunks; ++k) b.prologue(k);
   ln_params(da, a.x, a.sv1, a.dg1, a.dbe1);

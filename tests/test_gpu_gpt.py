@@ -123,3 +123,29 @@ def test_gpt_layer_shape_errors():
         torch.cuda.synchronize()
     finally:
         mesh.destroy()
+
+
+@pytest.mark.parametrize("gated", [False, True])
+def test_gpt_layer_signalled_stages_with_cap(gated):
+    """Chunked all-reduce stages of the full layer run as signalled stages (one GEMM per stage);
+    with a GEMM CTA cap and gating on, the stages after LayerNorm must not gate on stale chunk gates."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, seq, d1, d2, chunks = 1024, 1024, 2048, 8, 256, 2, 2, 4
+    g, fw, bw = _oracle(T, h, F, heads, seq, 17)
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        mesh.set_gemm_ctas(32)
+        mesh.set_gating(gated)
+        bufs = [atp.alloc_gpt_rank(d1, d2, r, T, h, F, heads, "cuda", 17) for r in range(d1 * d2)]
+        call = atp.GptCall(mesh, bufs, T, h, F, heads, seq, chunks, True)
+        for _ in range(2):
+            call()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    for r, b in enumerate(bufs):
+        for name in ("z", "dx", "dwqkv", "dw1", "dg2"):
+            exp = _expected(name, fw, bw, d1, d2, r, h, F)
+            assert rel(b[name].float().cpu().numpy().reshape(exp.shape), exp) < TOL, (name, r)
