@@ -69,6 +69,9 @@ def parse():
     p.add_argument("--busbw", type=float, default=725.0,
                    help="all-reduce bus GB/s for the chunk planner (8-rank NCCL on this pool, B200_PROFILING.md)")
     p.add_argument("--gemm-ctas", type=int, default=-1, help="GEMM CTA cap (default: all SMs at N=1, SMs-16 else)")
+    p.add_argument("--share-gpu", action="store_true",
+                   help="TEST ONLY: N>1 ranks share cuda:0 (distinct NCCL_HOSTID per rank, NCCL over sockets); "
+                        "exercises the multi-process data path on a 1-GPU box, timings meaningless")
     p.add_argument("--seed", type=int, default=2301)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -322,10 +325,14 @@ def main() -> None:
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    if a.share_gpu:
+        os.environ["NCCL_HOSTID"] = f"atp-shared-gpu-rank{rank}"  # NCCL rejects two ranks on one device of one host
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _quiet(lambda: dist.init_process_group("nccl", device_id=dev))  # eager NCCL init prints its banner
 
     h, heads = a.hidden, a.heads
     F = a.ffn or 4 * h
@@ -577,6 +584,8 @@ def main() -> None:
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
                        "allreduce": "fused peer-memory kernel" if (a.fused_ar and world > 1) else "nccl",
                        "gated": bool(a.gated and world > 1), "mesh_source": mesh_source,
+                       **({"shared_gpu": "TEST ONLY: all ranks on cuda:0, NCCL over sockets; timings meaningless"}
+                          if a.share_gpu else {}),
                        "l2": "working set > 126 MB L2 (weights+activations ~1-2 GB), no flush"},
             "tflops_per_gpu": per_gpu, "exposed_comm_ms": exposed, "ms_per_step_comm_disabled": ms_nocomm,
             "flops_per_step": fl, "clocks": clocks, "gpu_launches": launches,
