@@ -158,6 +158,18 @@ atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled);
 atp_status atp_debug_counters(atp_mesh* mesh, int rank, uint32_t* out, int n);
 atp_status atp_profile_begin(atp_mesh* mesh);
 atp_status atp_profile_end(atp_mesh* mesh, atp_profile* out);
+/* Per-op timeline of the profiled region (call before atp_profile_end, which
+ * resets it): for each bracketed launch in enqueue order, its class (as
+ * above), stream (0 compute, 1 communication, 2 auxiliary), op kind (GEMM,
+ * elementwise, collective, fused all-reduce), sub-kind (GEMM epilogue /
+ * elementwise kind / collective kind) and start / end in device milliseconds
+ * from the first record's start.  Writes min(cap, records) entries to out and
+ * the record count to *n.  Synchronises on the events. */
+typedef struct {
+  int cls, stream, kind, sub;
+  double t0_ms, t1_ms;
+} atp_trace_rec;
+atp_status atp_profile_trace(atp_mesh* mesh, atp_trace_rec* out, int cap, int* n);
 atp_status atp_launch_count(uint64_t* out);
 
 /* ------------------------------------------------------------------ local GEMM

@@ -100,6 +100,11 @@ class Profile(C.Structure):
     _fields_ = [("launches", i64 * 4), ("ms", C.c_double * 4), ("flops", C.c_double * 4), ("bytes", C.c_double * 4)]
 
 
+class TraceRec(C.Structure):
+    _fields_ = [("cls", C.c_int), ("stream", C.c_int), ("kind", C.c_int), ("sub", C.c_int), ("t0_ms", C.c_double),
+                ("t1_ms", C.c_double)]
+
+
 class Call(C.Structure):
     _fields_ = [("phase", C.c_int), ("block", C.c_int), ("dim", C.c_int), ("p", C.c_int), ("elems", i64)]
 
@@ -123,6 +128,7 @@ SIGNATURES = {
     "atp_debug_counters": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint32), C.c_int]),
     "atp_profile_begin": (C.c_int, [vp]),
     "atp_profile_end": (C.c_int, [vp, C.POINTER(Profile)]),
+    "atp_profile_trace": (C.c_int, [vp, C.POINTER(TraceRec), C.c_int, C.POINTER(C.c_int)]),
     "atp_launch_count": (C.c_int, [C.POINTER(C.c_uint64)]),
     "atp_attn_core_fwd": (C.c_int, [vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64, vp, vp]),
     "atp_attn_core_bwd": (C.c_int, [vp, i64, vp, i64, vp, vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64,

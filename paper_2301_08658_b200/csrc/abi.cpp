@@ -199,6 +199,23 @@ atp_status atp_profile_end(atp_mesh* mesh, atp_profile* out) {
   return ATP_OK;
 }
 
+atp_status atp_profile_trace(atp_mesh* mesh, atp_trace_rec* out, int cap, int* n) {
+  if (mesh == nullptr || n == nullptr || (cap > 0 && out == nullptr))
+    return fail(ATP_ERR_INVALID, "atp_profile_trace: NULL argument");
+  cudaSetDevice(mesh->device);
+  *n = static_cast<int>(mesh->prof_used);
+  for (size_t i = 0; i < mesh->prof_used && static_cast<int>(i) < cap; ++i) {
+    const atp::ProfRec& r = mesh->prof[i];
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("atp_profile_trace: ") + cudaGetErrorString(e));
+    float t0 = 0.f, t1 = 0.f;
+    cudaEventElapsedTime(&t0, mesh->prof[0].a, r.a);
+    cudaEventElapsedTime(&t1, mesh->prof[0].a, r.b);
+    out[i] = atp_trace_rec{r.cls, r.stream, r.kind, r.sub, t0, t1};
+  }
+  return ATP_OK;
+}
+
 atp_status atp_launch_count(uint64_t* out) {
   if (out == nullptr) return fail(ATP_ERR_INVALID, "atp_launch_count: NULL");
   *out = atp::launch_count();

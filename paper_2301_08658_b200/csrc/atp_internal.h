@@ -30,6 +30,8 @@ struct EpiParams {
 struct GemmDesc {
   alignas(64) CUtensorMap tmA;
   alignas(64) CUtensorMap tmB;
+  alignas(64) CUtensorMap tmC;   // epilogue TMA-store map of ep.C
+  alignas(64) CUtensorMap tmC2;  // ... of ep.C2 (EPI_BIAS_GELU), else a copy of tmC
   int M = 0, N = 0, K = 0;
   bool a_mn = false, b_mn = false;
   int bn = 0;        // 128 or 256 (0 = choose)

@@ -78,9 +78,13 @@ struct SmemLayout {
   static constexpr uint32_t kABytes = BM * BK * 2;             // this CTA's 128 rows of A
   static constexpr uint32_t kBBytes = (BN / CG) * BK * 2;      // this CTA's share of B
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
+  // epilogue staging: per epilogue warp two 2 KB buffers (double-buffered TMA stores)
+  static constexpr uint32_t kStgOffset = STAGES * kStageBytes;
+  static constexpr uint32_t kStgBytesPerWarp = 4096;
+  static constexpr uint32_t kBarOffset = kStgOffset + kEpiWarps * kStgBytesPerWarp;
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem slot
   static constexpr uint32_t kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static_assert(kBytes <= 232448, "shared memory budget");
 };
 
 // Tile order: chunk by chunk (mt_chunk M-tiles per chunk; = all M-tiles when
@@ -106,7 +110,27 @@ __device__ __forceinline__ void tile_coords(int tile, int mt_chunk, int num_n, i
 // of 320 threads without spilling; the light epilogues use 32-column slices.
 template <int EPI>
 __host__ __device__ constexpr int slice_width() {
-  return (EPI == EPI_BIAS_GELU || EPI == EPI_DGELU || EPI == EPI_RESID) ? 16 : 32;
+  return EPI == EPI_BF16 ? 32 : 16;
+}
+// Bytes of one output row of a slice (the TMA store box's inner extent): 64 B
+// (SWIZZLE_64B) for bf16 x 32 and fp32 x 16, 32 B (SWIZZLE_32B) for bf16 x 16.
+template <int EPI>
+__host__ __device__ constexpr int slice_row_bytes() {
+  return slice_width<EPI>() * (EPI == EPI_F32 ? 4 : 2);
+}
+// Swizzled byte offset of 16-byte chunk c of row r (0..31) in a [32 rows][RB bytes]
+// staging box: CUTLASS Swizzle<1|2, 4, 3> (the TMA SWIZZLE_32B / _64B patterns),
+// which spreads a warp's 32 row-writes over all banks (4 wavefronts per 512 B).
+template <int RB>
+__device__ __forceinline__ uint32_t stage_off(int r, int c) {
+  if constexpr (RB == 64) {
+    return static_cast<uint32_t>(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+  } else {
+    return static_cast<uint32_t>(r * 32 + ((c ^ ((r >> 2) & 1)) << 4));
+  }
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 template <int EPI>
 __host__ __device__ constexpr bool uses_bias() {
@@ -146,30 +170,30 @@ __device__ __forceinline__ float bf16_at(const uint4 (&v)[NV], int j) {
   return __bfloat162float(p[j % 8]);
 }
 
-// One W-column slice of one accumulator row: fused epilogue + 16-byte stores.
+// One W-column slice of one accumulator row (row r = lane of this warp's
+// 32-row box): fused epilogue, result written to this warp's shared staging
+// box(es) in the swizzled layout the TMA store reads.  Lanes whose row is past
+// M still write (the store clips rows >= M and columns >= N).
 template <int EPI, int W>
-__device__ __forceinline__ void epilogue_chunk(float (&f)[W], const Side<W>& sd, int row, int col0, int M, int N,
-                                               const EpiParams& ep) {
-  if (row >= M || col0 >= N) return;
+__device__ __forceinline__ void epilogue_chunk(float (&f)[W], const Side<W>& sd, int r, const EpiParams& ep,
+                                               uint32_t stg) {
+  constexpr int RB = slice_row_bytes<EPI>();
   if (uses_bias<EPI>() && ep.bias != nullptr) {
 #pragma unroll
     for (int j = 0; j < W; ++j) f[j] += bf16_at(sd.bias, j);
   }
-  const bool full = (col0 + W <= N);
   if constexpr (EPI == EPI_F32) {
-    float* dst = static_cast<float*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
 #pragma unroll
     for (int g = 0; g < W / 4; ++g)
-      if (full || col0 + 4 * g + 4 <= N)
-        reinterpret_cast<float4*>(dst)[g] = make_float4(f[4 * g], f[4 * g + 1], f[4 * g + 2], f[4 * g + 3]);
+      st_shared_v4(stg + stage_off<RB>(r, g), __float_as_uint(f[4 * g]), __float_as_uint(f[4 * g + 1]),
+                   __float_as_uint(f[4 * g + 2]), __float_as_uint(f[4 * g + 3]));
   } else {
     if constexpr (EPI == EPI_RESID) {
 #pragma unroll
       for (int j = 0; j < W; ++j) f[j] += bf16_at(sd.aux, j);
     }
     if constexpr (EPI == EPI_BIAS_GELU) {
-      // U = acc + bias (stored, rounded once); H = GeLU(U) from the rounded U
-      __nv_bfloat16* dh = static_cast<__nv_bfloat16*>(ep.C2) + static_cast<int64_t>(row) * ep.ldc2 + col0;
+      // U = acc + bias (stored, rounded once); H = GeLU(U) from the rounded U -> second box
       uint32_t hp[W / 2];
 #pragma unroll
       for (int j = 0; j < W / 2; ++j) {
@@ -179,8 +203,7 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[W], const Side<W>& sd,
       }
 #pragma unroll
       for (int g = 0; g < W / 8; ++g)
-        if (full || col0 + 8 * g + 8 <= N)
-          reinterpret_cast<uint4*>(dh)[g] = make_uint4(hp[4 * g], hp[4 * g + 1], hp[4 * g + 2], hp[4 * g + 3]);
+        st_shared_v4(stg + 32 * RB + stage_off<RB>(r, g), hp[4 * g], hp[4 * g + 1], hp[4 * g + 2], hp[4 * g + 3]);
     }
     if constexpr (EPI == EPI_DGELU) {
       // dU = dH * GeLU'(U); dH is the bf16-rounded product (as after an all-reduce)
@@ -190,14 +213,12 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[W], const Side<W>& sd,
         f[j] = dh * gelu_grad_f(bf16_at(sd.aux, j));
       }
     }
-    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.C) + static_cast<int64_t>(row) * ep.ldc + col0;
     uint32_t p[W / 2];
 #pragma unroll
     for (int j = 0; j < W / 2; ++j) p[j] = pack_bf16(f[2 * j], f[2 * j + 1]);
 #pragma unroll
     for (int g = 0; g < W / 8; ++g)
-      if (full || col0 + 8 * g + 8 <= N)
-        reinterpret_cast<uint4*>(dst)[g] = make_uint4(p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
+      st_shared_v4(stg + stage_off<RB>(r, g), p[4 * g], p[4 * g + 1], p[4 * g + 2], p[4 * g + 3]);
   }
 }
 
@@ -210,6 +231,7 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[W], const Side<W>& sd,
 template <int CG, int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                       int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows, const uint32_t* gate,
                       uint32_t gate_target, int group_m) {
   using L = SmemLayout<CG, BN, STAGES>;
@@ -242,6 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmC);
+    if (EPI == EPI_BIAS_GELU) ptx::prefetch_tmap(&tmC2);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), 1);
       ptx::mbar_init(empty_bar(s), 1);
@@ -370,8 +394,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------ epilogue warps 2..9 (both CTAs)
+    // TMEM -> registers -> fused epilogue -> this warp's swizzled smem box
+    // [32 rows][W cols] -> one TMA bulk store per slice (double-buffered): 4
+    // shared-memory wavefronts per 512 B instead of 32 scattered global-store
+    // wavefronts per warp instruction, and full-line writes into L2.  (Measured
+    // time-neutral against direct 16-byte stores: these GEMMs are power-bound,
+    // profiles/r01_epi_ab.md.)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int half = (warp - 2) / 4;  // which half of the BN columns this warp drains
+    constexpr int W = slice_width<EPI>();
+    const uint32_t stg0 = base + L::kStgOffset + static_cast<uint32_t>(warp - 2) * L::kStgBytesPerWarp;
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = unit; tile < num_tiles; tile += n_units) {
@@ -383,10 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const int row = m0 + 32 * q + static_cast<int>(lane);
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
-      constexpr int W = slice_width<EPI>();
       const int c_begin = half * (BN / 2 / W), c_end = (half + 1) * (BN / 2 / W);
       // software pipeline: the TMEM slice and side inputs of slice c+1 are in
-      // flight while slice c is converted and stored
+      // flight while slice c is converted and staged
       uint32_t v[W];
       Side<W> sd;
       ptx::tmem_ld_slice<W>(tbase + W * c_begin, v);
@@ -402,7 +434,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld_slice<W>(tbase + W * (c + 1), v);
           load_side<EPI, W>(sd, row, n0 + W * (c + 1), M, N, ep);
         }
-        epilogue_chunk<EPI, W>(f, cur, row, n0 + W * c, M, N, ep);
+        const int col0 = n0 + W * c;
+        if (col0 >= N || m0 + 32 * q >= M) continue;  // warp-uniform: box entirely outside C
+        const uint32_t stg = stg0 + static_cast<uint32_t>(sbuf) * 2048u;
+        if (lane == 0) ptx::bulk_wait_read1();  // the store that last read this buffer is done reading
+        __syncwarp();
+        epilogue_chunk<EPI, W>(f, cur, static_cast<int>(lane), ep, stg);
+        ptx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&tmC, stg, col0, m0 + 32 * q);
+          if constexpr (EPI == EPI_BIAS_GELU)
+            ptx::tma_store_2d(&tmC2, stg + 32 * slice_row_bytes<EPI>(), col0, m0 + 32 * q);
+          ptx::bulk_commit();
+        }
+        sbuf ^= 1;
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -414,8 +460,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (sig != nullptr) {
-        // all epilogue warps of this CTA have issued their stores of this tile;
-        // make them visible (system scope: NCCL peers read them) and count the tile.
+        // every epilogue warp's bulk stores of this tile complete and visible
+        // (system scope: NCCL / peer ranks read them), then count the tile.
+        if (lane == 0) {
+          ptx::bulk_wait0();
+          __threadfence_system();
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
         if (warp == 2 && lane == 0) {
           __threadfence_system();
@@ -427,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) ptx::bulk_wait0();  // staging smem stays valid until the last stores completed
   }
 
   ptx::tc_fence_before();
@@ -497,8 +548,8 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate, d.gate_target,
-                            d.group_m > 0 ? d.group_m : 16);
+  return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.tmC, d.tmC2, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate,
+                            d.gate_target, d.group_m > 0 ? d.group_m : 16);
 }
 
 template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>
@@ -549,6 +600,21 @@ int raster_group_m(int rows_per_mtile, int K) {
   const double panel = static_cast<double>(rows_per_mtile) * K * 2.0;
   int g = static_cast<int>(40e6 / panel);
   return g < 1 ? 1 : (g > 16 ? 16 : g);
+}
+
+// Output map of the epilogue's TMA stores: [rows, cols] (pitch ld elements of
+// esz bytes), box [32 rows][box_cols], swizzle = the box row's bytes (32 / 64).
+bool make_tmap_out(CUtensorMap* m, const void* ptr, int esz, int64_t rows, int64_t cols, int64_t ld, int box_cols) {
+  if (!get_encode()) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), 32u};
+  cuuint32_t estr[2] = {1, 1};
+  const int rb = box_cols * esz;
+  return g_encode(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool tmap_bf16_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
@@ -617,6 +683,19 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
   else
     ok = make_tmap(&d.tmB, B, K, N, ldb, BK, 64);
   if (!ok) return "gemm: cuTensorMapEncodeTiled failed for B";
+  // epilogue output maps (the EpiParams must be final here)
+  const int epi = d.epi;
+  const int esz = epi == EPI_F32 ? 4 : 2;
+  const int w = epi == EPI_BF16 ? 32 : 16;  // slice_width<EPI>()
+  if (d.ep.C == nullptr || (reinterpret_cast<uintptr_t>(d.ep.C) & 15) || (d.ep.ldc * esz) % 16)
+    return "gemm: output must be 16-byte aligned with a 16-byte multiple row pitch";
+  if (!make_tmap_out(&d.tmC, d.ep.C, esz, M, N, d.ep.ldc, w)) return "gemm: cuTensorMapEncodeTiled failed for C";
+  d.tmC2 = d.tmC;
+  if (epi == EPI_BIAS_GELU) {
+    if (d.ep.C2 == nullptr || (reinterpret_cast<uintptr_t>(d.ep.C2) & 15) || (d.ep.ldc2 * 2) % 16)
+      return "gemm: GeLU output must be 16-byte aligned with a 16-byte multiple row pitch";
+    if (!make_tmap_out(&d.tmC2, d.ep.C2, 2, M, N, d.ep.ldc2, w)) return "gemm: cuTensorMapEncodeTiled failed for C2";
+  }
   return nullptr;
 }
 

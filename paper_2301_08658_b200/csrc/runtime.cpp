@@ -163,6 +163,9 @@ static ProfRec* prof_begin(atp_mesh* m, const Op& op, cudaStream_t st) {
   ProfRec* r = &m->prof[m->prof_used++];
   const int p = op.kind == OP_AR ? (op.ar_dim == 1 ? m->d1 : m->d2) : 1;
   op_cost(op, p, &r->cls, &r->flops, &r->bytes);
+  r->stream = op.stream;
+  r->kind = op.kind;
+  r->sub = op.kind == OP_GEMM ? op.g.epi : (op.kind == OP_EW ? op.e.kind : op.coll);
   cudaEventRecord(r->a, st);
   return r;
 }

@@ -94,6 +94,9 @@ namespace atp {
 struct ProfRec {
   cudaEvent_t a = nullptr, b = nullptr;
   int cls = 0;
+  int stream = 0;  // 0 compute, 1 communication, 2 auxiliary
+  int kind = 0;    // OpKind
+  int sub = 0;     // GEMM epilogue kind / elementwise kind / collective kind
   double flops = 0, bytes = 0;
 };
 }  // namespace atp
