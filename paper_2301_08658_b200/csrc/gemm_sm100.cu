@@ -49,12 +49,26 @@ struct ErfExp {
   float erf_abs;  // erf(|x|/sqrt 2)
   float e;        // exp(-x^2/2)
 };
+// MUFU reciprocal / exp2 (one instruction each, ~1 ulp): the epilogue runs on
+// the SM sub-partitions that also issue the MMAs and TMA loads, so its
+// instruction count shows up in tensor-pipe utilisation (GeLU GEMMs 88% vs
+// 97% for light epilogues, profiles/r01_ncu_gemm_full_v4.md).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ ErfExp erf_as(float x) {
   const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.0f));
+  const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
   const float poly =
       t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
-  const float e = exp2f(-0.72134752044448170f * x * x);  // exp(-x^2/2) = 2^(-x^2 / (2 ln 2))
+  const float e = ex2_approx(-0.72134752044448170f * x * x);  // exp(-x^2/2) = 2^(-x^2 / (2 ln 2))
   return {1.0f - poly * e, e};
 }
 __device__ __forceinline__ float gelu_f(float x) {
