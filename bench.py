@@ -72,6 +72,8 @@ def parse():
     p.add_argument("--share-gpu", action="store_true",
                    help="TEST ONLY: N>1 ranks share cuda:0 (distinct NCCL_HOSTID per rank, NCCL over sockets); "
                         "exercises the multi-process data path on a 1-GPU box, timings meaningless")
+    p.add_argument("--no-graph", action="store_true",
+                   help="time direct calls instead of the step captured as one CUDA graph (atp_graph_*)")
     p.add_argument("--seed", type=int, default=2301)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -398,7 +400,8 @@ def main() -> None:
 
         def make_call(bb, c):
             return atp.LayerCall(mesh, [bb], T, h, F, heads, c, True)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # a capturable (non-legacy) stream for every launch of the bench
+    torch.cuda.set_stream(stream)
 
     def barrier():
         if world > 1:
@@ -448,6 +451,30 @@ def main() -> None:
         call(stream)
     torch.cuda.synchronize()
 
+    # ---- the step as one CUDA graph (atp_graph_*): host cost per step = one
+    # cudaGraphLaunch; direct calls stay in use for the comm-disabled twin and
+    # the profiled pass (per-launch events cannot be captured)
+    graphs, capture_errors = [], []
+
+    def as_graph(c):
+        if a.no_graph:
+            return c
+        try:
+            g = atp.Graph.capture(mesh, c, stream)
+        except Exception as e:  # noqa: BLE001  (fused peer-memory meshes refuse capture)
+            capture_errors.append(str(e))
+            return c
+        graphs.append(g)
+        return g
+
+    run = as_graph(call)
+    graph_note = ("direct calls (--no-graph)" if a.no_graph else
+                  f"direct calls (graph capture unavailable: {capture_errors[0]})" if capture_errors else
+                  "step captured once as a CUDA graph, one cudaGraphLaunch per step")
+    for _ in range(2):
+        run(stream)
+    torch.cuda.synchronize()
+
     # ---- timed region (clocks sampled during it)
     sampler = ClockSampler(local_rank)
     import ctypes as C
@@ -455,7 +482,7 @@ def main() -> None:
     n0 = C.c_uint64()
     _abi.check(_abi.lib().atp_launch_count(C.byref(n0)))
     t0 = time.time()
-    ms = timed(a.steps)
+    ms = timed(a.steps, run)
     t1 = time.time()
     n1 = C.c_uint64()
     _abi.check(_abi.lib().atp_launch_count(C.byref(n1)))
@@ -471,7 +498,7 @@ def main() -> None:
     ms_nocomm = ms
     if d1 > 1 or d2 > 1:
         _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 0))
-        ms_nocomm = timed(max(10, a.steps // 2))
+        ms_nocomm = timed(max(10, a.steps // 2), call)
         _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 1))
         exposed = max(0.0, ms - ms_nocomm)
 
@@ -479,7 +506,7 @@ def main() -> None:
     prof = _abi.Profile()
     n_prof = max(5, min(a.steps, 30))
     _abi.check(_abi.lib().atp_profile_begin(mesh.handle))
-    ms_prof = timed(n_prof)
+    ms_prof = timed(n_prof, call)
     _abi.check(_abi.lib().atp_profile_end(mesh.handle, C.byref(prof)))
     pk = peaks(a.peaks)
     gemm_ms = prof.ms[0] / n_prof
@@ -519,7 +546,8 @@ def main() -> None:
         h2d = hx.numel() * hx.element_size() + hdz.numel() * hdz.element_size()
         d2h = sum(r.numel() * r.element_size() for r in res)
         bufs_b = dict(bufs, x=torch.empty_like(bufs["x"]), dz=torch.empty_like(bufs["dz"]))
-        sets = [(bufs, call), (bufs_b, make_call(bufs_b, chunks))]
+        sets = [(bufs, run), (bufs_b, as_graph(make_call(bufs_b, chunks)) if run is not call else
+                                  make_call(bufs_b, chunks))]
         copy_stream = torch.cuda.Stream()
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -569,6 +597,8 @@ def main() -> None:
         cpu = (cpu_baseline_gpt(h, F, heads, a.seq, a.seed) if gpt_mode
                else cpu_baseline(h, F, heads, a.seed, a.cpu_seconds))
 
+    for g in graphs:
+        g.destroy()
     mesh.destroy()
     if rank == 0:
         out = {
@@ -583,7 +613,7 @@ def main() -> None:
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
                        "allreduce": "fused peer-memory kernel" if (a.fused_ar and world > 1) else "nccl",
-                       "gated": bool(a.gated and world > 1), "mesh_source": mesh_source,
+                       "gated": bool(a.gated and world > 1), "mesh_source": mesh_source, "launch": graph_note,
                        **({"shared_gpu": "TEST ONLY: all ranks on cuda:0, NCCL over sockets; timings meaningless"}
                           if a.share_gpu else {}),
                        "l2": "working set > 126 MB L2 (weights+activations ~1-2 GB), no flush"},

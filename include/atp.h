@@ -172,6 +172,29 @@ typedef struct {
 atp_status atp_profile_trace(atp_mesh* mesh, atp_trace_rec* out, int cap, int* n);
 atp_status atp_launch_count(uint64_t* out);
 
+/* ------------------------------------------------------------------ CUDA graphs
+ * Capture a sequence of calls on one mesh (e.g. one atp_layer_fwd_bwd, or a
+ * stack of layers) into a CUDA graph and replay it: one cudaGraphLaunch per
+ * step instead of the host building and enqueuing every GEMM, elementwise
+ * step, stream wait and collective (NCCL calls are captured as graph nodes).
+ *   atp_graph_begin(mesh, stream): starts stream capture (thread-local mode) on
+ *     `stream`; the calls that follow enqueue into the capture.  Make one
+ *     uncaptured call with the same arguments first (first-use setup).
+ *   atp_graph_end(mesh, stream, &g): ends the capture, instantiates the graph.
+ *   atp_graph_launch(g, stream): replays it (asynchronous, stream order).  The
+ *     captured calls read and write the same device buffers on every replay.
+ *   atp_graph_destroy(g).
+ * Every call starts from zeroed chunk counters (no state carried between
+ * calls), so replays are independent.  Not available while profiling, or on a
+ * mesh with the fused peer-memory all-reduce (its counters are shared with
+ * peers): ATP_ERR_UNSUPPORTED.  Errors: ATP_ERR_INVALID, ATP_ERR_CUDA (capture
+ * or instantiation failed; the capture is ended and discarded). */
+typedef struct atp_graph atp_graph;
+atp_status atp_graph_begin(atp_mesh* mesh, void* stream);
+atp_status atp_graph_end(atp_mesh* mesh, void* stream, atp_graph** out);
+atp_status atp_graph_launch(atp_graph* graph, void* stream);
+atp_status atp_graph_destroy(atp_graph* graph);
+
 /* ------------------------------------------------------------------ local GEMM
  * One local shard contraction on the tcgen05 tensor cores (the building block
  * of F3/F6/F8/F11 and of dX = dY W^T, dW = X^T dY):

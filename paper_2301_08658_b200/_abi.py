@@ -130,6 +130,10 @@ SIGNATURES = {
     "atp_profile_end": (C.c_int, [vp, C.POINTER(Profile)]),
     "atp_profile_trace": (C.c_int, [vp, C.POINTER(TraceRec), C.c_int, C.POINTER(C.c_int)]),
     "atp_launch_count": (C.c_int, [C.POINTER(C.c_uint64)]),
+    "atp_graph_begin": (C.c_int, [vp, vp]),
+    "atp_graph_end": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "atp_graph_launch": (C.c_int, [vp, vp]),
+    "atp_graph_destroy": (C.c_int, [vp]),
     "atp_attn_core_fwd": (C.c_int, [vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64, vp, vp]),
     "atp_attn_core_bwd": (C.c_int, [vp, i64, vp, i64, vp, vp, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, i64,
                                     vp, C.c_size_t, vp]),

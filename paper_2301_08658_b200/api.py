@@ -10,7 +10,7 @@ import ctypes as C
 from dataclasses import dataclass, field
 
 from . import _abi
-from ._abi import check, lib
+from ._abi import AtpError, check, lib
 from . import layout
 
 
@@ -248,6 +248,41 @@ def atp_mlp_fwd(mesh, bufs, T, h, F, chunks=1, stream=None):
 def atp_mlp_bwd(mesh, bufs, T, h, F, chunks=1, stream=None):
     a = _arr(_abi.MlpBwdArgs, [_mlp_bwd(b) for b in bufs])
     check(lib().atp_mlp_bwd(mesh.handle, a, T, h, F, chunks, _dt(bufs[0]["y1"]), _stream(stream)))
+
+
+class Graph:
+    """A CUDA graph of libatp calls on one mesh (atp_graph_begin/end/launch):
+    `Graph.capture(mesh, fn, stream)` runs `fn(stream)` once uncaptured
+    (first-use setup), then captures it; calling the Graph replays it."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    @classmethod
+    def capture(cls, mesh: "Mesh", fn, stream=None) -> "Graph":
+        import torch
+
+        st = stream if stream is not None else torch.cuda.current_stream()
+        if st.cuda_stream == 0:
+            raise AtpError("Graph.capture: needs a non-default stream (legacy stream 0 cannot be captured)")
+        fn(st)
+        st.synchronize()
+        check(lib().atp_graph_begin(mesh.handle, st.cuda_stream))
+        try:
+            fn(st)
+        finally:
+            h = C.c_void_p()
+            rc = lib().atp_graph_end(mesh.handle, st.cuda_stream, C.byref(h))
+        check(rc)
+        return cls(h.value)
+
+    def __call__(self, stream=None) -> None:
+        check(lib().atp_graph_launch(self.handle, _stream(stream)))
+
+    def destroy(self) -> None:
+        if self.handle:
+            lib().atp_graph_destroy(self.handle)
+            self.handle = None
 
 
 class LayerCall:

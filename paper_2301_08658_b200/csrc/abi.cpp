@@ -141,6 +141,7 @@ atp_status atp_mesh_groups(int d1, int d2, int dim, int* out) {
 
 atp_status atp_mesh_enable_fused_ar(atp_mesh* mesh, size_t part_bytes) {
   if (mesh == nullptr || part_bytes == 0) return fail(ATP_ERR_INVALID, "atp_mesh_enable_fused_ar: bad arguments");
+  if (mesh->capture_stream != nullptr) return fail(ATP_ERR_UNSUPPORTED, "atp_mesh_enable_fused_ar: mesh is capturing a graph");
   cudaSetDevice(mesh->device);
   return static_cast<atp_status>(atp::enable_fused_ar(mesh, part_bytes));
 }
@@ -174,6 +175,7 @@ atp_status atp_mesh_set_comm_enabled(atp_mesh* mesh, int enabled) {
 
 atp_status atp_profile_begin(atp_mesh* mesh) {
   if (mesh == nullptr) return fail(ATP_ERR_INVALID, "atp_profile_begin: NULL mesh");
+  if (mesh->capture_stream != nullptr) return fail(ATP_ERR_UNSUPPORTED, "atp_profile_begin: mesh is capturing a graph");
   mesh->profiling = true;
   mesh->prof_used = 0;
   return ATP_OK;
@@ -213,6 +215,71 @@ atp_status atp_profile_trace(atp_mesh* mesh, atp_trace_rec* out, int cap, int* n
     cudaEventElapsedTime(&t1, mesh->prof[0].a, r.b);
     out[i] = atp_trace_rec{r.cls, r.stream, r.kind, r.sub, t0, t1};
   }
+  return ATP_OK;
+}
+
+struct atp_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t launches = 0;  // libatp kernels per replay (for atp_launch_count)
+  int device = 0;
+};
+
+atp_status atp_graph_begin(atp_mesh* mesh, void* stream) {
+  if (mesh == nullptr || stream == nullptr) return fail(ATP_ERR_INVALID, "atp_graph_begin: NULL mesh or stream");
+  if (mesh->capture_stream != nullptr) return fail(ATP_ERR_INVALID, "atp_graph_begin: already capturing");
+  if (mesh->profiling) return fail(ATP_ERR_UNSUPPORTED, "atp_graph_begin: mesh is profiling");
+  for (const auto& r : mesh->rs)
+    if (r.sym_base != nullptr)
+      return fail(ATP_ERR_UNSUPPORTED, "atp_graph_begin: fused peer-memory all-reduce keeps cross-call state");
+  cudaSetDevice(mesh->device);
+  cudaError_t e = cudaStreamBeginCapture(static_cast<cudaStream_t>(stream), cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+  mesh->capture_stream = stream;
+  mesh->capture_launch0 = atp::launch_count();
+  return ATP_OK;
+}
+
+atp_status atp_graph_end(atp_mesh* mesh, void* stream, atp_graph** out) {
+  if (mesh == nullptr || out == nullptr || stream == nullptr || stream != mesh->capture_stream)
+    return fail(ATP_ERR_INVALID, "atp_graph_end: not capturing on this stream");
+  *out = nullptr;
+  mesh->capture_stream = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g);
+  if (e != cudaSuccess || g == nullptr) {
+    if (g) cudaGraphDestroy(g);
+    return fail(ATP_ERR_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+  }
+  cudaGraphExec_t x = nullptr;
+  e = cudaGraphInstantiate(&x, g, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return fail(ATP_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+  }
+  auto* h = new atp_graph;
+  h->graph = g;
+  h->exec = x;
+  h->launches = atp::launch_count() - mesh->capture_launch0;
+  h->device = mesh->device;
+  *out = h;
+  return ATP_OK;
+}
+
+atp_status atp_graph_launch(atp_graph* graph, void* stream) {
+  if (graph == nullptr) return fail(ATP_ERR_INVALID, "atp_graph_launch: NULL graph");
+  cudaError_t e = cudaGraphLaunch(graph->exec, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(ATP_ERR_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+  atp::count_launch(graph->launches);
+  return ATP_OK;
+}
+
+atp_status atp_graph_destroy(atp_graph* graph) {
+  if (graph == nullptr) return ATP_OK;
+  cudaSetDevice(graph->device);
+  if (graph->exec) cudaGraphExecDestroy(graph->exec);
+  if (graph->graph) cudaGraphDestroy(graph->graph);
+  delete graph;
   return ATP_OK;
 }
 

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -276,9 +277,25 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
     int rc = ensure_events(m->rs[r], sch[r].n_events);
     if (rc) return rc;
   }
-  cudaError_t e = cudaEventRecord(m->ev_start, stream);
+  cudaError_t e = cudaSuccess;
+  // Without peer-memory all-reduce, a rank's chunk counters and gates are read
+  // only by its own streams, so every call starts from zeroed counters (one
+  // memset, ordered after the previous call's join): each call is
+  // self-contained, which is what makes a captured CUDA graph replayable.
+  // Fused meshes keep cumulative counters (peers may still read them).
+  for (int r = 0; r < n; ++r) {
+    RankState& s = m->rs[r];
+    if (s.sym_base != nullptr) {
+      ++s.epoch;
+      continue;
+    }
+    if ((e = cudaMemsetAsync(s.sig_buf, 0, kSigSlots * sizeof(uint32_t), stream)) != cudaSuccess)
+      return cuda_fail(e, "counter reset");
+    std::fill(s.sig_total.begin(), s.sig_total.end(), 0u);
+    s.epoch = 1;
+  }
+  e = cudaEventRecord(m->ev_start, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-  for (int r = 0; r < n; ++r) ++m->rs[r].epoch;
   for (int r = 0; r < n; ++r) {
     cudaStreamWaitEvent(m->rs[r].comm, m->ev_start, 0);
     cudaStreamWaitEvent(m->rs[r].aux, m->ev_start, 0);

@@ -109,6 +109,8 @@ struct atp_mesh {
   bool signalled = true;    // signalled stages (ATP_SIGNALLED=0 disables, for A/B runs)
   bool gated = false;       // chunk-gated GEMMs (atp_mesh_set_gating; ATP_GATED=1 initial value)
   bool profiling = false;
+  void* capture_stream = nullptr;  // atp_graph_begin .. atp_graph_end: the stream being captured
+  uint64_t capture_launch0 = 0;    // libatp launch count when the capture began
   std::vector<atp::ProfRec> prof;  // event pool; the first prof_used are live
   size_t prof_used = 0;
   bool is_virtual = false;

@@ -23,7 +23,7 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
         sys.path.insert(0, p)
 
 
-def _layer(atp, mesh, d1, d2, rank, chunks, seed):
+def _layer(atp, mesh, d1, d2, rank, chunks, seed, graph=False):
     import numpy as np
     import torch
 
@@ -48,6 +48,19 @@ def _layer(atp, mesh, d1, d2, rank, chunks, seed):
         worst = max(worst, e)
     for k, v in snap.items():
         assert torch.equal(b[k], v), k
+    if graph:  # CUDA-graph capture of the step (NCCL collectives as graph nodes), replayed twice
+        st = torch.cuda.Stream()
+        g = atp.Graph.capture(mesh, call, st)
+        try:
+            for _ in range(2):
+                for k in snap:
+                    b[k].fill_(float("nan"))
+                g(st)
+                st.synchronize()
+                for k, v in snap.items():
+                    assert torch.equal(b[k], v), ("graph replay", k)
+        finally:
+            g.destroy()
     # replicas: digests of the tensors replicated over each dim must agree in the group
     return worst, {k: float(b[k].double().sum().item()) for k in ("qkv", "u", "db1", "y1", "z", "dx", "db2")}
 
@@ -104,7 +117,7 @@ def worker(rank: int, world: int, port: int, jobs: list, results) -> None:
                 if opts.get("fused"):
                     mesh.enable_fused_ar(opts["fused"])  # CUDA IPC peer buffers, opened across processes
                 if kind == "layer":
-                    worst, dig = _layer(atp, mesh, d1, d2, rank, chunks, 43)
+                    worst, dig = _layer(atp, mesh, d1, d2, rank, chunks, 43, bool(opts.get("graph")))
                 else:
                     worst, dig = _gpt(atp, mesh, d1, d2, rank, chunks, 47), {}
             finally:

@@ -68,6 +68,7 @@ def test_nccl_two_ranks():
     jobs = [("layer", 2, 1, 1, {}), ("layer", 2, 1, 2, {}), ("layer", 1, 2, 2, {}),
             ("layer", 1, 2, 4, {"gemm_ctas": 32, "gated": True}), ("layer", 2, 1, 4, {"fused": FUSED_BYTES}),
             ("layer", 1, 2, 2, {"fused": FUSED_BYTES, "gemm_ctas": 32, "gated": True}),
+            ("layer", 2, 1, 2, {"graph": True}), ("layer", 1, 2, 4, {"graph": True, "gemm_ctas": 32, "gated": True}),
             ("gpt", 1, 2, 2, {}), ("gpt", 2, 1, 1, {})]
     res = _spawn(2, jobs)
     for job in jobs:
@@ -93,7 +94,8 @@ def test_nccl_four_ranks():
 def test_nccl_eight_ranks():
     """The four 8-GPU meshes of cfgs 3-5 (1x8, 2x4, 4x2, 8x1) as 8 processes."""
     jobs = [("layer", 8, 1, 2, {}), ("layer", 4, 2, 4, {"gemm_ctas": 32, "gated": True}), ("layer", 2, 4, 2, {}),
-            ("layer", 1, 8, 1, {}), ("layer", 4, 2, 2, {"fused": FUSED_BYTES}), ("gpt", 4, 2, 2, {})]
+            ("layer", 1, 8, 1, {}), ("layer", 4, 2, 2, {"fused": FUSED_BYTES}), ("layer", 4, 2, 4, {"graph": True}),
+            ("gpt", 4, 2, 2, {})]
     res = _spawn(8, jobs)
     for job in jobs:
         key = str(job[:4])
