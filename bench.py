@@ -514,7 +514,9 @@ def main() -> None:
     gemm_tflops = (prof.flops[0] / n_prof) / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     peak_tc = pk["bf16_tflops_sustained"] or pk["bf16_tflops"]
     roofline = {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_tc, "unit": "TFLOP/s",
-                "frac": gemm_tflops / peak_tc, "traffic": traffic_for(a.peaks, h, T),
+                "frac": gemm_tflops / peak_tc,
+                "traffic": (lambda t: t["dram_bytes_per_gemm_launch"] if t else None)(traffic_for(a.peaks, h, T)),
+                "traffic_detail": traffic_for(a.peaks, h, T),
                 "kernel": "gemm_sm100_kernel (tcgen05, all GEMM launches of the step)",
                 "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside a long step)",
                 "gemm_share_of_step": gemm_ms / ms_prof if ms_prof > 0 else None,

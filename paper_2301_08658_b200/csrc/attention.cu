@@ -738,12 +738,13 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
 //   dP^T = V dO_i^T       [128 keys][64 q]   (A = V K-major,  B = dO_i K-major)
 //   P^T  = exp2(S^T c - lse_q),  dS^T = P^T * (dP^T - D_q)   (softmax warps, lane = key)
 //   dV  += P^T dO_i       [128 keys][128 d]  (A = P^T from TMEM, B = dO_i MN-major)
-//   dK  += dS^T Q_i       [128 keys][128 d]  (A = dS^T smem K-major, B = Q_i MN-major)
+//   dK  += dS^T Q_i       [128 keys][128 d]  (A = dS^T from TMEM, B = Q_i MN-major)
 //   dQ_i^T = K^T dS^T     [128 d][64 q]      (A = K MN-major, B = dS^T MN-major) -> fp32
 //            accumulator with a TMA bulk reduce-add by four dQ warps.
 // TMEM: S^T and dP^T double-buffered (2 x 64 + 2 x 64 columns), dV and dK 2 x
-// 128.  The softmax writes P^T (bf16 pairs) over the S^T columns it read, and
-// dQ_i^T goes into the dP^T buffer of its block once the softmax has read it.
+// 128.  The softmax writes P^T and dS^T (bf16 pairs) over the S^T / dP^T
+// columns it read (dS^T also to shared memory, the B operand of dQ^T), and
+// dQ_i^T goes into the dP^T buffer of its block, issued after dK read it.
 // The MMA warp issues S^T / dP^T of block i+1 before waiting for the softmax of
 // block i, so the tensor core works on the next block while the softmax warps
 // run; dQ readout has its own warps.  Q_i, dO_i (+ lse, D) sit in a 3-deep TMA
@@ -903,11 +904,12 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
           ptx::mma_bf16_ts(tdV, tS(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), desc_mn64(sdo, kk), id_kv,
                            (t | kk) != 0 ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < BQ2 / 16; ++kk)  // dK += dS^T Q
-          ptx::mma_bf16_ss(tdK, desc_k_ps(sds, kk), desc_mn64(sq_, kk), id_kv, (t | kk) != 0 ? 1u : 0u);
+        for (int kk = 0; kk < BQ2 / 16; ++kk)  // dK += dS^T Q  (dS^T from TMEM, same column layout as P^T)
+          ptx::mma_bf16_ts(tdK, tdP(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), desc_mn64(sq_, kk), id_kv,
+                           (t | kk) != 0 ? 1u : 0u);
         ptx::mma_commit(q_empty(q));  // Q_i, dO_i (and lse, D) no longer read
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)  // dQ^T = K^T dS^T  (into the consumed dP^T buffer)
+        for (int kk = 0; kk < BKV / 16; ++kk)  // dQ^T = K^T dS^T  (into dP^T[s]: issued after dK, which read dS^T there)
           ptx::mma_bf16_ss(tdP(s), desc_mnmajor(base + L::K, kk), desc_mn_ps(sds, kk), id_dq, kk > 0 ? 1u : 0u);
         ptx::mma_commit(dq_full(s));
         ptx::mma_commit(p_free(s));  // dS^T smem of block t may be overwritten
@@ -947,7 +949,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
         pk[k / 2] = pack_bf16(pv[0], pv[1]);
         dk[k / 2] = pack_bf16(ds[0], ds[1]);
       }
-      ptx::tmem_st_32x32b_x16(tS(s) + lane_off + c0, pk);  // P^T over this thread's own S^T columns
+      ptx::tmem_st_32x32b_x16(tS(s) + lane_off + c0, pk);   // P^T over this thread's own S^T columns
+      ptx::tmem_st_32x32b_x16(tdP(s) + lane_off + c0, dk);  // dS^T over its own dP^T columns (A of dK)
       const uint32_t sds = base + L::dS + s * kPS;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
