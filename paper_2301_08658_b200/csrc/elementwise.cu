@@ -20,17 +20,23 @@
 #include "atp_internal.h"
 #include "attention.h"
 #include "elementwise.h"
+#include "gelu.cuh"
 
 namespace atp {
 
 namespace {
 
+// bf16 path: the MUFU-based exact-erf form (gelu.cuh; erff made these kernels
+// ALU-bound at ~2.4 TB/s); fp32 check mode: erff / expf.
+template <class T>
 __device__ __forceinline__ float gelu_f(float x) {
+  if constexpr (sizeof(T) == 2) return gelu::gelu(x);
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
 }
+template <class T>
 __device__ __forceinline__ float gelu_grad_f(float x) {
-  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
-         x * 0.39894228040143268f * __expf(-0.5f * x * x);
+  if constexpr (sizeof(T) == 2) return gelu::gelu_grad(x);
+  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * expf(-0.5f * x * x);
 }
 
 struct V8 {
@@ -74,7 +80,7 @@ __global__ void gelu_kernel(const T* __restrict__ u, T* __restrict__ h, int64_t 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     V8 v = ld8(u + 8 * i);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v.f[j] = gelu_f(v.f[j]);
+    for (int j = 0; j < 8; ++j) v.f[j] = gelu_f<T>(v.f[j]);
     st8(h + 8 * i, v);
   }
 }
@@ -85,7 +91,7 @@ __global__ void dgelu_kernel(T* __restrict__ dh, const T* __restrict__ u, int64_
     V8 g = ld8(dh + 8 * i);
     V8 x = ld8(u + 8 * i);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) g.f[j] *= gelu_grad_f(x.f[j]);
+    for (int j = 0; j < 8; ++j) g.f[j] *= gelu_grad_f<T>(x.f[j]);
     st8(dh + 8 * i, g);
   }
 }

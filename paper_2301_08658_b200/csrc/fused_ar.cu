@@ -31,15 +31,14 @@
 #include "atp_internal.h"
 #include "elementwise.h"
 #include "fused_ar.h"
+#include "gelu.cuh"
 
 namespace atp {
 
 namespace {
 
-__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
-__device__ __forceinline__ float gelu_grad_f(float x) {
-  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x);
-}
+__device__ __forceinline__ float gelu_f(float x) { return gelu::gelu(x); }  // bf16 path (gelu.cuh)
+__device__ __forceinline__ float gelu_grad_f(float x) { return gelu::gelu_grad(x); }
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;

@@ -28,6 +28,7 @@
 #include <mutex>
 
 #include "atp_internal.h"
+#include "gelu.cuh"
 #include "sm100_ptx.cuh"
 
 namespace atp {
@@ -40,47 +41,8 @@ constexpr int kEpiWarps = 8;                 // 2 per SM sub-partition: hides ep
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer warp + MMA warp + epilogue warps
 constexpr uint32_t kBoxBytesMN = 64 * 64 * 2;  // one MN-major box: 64 (mn) x 64 (k)
 
-// Exact-erf GeLU (reading G15) for the bf16 epilogues.  erf via Abramowitz &
-// Stegun 7.1.26 (|error| <= 1.5e-7, fp32 level; the output is rounded to bf16,
-// 2^-9 relative): erf(z) = 1 - t(a1 + t(a2 + t(a3 + t(a4 + t a5)))) e^{-z^2},
-// t = 1/(1 + p z), z >= 0.  With z = |x|/sqrt(2), e^{-z^2} = e^{-x^2/2} is also
-// phi(x)*sqrt(2 pi), so GeLU'(x) = Phi(x) + x phi(x) reuses it.
-struct ErfExp {
-  float erf_abs;  // erf(|x|/sqrt 2)
-  float e;        // exp(-x^2/2)
-};
-// MUFU reciprocal / exp2 (one instruction each, ~1 ulp): the epilogue runs on
-// the SM sub-partitions that also issue the MMAs and TMA loads, so its
-// instruction count shows up in tensor-pipe utilisation (GeLU GEMMs 88% vs
-// 97% for light epilogues, profiles/r01_ncu_gemm_full_v4.md).
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ ErfExp erf_as(float x) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
-  const float poly =
-      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
-  const float e = ex2_approx(-0.72134752044448170f * x * x);  // exp(-x^2/2) = 2^(-x^2 / (2 ln 2))
-  return {1.0f - poly * e, e};
-}
-__device__ __forceinline__ float gelu_f(float x) {
-  const ErfExp r = erf_as(x);
-  const float erf = copysignf(r.erf_abs, x);
-  return 0.5f * x * (1.0f + erf);
-}
-__device__ __forceinline__ float gelu_grad_f(float x) {
-  const ErfExp r = erf_as(x);
-  const float erf = copysignf(r.erf_abs, x);
-  return fmaf(0.5f, 1.0f + erf, x * 0.39894228040143268f * r.e);
-}
+__device__ __forceinline__ float gelu_f(float x) { return gelu::gelu(x); }
+__device__ __forceinline__ float gelu_grad_f(float x) { return gelu::gelu_grad(x); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
