@@ -365,9 +365,13 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; each tcgen05 op is issued by one elected lane
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, 128, 0, 1);
+      auto adv = [](uint64_t d, uint32_t bytes) { return d + (bytes >> 4); };
+      const uint64_t q_kmaj[2] = {ptx::smem_desc_sw128(sQ(0), 16, 1024), ptx::smem_desc_sw128(sQ(1), 16, 1024)};
+      const uint64_t k_kmaj[2] = {ptx::smem_desc_sw128(sK(0), 16, 1024), ptx::smem_desc_sw128(sK(1), 16, 1024)};
+      const uint64_t v_mnmaj[2] = {ptx::smem_desc_sw128(sV(0), kHalf, 1024), ptx::smem_desc_sw128(sV(1), kHalf, 1024)};
       int kv_seen = -1;
       auto need_kv = [&](int j) {
         if (j > kv_seen) {
@@ -379,9 +383,9 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
       auto issue_s = [&](int t, int j) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          ptx::mma_bf16_ss(tmem + 256 * t, desc_kmajor(sQ(t), kk), desc_kmajor(sK(j & 1), kk), idesc_s,
-                           kk > 0 ? 1u : 0u);
-        ptx::mma_commit(s_full(t));
+          ptx::mma_bf16_ss_w(tmem + 256 * t, adv(q_kmaj[t], (kk >> 2) * kHalf + (kk & 3) * 32),
+                             adv(k_kmaj[j & 1], (kk >> 2) * kHalf + (kk & 3) * 32), idesc_s, kk > 0 ? 1u : 0u);
+        ptx::mma_commit_w(s_full(t));
       };
       ptx::mbar_wait(q_full, 0);
       need_kv(0);
@@ -394,15 +398,15 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
           ptx::tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)
-            ptx::mma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, desc_mnmajor(sV(j & 1), kk), idesc_o,
-                             (j | kk) != 0 ? 1u : 0u);
-          ptx::mma_commit(o_done(t));
+            ptx::mma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, adv(v_mnmaj[j & 1], kk * 2048), idesc_o,
+                               (j | kk) != 0 ? 1u : 0u);
+          ptx::mma_commit_w(o_done(t));
           if (j + 1 < n[t]) {
             need_kv(j + 1);
             issue_s(t, j + 1);
           }
         }
-        ptx::mma_commit(kv_empty(j & 1));
+        ptx::mma_commit_w(kv_empty(j & 1));
       }
     }
   } else {
@@ -871,24 +875,34 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; each tcgen05 op is issued by one elected lane
       constexpr uint32_t id_st = ptx::idesc_bf16_f32(128, BQ2, 0, 0);  // S^T, dP^T: both K-major
-      constexpr uint32_t id_kv = ptx::idesc_bf16_f32(128, 128, 0, 1);  // dV (A in TMEM), dK: B MN-major
+      constexpr uint32_t id_kv = ptx::idesc_bf16_f32(128, 128, 0, 1);  // dV, dK (A in TMEM): B MN-major
       constexpr uint32_t id_dq = ptx::idesc_bf16_f32(128, BQ2, 1, 1);  // dQ^T: both MN-major
+      // Descriptors built once; per K step only the 14-bit start address moves
+      // (a 64-bit add of a compile-time offset >> 4): the single issuing thread
+      // must keep up with N=64 MMAs of 32 cycles each.
+      auto adv = [](uint64_t d, uint32_t bytes) { return d + (bytes >> 4); };
+      const uint64_t k_kmaj = ptx::smem_desc_sw128(base + L::K, 16, 1024);
+      const uint64_t v_kmaj = ptx::smem_desc_sw128(base + L::V, 16, 1024);
+      const uint64_t k_mnmaj = ptx::smem_desc_sw128(base + L::K, kHalf, 1024);
       auto issue_sdp = [&](int t) {
         const int s = t & 1, q = t % kQSlots;
         ptx::mbar_wait(q_full(q), (t / kQSlots) & 1);
         if (t >= 2) ptx::mbar_wait(s_free(s), ((t - 2) >> 1) & 1);  // dQ^T of block t-2 read out of dP^T[s]
         ptx::tc_fence_after();
-        const uint32_t sq_ = base + L::Q + q * kQ2, sdo = base + L::dO + q * kQ2;
+        const uint64_t q_kmaj = ptx::smem_desc_sw128(base + L::Q + q * kQ2, 16, 1024);
+        const uint64_t do_kmaj = ptx::smem_desc_sw128(base + L::dO + q * kQ2, 16, 1024);
         // S^T[s] overwrites P^T of block t-2: in issue order after dV(t-2), which read it
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          ptx::mma_bf16_ss(tS(s), desc_kmajor(base + L::K, kk), desc_k64(sq_, kk), id_st, kk > 0 ? 1u : 0u);
+          ptx::mma_bf16_ss_w(tS(s), adv(k_kmaj, (kk >> 2) * kHalf + (kk & 3) * 32),
+                           adv(q_kmaj, (kk >> 2) * kBox64 + (kk & 3) * 32), id_st, kk > 0 ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          ptx::mma_bf16_ss(tdP(s), desc_kmajor(base + L::V, kk), desc_k64(sdo, kk), id_st, kk > 0 ? 1u : 0u);
-        ptx::mma_commit(s_full(s));
+          ptx::mma_bf16_ss_w(tdP(s), adv(v_kmaj, (kk >> 2) * kHalf + (kk & 3) * 32),
+                           adv(do_kmaj, (kk >> 2) * kBox64 + (kk & 3) * 32), id_st, kk > 0 ? 1u : 0u);
+        ptx::mma_commit_w(s_full(s));
       };
       ptx::mbar_wait(kv_full, 0);
       if (n > 0) issue_sdp(0);
@@ -897,24 +911,25 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
         if (t + 1 < n) issue_sdp(t + 1);  // the next block's products run during this block's softmax
         ptx::mbar_wait(ds_full(s), (t >> 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t sq_ = base + L::Q + q * kQ2, sdo = base + L::dO + q * kQ2;
-        const uint32_t sds = base + L::dS + s * kPS;
+        const uint64_t q_mnmaj = ptx::smem_desc_sw128(base + L::Q + q * kQ2, kBox64, 1024);
+        const uint64_t do_mnmaj = ptx::smem_desc_sw128(base + L::dO + q * kQ2, kBox64, 1024);
+        const uint64_t ds_mnmaj = ptx::smem_desc_sw128(base + L::dS + s * kPS, kPS, 1024);
 #pragma unroll
         for (int kk = 0; kk < BQ2 / 16; ++kk)  // dV += P^T dO  (P^T from TMEM: q 0-31 at cols 0-15, 32-63 at 32-47)
-          ptx::mma_bf16_ts(tdV, tS(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), desc_mn64(sdo, kk), id_kv,
+          ptx::mma_bf16_ts_w(tdV, tS(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), adv(do_mnmaj, kk * 2048), id_kv,
                            (t | kk) != 0 ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < BQ2 / 16; ++kk)  // dK += dS^T Q  (dS^T from TMEM, same column layout as P^T)
-          ptx::mma_bf16_ts(tdK, tdP(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), desc_mn64(sq_, kk), id_kv,
+          ptx::mma_bf16_ts_w(tdK, tdP(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), adv(q_mnmaj, kk * 2048), id_kv,
                            (t | kk) != 0 ? 1u : 0u);
-        ptx::mma_commit(q_empty(q));  // Q_i, dO_i (and lse, D) no longer read
+        ptx::mma_commit_w(q_empty(q));  // Q_i, dO_i (and lse, D) no longer read
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)  // dQ^T = K^T dS^T  (into dP^T[s]: issued after dK, which read dS^T there)
-          ptx::mma_bf16_ss(tdP(s), desc_mnmajor(base + L::K, kk), desc_mn_ps(sds, kk), id_dq, kk > 0 ? 1u : 0u);
-        ptx::mma_commit(dq_full(s));
-        ptx::mma_commit(p_free(s));  // dS^T smem of block t may be overwritten
+          ptx::mma_bf16_ss_w(tdP(s), adv(k_mnmaj, kk * 2048), adv(ds_mnmaj, kk * 2048), id_dq, kk > 0 ? 1u : 0u);
+        ptx::mma_commit_w(dq_full(s));
+        ptx::mma_commit_w(p_free(s));  // dS^T smem of block t may be overwritten
       }
-      ptx::mma_commit(done);
+      ptx::mma_commit_w(done);
     }
   } else if (warp < 10) {
     // ---- softmax warps: lane = key row, 32 query columns each
