@@ -319,9 +319,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {
       // ------------------------------------------------ MMA issuer (leader CTA only)
+      // The whole warp runs the loop and one elected lane issues each tcgen05
+      // op; the stage descriptors are built once and advanced by constants, so
+      // the issue cost per MMA is a few uniform instructions even while the
+      // epilogue warps of the same sub-partitions are busy.
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM * CG, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      auto adv = [](uint64_t d, uint32_t bytes) { return d + (bytes >> 4); };
+      const uint64_t a0 = A_MN ? ptx::smem_desc_sw128(base, kBoxBytesMN, 1024) : ptx::smem_desc_sw128(base, 16, 1024);
+      const uint64_t b0 = B_MN ? ptx::smem_desc_sw128(base + L::kABytes, kBoxBytesMN, 1024)
+                               : ptx::smem_desc_sw128(base + L::kABytes, 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -333,24 +341,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < num_k; ++kb) {
           ptx::mbar_wait(full_bar(stage), phase);
           ptx::tc_fence_after();
-          const uint32_t sA = base + stage * L::kStageBytes;
-          const uint32_t sB = sA + L::kABytes;
+          const uint32_t so = static_cast<uint32_t>(stage) * L::kStageBytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(sA + kk * 2048, kBoxBytesMN, 1024)
-                                     : ptx::smem_desc_sw128(sA + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(sB + kk * 2048, kBoxBytesMN, 1024)
-                                     : ptx::smem_desc_sw128(sB + kk * 32, 16, 1024);
+            const uint64_t ad = adv(a0, so + (A_MN ? kk * 2048 : kk * 32));
+            const uint64_t bd = adv(b0, so + (B_MN ? kk * 2048 : kk * 32));
             if constexpr (CG == 2) {
-              ptx::mma_bf16_ss_cg2(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+              ptx::mma_bf16_ss_cg2_w(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
             } else {
-              ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+              ptx::mma_bf16_ss_w(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
             }
           }
           if constexpr (CG == 2) {
-            ptx::mma_commit_cg2_mc(empty_bar(stage), 0x3);
+            ptx::mma_commit_cg2_mc_w(empty_bar(stage), 0x3);
           } else {
-            ptx::mma_commit(empty_bar(stage));
+            ptx::mma_commit_w(empty_bar(stage));
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -358,9 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if constexpr (CG == 2) {
-          ptx::mma_commit_cg2_mc(tfull_bar(acc), 0x3);
+          ptx::mma_commit_cg2_mc_w(tfull_bar(acc), 0x3);
         } else {
-          ptx::mma_commit(tfull_bar(acc));
+          ptx::mma_commit_w(tfull_bar(acc));
         }
         if (++acc == 2) {
           acc = 0;
