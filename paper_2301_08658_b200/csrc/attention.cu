@@ -77,11 +77,32 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile, int kk) {
 
 struct FwdParams {
   int T, seq, heads, causal;
+  int grouped;  // CTA order: G > 0 = chunks of G (sequence, head) groups, heaviest first inside a chunk (L2 reuse)
   float scale_log2;  // log2(e) / sqrt(d)
   __nv_bfloat16* ctx;
   int64_t ld_ctx;
   float* lse;  // [heads][T], natural log
 };
+
+// CTA order.  G == 0: heaviest work first across the whole grid.  G > 0: the
+// (sequence, head) groups are taken G at a time (a chunk of ~2 waves of CTAs
+// whose K/V or Q/dO stay in L2 while every block of the chunk re-reads them),
+// heaviest first inside a chunk (so the tail stays light).  `per_group` =
+// CTAs of one group, `j` = heaviness rank inside the group (0 = heaviest).
+__device__ __forceinline__ void cta_order(int G, int n_groups, int per_group, int& j, int& group) {
+  const int b = static_cast<int>(blockIdx.x);
+  if (G <= 0) {
+    j = b / n_groups;
+    group = b % n_groups;
+    return;
+  }
+  const int c = b / (G * per_group);
+  const int first = c * G;
+  const int gc = min(G, n_groups - first);
+  const int in = b - first * per_group;
+  j = in / gc;
+  group = first + in % gc;
+}
 
 // Block index -> (query block, head, sequence); causal: heaviest query blocks first.
 __device__ __forceinline__ void fwd_coords(const FwdParams& p, int& qb, int& head, int& sq) {
@@ -310,9 +331,9 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nq = p.seq / BQ, nm = (nq + 1) / 2, nseq = p.T / p.seq;
   const int per = p.heads * nseq;
-  int m = static_cast<int>(blockIdx.x) / per;
+  int m, rest;
+  cta_order(p.grouped, per, nm, m, rest);
   if (p.causal) m = nm - 1 - m;  // heaviest first
-  const int rest = static_cast<int>(blockIdx.x) % per;
   const int head = rest % p.heads, sq = rest / p.heads;
   const int row0 = sq * p.seq;
   int qblk[2], n[2];
@@ -518,6 +539,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
 // kernel scales and converts them.
 struct BwdParams {
   int T, seq, heads, causal;
+  int grouped;  // as FwdParams::grouped
   float scale_log2;  // log2(e) / sqrt(d)
   float scale;       // 1 / sqrt(d)
   const float* lse;  // [heads][T] natural log (forward output)
@@ -810,9 +832,9 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 144 - raw));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nseq = p.T / p.seq, per = p.heads * nseq;
-  const int jb = static_cast<int>(blockIdx.x) / per;  // causal: key block 0 sees the most query blocks
-  const int rest = static_cast<int>(blockIdx.x) % per;
+  const int nseq = p.T / p.seq, per = p.heads * nseq, nkb = p.seq / BKV;
+  int jb, rest;  // causal: key block 0 sees the most query blocks
+  cta_order(p.grouped, per, nkb, jb, rest);
   const int head = rest % p.heads, sq = rest / p.heads;
   const int row0 = sq * p.seq, kvrow = row0 + jb * BKV;
   const int nqb = p.seq / BQ2;
@@ -1122,7 +1144,17 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
                cudaSuccess;
   }();
   (void)attr;
+  static const bool grouped = [] {
+    const char* e = getenv("ATP_ATTN_ORDER");
+    return !(e && e[0] == '0');
+  }();
   FwdParams p;
+  {
+    // causal: global heaviest-first (measured better: the load balance matters
+    // more than K/V reuse); non-causal (uniform CTAs): chunks of ~4 waves
+    const int per_group = (seq / BQ + 1) / 2;  // CTAs of one (sequence, head): query-tile pairs
+    p.grouped = grouped && !causal ? (4 * num_sms() + per_group - 1) / per_group : 0;
+  }
   p.T = T;
   p.seq = seq;
   p.heads = heads;
@@ -1160,7 +1192,13 @@ cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, in
   const int sms = num_sms();
   attn_bwd_prep_kernel<<<sms * 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(ctx), ld_ctx,
                                                 static_cast<const __nv_bfloat16*>(dctx), ld_dctx, T, heads, D, dq_acc);
+  static const bool grouped = [] {
+    const char* e = getenv("ATP_ATTN_ORDER");
+    return !(e && e[0] == '0');
+  }();
   BwdParams p;
+  // chunks of ~4 waves of key-block CTAs (seq / 128 per group): Q/dO of a chunk stay in L2
+  p.grouped = grouped ? (4 * num_sms() + seq / BKV - 1) / (seq / BKV) : 0;
   p.T = T;
   p.seq = seq;
   p.heads = heads;
