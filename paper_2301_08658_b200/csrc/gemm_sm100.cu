@@ -271,8 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       // ------------------------------------------------ TMA producer (both CTAs)
+      // whole warp runs the loop; one elected lane issues each TMA / expect_tx
       int stage = 0;
       uint32_t phase = 0;
       int gated_chunk = -1;
@@ -290,13 +291,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sA = base + stage * L::kStageBytes;
           const uint32_t sB = sA + L::kABytes;
           const uint32_t fb = full_bar(stage);
-          if (leader) ptx::mbar_arrive_expect_tx(fb, L::kStageBytes * CG);
+          if (leader) ptx::mbar_arrive_expect_tx_w(fb, L::kStageBytes * CG);
           const int k0 = kb * BK;
           auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1) {
             if constexpr (CG == 2) {
-              ptx::tma_load_2d_cg2(dst, tm, fb, c0, c1);
+              ptx::tma_load_2d_cg2_w(dst, tm, fb, c0, c1);
             } else {
-              ptx::tma_load_2d(dst, tm, fb, c0, c1);
+              ptx::tma_load_2d_w(dst, tm, fb, c0, c1);
             }
           };
           if constexpr (!A_MN) {
