@@ -157,6 +157,83 @@ __global__ void ln_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, int64_
   }
 }
 
+// d2 == 1: statistics and apply in one kernel (one warp per row; the second
+// pass re-reads the row, mostly from L2).  Measured against the split kernels
+// (profiles/r01_ln_fused.md): forward 119 -> 87 us per step (x leaves HBM
+// once), backward even (its two passes touch 3x more bytes per row than L2 can
+// hold across the resident warps).  Holding the row in registers instead was
+// slower (one 8-warp CTA per SM at 220 registers).
+__global__ void ln_fwd_fused_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t rows, int64_t cols,
+                                    const __nv_bfloat16* __restrict__ gamma, const __nv_bfloat16* __restrict__ beta,
+                                    __nv_bfloat16* __restrict__ y, int64_t ldy, float* __restrict__ saved) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    float s = 0.f, q = 0.f;
+#pragma unroll 4
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 v = ld8(x + r * ldx + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s += v.v[i];
+        q += v.v[i] * v.v[i];
+      }
+    }
+    s = warp_sum(s);
+    q = warp_sum(q);
+    const float mean = s / static_cast<float>(cols);
+    const float var = fmaxf(q / static_cast<float>(cols) - mean * mean, 0.f);
+    const float rstd = rsqrtf(var + kLnEps);
+#pragma unroll 4
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 v = ld8(x + r * ldx + c), g = ld8(gamma + c), b = ld8(beta + c);
+      F8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o.v[i] = (v.v[i] - mean) * rstd * g.v[i] + b.v[i];
+      st8(y + r * ldy + c, o);
+    }
+    if (lane == 0) {
+      saved[2 * r] = mean;
+      saved[2 * r + 1] = rstd;
+    }
+  }
+}
+
+__global__ void ln_bwd_fused_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy, const __nv_bfloat16* __restrict__ x,
+                                    int64_t ldx, int64_t rows, int64_t cols, const __nv_bfloat16* __restrict__ gamma,
+                                    const float* __restrict__ saved, const __nv_bfloat16* res, int64_t ldres,
+                                    __nv_bfloat16* out, int64_t ldo) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    const float mean = saved[2 * r], rstd = saved[2 * r + 1];
+    float s = 0.f, q = 0.f;
+#pragma unroll 4
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 d = ld8(dy + r * lddy + c), v = ld8(x + r * ldx + c), g = ld8(gamma + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gg = d.v[i] * g.v[i];
+        s += gg;
+        q += gg * (v.v[i] - mean) * rstd;
+      }
+    }
+    const float m1 = warp_sum(s) / static_cast<float>(cols), m2 = warp_sum(q) / static_cast<float>(cols);
+#pragma unroll 4
+    for (int64_t c = 8 * lane; c < cols; c += 256) {
+      const F8 d = ld8(dy + r * lddy + c), v = ld8(x + r * ldx + c), g = ld8(gamma + c);
+      const F8 rr = ld8(res + r * ldres + c);
+      F8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (v.v[i] - mean) * rstd;
+        o.v[i] = rr.v[i] + rstd * (d.v[i] * g.v[i] - m1 - xh * m2);
+      }
+      st8(out + r * ldo + c, o);
+    }
+  }
+}
+
 // Partial column sums over row segment blockIdx.y: part[0][seg][c] = sum dy*xhat,
 // part[1][seg][c] = sum dy.  One thread per column.
 __global__ void ln_param_part_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
@@ -236,6 +313,17 @@ cudaError_t gpt_ew_launch(const EwDesc& e, cudaStream_t st) {
           static_cast<const bf*>(e.c), static_cast<const float*>(e.ws), static_cast<const float*>(e.out2),
           static_cast<float>(e.n_total), static_cast<const bf*>(e.res), e.ldres > 0 ? e.ldres : e.cols,
           static_cast<bf*>(e.out), ldo);
+      break;
+    case EW_LN_FWD:
+      ln_fwd_fused_kernel<<<grid_for(e.rows), 256, 0, st>>>(
+          static_cast<const bf*>(e.a), lda, e.rows, e.cols, static_cast<const bf*>(e.b), static_cast<const bf*>(e.c),
+          static_cast<bf*>(e.out), ldo, static_cast<float*>(e.ws));
+      break;
+    case EW_LN_BWD:
+      ln_bwd_fused_kernel<<<grid_for(e.rows), 256, 0, st>>>(
+          static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b), e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
+          static_cast<const bf*>(e.c), static_cast<const float*>(e.ws), static_cast<const bf*>(e.res),
+          e.ldres > 0 ? e.ldres : e.cols, static_cast<bf*>(e.out), ldo);
       break;
     case EW_LN_PARAM_GRAD: {
       float* part = static_cast<float*>(e.out2);  // workspace: ln_param_workspace_bytes(cols)

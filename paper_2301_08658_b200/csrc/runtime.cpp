@@ -141,6 +141,8 @@ void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes) {
       case EW_LN_STATS: case EW_PACK: case EW_UNPACK: *bytes = (op.e.kind == EW_LN_STATS ? 2.0 : 4.0) * n; break;
       case EW_LN_APPLY: case EW_LN_BWD_STATS: *bytes = 4.0 * n; break;
       case EW_LN_BWD_APPLY: *bytes = 8.0 * n; break;
+      case EW_LN_FWD: *bytes = 4.0 * n; break;   // x read once, y written
+      case EW_LN_BWD: *bytes = 8.0 * n; break;   // dy, x, res read once, out written
       case EW_LN_PARAM_GRAD: *bytes = 4.0 * n; break;
       default: break;
     }

@@ -689,6 +689,12 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
   // LayerNorm of every chunk: row statistics, dim-2 all-reduce (G33), apply (deferred)
   auto layernorm = [&](const void* x, const void* g, const void* be, size_t st_off, float* sv, void* y) {
     for (int k = 0; k < chunks; ++k) {
+      if (d2 == 1) {  // the whole row is local: statistics + apply in one kernel
+        EwDesc e = ln_apply(R(x, k, hc), g, be, nullptr, static_cast<float*>(R(sv, k, 2, 4)), R(y, k, hc), Mc);
+        e.kind = EW_LN_FWD;
+        ew_k(k, e);
+        continue;
+      }
       float* st = static_cast<float*>(R(W(st_off), k, 2, 4));
       ew_k(k, ln_stats(R(x, k, hc), Mc, st));
       const EwDesc ap = ln_apply(R(x, k, hc), g, be, st, static_cast<float*>(R(sv, k, 2, 4)), R(y, k, hc), Mc);
@@ -703,6 +709,12 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
     for (int k = 0; k < chunks; ++k) {
       float* bs = static_cast<float*>(R(W(bs_off), k, 2, 4));
       float* svk = static_cast<float*>(R(sv, k, 2, 4));
+      if (d2 == 1) {  // statistics + apply in one kernel
+        EwDesc e = ln_bapply(R(dy, k, hc), R(x, k, hc), g, svk, nullptr, R(res, k, hc), R(o, k, hc), Mc);
+        e.kind = EW_LN_BWD;
+        ew_k(k, e);
+        continue;
+      }
       ew_k(k, ln_bstats(R(dy, k, hc), R(x, k, hc), g, svk, bs, Mc));
       const EwDesc ap = ln_bapply(R(dy, k, hc), R(x, k, hc), g, svk, bs, R(res, k, hc), R(o, k, hc), Mc);
       if (d2 > 1)

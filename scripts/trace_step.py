@@ -16,7 +16,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 EW = ["gelu", "dgelu", "add", "core_fwd", "core_bwd", "colsum", "ln_stats", "ln_apply", "ln_bwd_stats",
-      "ln_bwd_apply", "ln_param_grad", "pack", "unpack", "attn_fwd", "attn_bwd"]
+      "ln_bwd_apply", "ln_param_grad", "pack", "unpack", "attn_fwd", "attn_bwd", "ln_fwd", "ln_bwd"]
 EPI = ["bf16", "f32", "resid", "bias_gelu", "dgelu"]
 KIND = {0: "gemm", 1: "ew", 2: "coll", 4: "fused_ar"}
 
