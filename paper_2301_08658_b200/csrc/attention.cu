@@ -545,7 +545,6 @@ struct BwdParams {
   const float* lse;  // [heads][T] natural log (forward output)
   const float* D;    // [heads][T] rowsum(dO * O)
   float* dq_acc;     // [T][heads*128] fp32
-  int skip_dq;       // timing experiments only (ATP_ATTN_NO_DQ=1): results wrong
   __nv_bfloat16* dqkv;
   int64_t ld_dqkv;
 };
@@ -698,11 +697,6 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
 #pragma unroll
       for (int c = 0; c < 2; ++c) ptx::tmem_ld_32x32b_x32(tmem + lane_off + 128 + c0 + 32 * c, qu[c]);
       ptx::tmem_wait_ld();
-      if (p.skip_dq) {
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(s_free);
-        continue;
-      }
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const uint32_t box = sP + static_cast<uint32_t>((c0 + 32 * c) / 32) * kHalf;  // [128 rows][32 fp32]
@@ -1208,11 +1202,6 @@ cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, in
   p.lse = lse;
   p.D = D;
   p.dq_acc = dq_acc;
-  static const int skip_dq = [] {
-    const char* e = getenv("ATP_ATTN_NO_DQ");
-    return e && e[0] == '1' ? 1 : 0;
-  }();
-  p.skip_dq = skip_dq;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dqkv = ld_dqkv;
   const int grid = (seq / BKV) * heads * (T / seq);
