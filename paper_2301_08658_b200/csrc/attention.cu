@@ -451,9 +451,13 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
         for (int c = 0; c < BKV; ++c)
           if (c > r) u[c / 32][c % 32] = __float_as_uint(-INFINITY);
       }
-      float mb = __uint_as_float(u[0][0]);
+      // row max as an 8-way tree (a 128-long dependent fmax chain was ~500 cycles)
+      float mx[8];
 #pragma unroll
-      for (int c = 1; c < BKV; ++c) mb = fmaxf(mb, __uint_as_float(u[c / 32][c % 32]));
+      for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(u[i / 32][i % 32]);
+#pragma unroll
+      for (int c = 8; c < BKV; ++c) mx[c % 8] = fmaxf(mx[c % 8], __uint_as_float(u[c / 32][c % 32]));
+      float mb = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
       mb *= p.scale_log2;
       // Lazy rescale (warp-uniform: tcgen05.ld/st are warp-collective).  P is
       // written with the new max first; O is corrected afterwards, once the
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
         f = ex2(m_run - m_new);
         m_run = m_new;
       }
-      float rs = 0.f;
+      float rsv[4] = {0.f, 0.f, 0.f, 0.f};  // four partial row sums (short dependency chains)
 #pragma unroll
       for (int c = 0; c < BKV / 32; ++c) {
         uint32_t pk[16];
@@ -474,11 +478,12 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
         for (int i = 0; i < 16; ++i) {
           const float e0 = ex2(fmaf(__uint_as_float(u[c][2 * i]), p.scale_log2, -m_run));
           const float e1 = ex2(fmaf(__uint_as_float(u[c][2 * i + 1]), p.scale_log2, -m_run));
-          rs += e0 + e1;
+          rsv[i % 4] += e0 + e1;
           pk[i] = pack_bf16(e0, e1);
         }
         ptx::tmem_st_32x32b_x16(tS + c * 16, pk);  // P (bf16 pairs) over the S columns
       }
+      const float rs = (rsv[0] + rsv[1]) + (rsv[2] + rsv[3]);
       l = l * f + rs;
       if (rescale && j > 0) {
 #pragma unroll
