@@ -50,6 +50,10 @@ struct GemmDesc {
   // previous stage's chunk k is all-reduced).  nullptr = no gating.
   const uint32_t* gate = nullptr;
   uint32_t gate_target = 0;
+  // Programmatic dependent launch (set by the executor only when the GEMM's
+  // sole dependency is the previous kernel of its stream and it spins on no
+  // gate: an early-launched CTA must never hold SMs another stream needs).
+  bool pdl = false;
   // fp32 check mode (gemm_f32.cu): dtype 1, raw operands instead of TMA maps
   int dtype = 0;
   const void* A = nullptr;

@@ -269,6 +269,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the set-up above (barriers, TMEM, tensor-map
+  // prefetch) overlapped the previous kernel's tail; the next GEMM may now be
+  // scheduled onto SMs as this grid's CTAs retire, and nothing here touches
+  // global memory before the previous grid has completed and flushed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     {
@@ -523,13 +529,19 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = L::kBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  static const bool pdl = [] {  // ATP_PDL=0 disables programmatic dependent launch (A/B runs)
+    const char* e = getenv("ATP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (pdl && d.pdl && d.gate == nullptr) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.tmC, d.tmC2, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate,
                             d.gate_target, d.group_m > 0 ? d.group_m : 16);
 }

@@ -224,9 +224,14 @@ static int ensure_events(RankState& s, int n) {
   return 0;
 }
 
-static cudaError_t launch_local(const Op& op, cudaStream_t st) {
+// `prev_kernel`: the previous enqueue on this stream in this call was one of
+// our kernels.  Only then may a GEMM use programmatic dependent launch (its
+// one dependency is that kernel; see GemmDesc::pdl): no event wait, no gate
+// spin, no chunk counters (which the per-call reset must precede), no profiling.
+static cudaError_t launch_local(Op& op, cudaStream_t st, bool prev_kernel, bool profiling) {
   if (op.kind == OP_GEMM) {
     count_launch(1);
+    op.g.pdl = prev_kernel && !profiling && op.n_waits == 0 && op.g.gate == nullptr && op.g.sig == nullptr;
     return gemm_launch(op.g, st);
   }
   count_launch(op.e.kind == EW_ATTN_BWD ? 3 : (op.e.kind == EW_LN_PARAM_GRAD ? 2 : 1));
@@ -306,6 +311,7 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
 
   if (!m->is_virtual) {
     RankState& s = m->rs[0];
+    bool prevk[3] = {false, false, false};
     for (Op& op : sch[0].ops) {
       cudaStream_t st = op.stream == 1 ? s.comm : (op.stream == 2 ? s.aux : stream);
       if ((e = wait_all(op, s, st)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
@@ -313,11 +319,13 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
       if (op.kind == OP_SIGNAL) {
         if ((e = signal_gate(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWriteValue32");
         if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+        prevk[op.stream] = false;
         continue;
       }
       if (op.kind == OP_WAITSIG) {
         if ((e = wait_sig(s, op, st)) != cudaSuccess) return cuda_fail(e, "cuStreamWaitValue32");
         if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
+        prevk[op.stream] = false;
         continue;
       }
       ProfRec* pr = prof_begin(m, op, st);
@@ -328,9 +336,10 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
           const int rc = nccl_coll(m, op, st);
           if (rc) return rc;
         }
-      } else if ((e = launch_local(op, st)) != cudaSuccess) {
+      } else if ((e = launch_local(op, st, prevk[op.stream] && op.n_waits == 0, m->profiling)) != cudaSuccess) {
         return cuda_fail(e, op.kind == OP_GEMM ? "gemm launch" : "elementwise launch");
       }
+      prevk[op.stream] = op.kind == OP_GEMM || op.kind == OP_EW;
       prof_end(pr, st);
       if (op.record >= 0) cudaEventRecord(s.ev[op.record], st);
     }
@@ -371,7 +380,7 @@ int execute(atp_mesh* m, std::vector<Sched>& sch, cudaStream_t stream) {
         ProfRec* pr = prof_begin(m, op, st);
         if (op.kind == OP_FUSED_AR) {
           if ((e = launch_fused(m, s, op, st)) != cudaSuccess) return cuda_fail(e, "fused all-reduce launch");
-        } else if ((e = launch_local(op, st)) != cudaSuccess) {
+        } else if ((e = launch_local(op, st, false, m->profiling)) != cudaSuccess) {  // virtual mesh: no PDL
           return cuda_fail(e, op.kind == OP_GEMM ? "gemm launch" : "elementwise launch");
         }
         prof_end(pr, st);
