@@ -25,7 +25,7 @@ namespace atp {
 namespace {
 
 constexpr float kLnEps = 1e-5f;  // reading G29 (Megatron / PyTorch default)
-constexpr int kSegs = 32;        // row segments of ln_param_grad
+constexpr int kSegs = 128;       // row segments of ln_param_grad (x cols/2048 CTAs)
 
 struct F8 {
   float v[8];
@@ -235,23 +235,32 @@ __global__ void ln_bwd_fused_kernel(const __nv_bfloat16* __restrict__ dy, int64_
 }
 
 // Partial column sums over row segment blockIdx.y: part[0][seg][c] = sum dy*xhat,
-// part[1][seg][c] = sum dy.  One thread per column.
+// part[1][seg][c] = sum dy.  Eight columns per thread (16-byte loads, eight
+// independent accumulators); rows in order, so the sums are deterministic.
 __global__ void ln_param_part_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
                                      const __nv_bfloat16* __restrict__ x, int64_t ldx, int64_t rows, int64_t cols,
                                      const float* __restrict__ saved, float* __restrict__ part) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t c = 8 * (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x);
   if (c >= cols) return;
   const int64_t per = (rows + kSegs - 1) / kSegs;
   const int64_t r0 = blockIdx.y * per, r1 = r0 + per < rows ? r0 + per : rows;
-  float sg = 0.f, sb = 0.f;
+  float sg[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, sb[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
   for (int64_t r = r0; r < r1; ++r) {
-    const float d = __bfloat162float(dy[r * lddy + c]);
-    const float xh = (__bfloat162float(x[r * ldx + c]) - saved[2 * r]) * saved[2 * r + 1];
-    sg += d * xh;
-    sb += d;
+    const F8 d = ld8(dy + r * lddy + c), v = ld8(x + r * ldx + c);
+    const float mean = saved[2 * r], rstd = saved[2 * r + 1];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      sg[i] += d.v[i] * ((v.v[i] - mean) * rstd);
+      sb[i] += d.v[i];
+    }
   }
-  part[static_cast<int64_t>(blockIdx.y) * cols + c] = sg;
-  part[(kSegs + static_cast<int64_t>(blockIdx.y)) * cols + c] = sb;
+  float* pg = part + static_cast<int64_t>(blockIdx.y) * cols + c;
+  float* pb = part + (kSegs + static_cast<int64_t>(blockIdx.y)) * cols + c;
+  reinterpret_cast<float4*>(pg)[0] = make_float4(sg[0], sg[1], sg[2], sg[3]);
+  reinterpret_cast<float4*>(pg)[1] = make_float4(sg[4], sg[5], sg[6], sg[7]);
+  reinterpret_cast<float4*>(pb)[0] = make_float4(sb[0], sb[1], sb[2], sb[3]);
+  reinterpret_cast<float4*>(pb)[1] = make_float4(sb[4], sb[5], sb[6], sb[7]);
 }
 
 __global__ void ln_param_final_kernel(const float* __restrict__ part, int64_t cols, float* __restrict__ dgamma,
@@ -327,7 +336,7 @@ cudaError_t gpt_ew_launch(const EwDesc& e, cudaStream_t st) {
       break;
     case EW_LN_PARAM_GRAD: {
       float* part = static_cast<float*>(e.out2);  // workspace: ln_param_workspace_bytes(cols)
-      dim3 grid(static_cast<unsigned>((e.cols + 255) / 256), kSegs);
+      dim3 grid(static_cast<unsigned>((e.cols / 8 + 255) / 256), kSegs);  // 8 columns per thread (cols % 8 == 0)
       ln_param_part_kernel<<<grid, 256, 0, st>>>(static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b),
                                                  e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
                                                  static_cast<const float*>(e.ws), part);
