@@ -60,6 +60,9 @@ def parse():
     p.add_argument("--mesh", default="", help="d1xd2; default: atp_search (uniform NVSwitch HCM, or --probe)")
     p.add_argument("--fused-ar", action="store_true",
                    help="N>1: fused peer-memory all-reduce (CUDA IPC) instead of NCCL on the data path")
+    p.add_argument("--nccl-only", action="store_true",
+                   help="N>1 linear block: skip timing the fused peer-memory all-reduce against NCCL "
+                        "(default: both are timed on this box and the faster one runs the measured steps)")
     p.add_argument("--gated", action="store_true",
                    help="N>1: chunk-gated GEMMs (the next stage's GEMM waits per chunk for the all-reduce tail)")
     p.add_argument("--probe", action="store_true",
@@ -475,6 +478,35 @@ def main() -> None:
         run(stream)
     torch.cuda.synchronize()
 
+    # ---- N>1 linear block: NCCL all-reduce (graph-captured step) vs the fused
+    # peer-memory all-reduce (GEMM signalling per chunk + one kernel per chunk
+    # doing the grouped all-reduce over NVLink peer memory with the elementwise
+    # step applied; §5), timed on this box, the faster one runs the measured
+    # steps.  The timings are max-reduced over ranks, so every rank chooses alike.
+    ar_choice = None
+    meshes = [mesh]
+    if world > 1 and not gpt_mode and not a.fused_ar and not a.nccl_only:
+        uid2 = atp.atp_get_unique_id() if rank == 0 else bytes(128)
+        obj = [uid2]
+        dist.broadcast_object_list(obj, src=0)
+        try:
+            mesh_f = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, obj[0], local_rank))
+            meshes.append(mesh_f)
+            mesh_f.set_gemm_ctas(ctas)
+            mesh_f.set_gating(a.gated)
+            mesh_f.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
+            call_f = atp.LayerCall(mesh_f, [bufs], T, h, F, heads, chunks, True)
+            for _ in range(3):
+                call_f(stream)
+            t_nccl, t_fused = timed(10, run), timed(10, call_f)
+            ar_choice = {"nccl_ms": t_nccl, "fused_peer_memory_ms": t_fused,
+                         "chosen": "fused" if t_fused < t_nccl else "nccl"}
+            if t_fused < t_nccl:
+                mesh, call, run = mesh_f, call_f, call_f
+                graph_note = "direct calls (fused peer-memory mesh keeps cross-rank state: no graph capture)"
+        except Exception as e:  # noqa: BLE001
+            ar_choice = {"error": str(e), "chosen": "nccl"}
+
     # ---- timed region (clocks sampled during it)
     sampler = ClockSampler(local_rank)
     import ctypes as C
@@ -601,7 +633,8 @@ def main() -> None:
 
     for g in graphs:
         g.destroy()
-    mesh.destroy()
+    for m in meshes:
+        m.destroy()
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
@@ -614,7 +647,8 @@ def main() -> None:
                                     f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}"),
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
-                       "allreduce": "fused peer-memory kernel" if (a.fused_ar and world > 1) else "nccl",
+                       "allreduce": ("fused peer-memory kernel" if ((a.fused_ar or (ar_choice or {}).get("chosen") == "fused")
+                                                                    and world > 1) else "nccl"),
                        "gated": bool(a.gated and world > 1), "mesh_source": mesh_source, "launch": graph_note,
                        **({"shared_gpu": "TEST ONLY: all ranks on cuda:0, NCCL over sockets; timings meaningless"}
                           if a.share_gpu else {}),
@@ -625,6 +659,8 @@ def main() -> None:
         }
         if chunk_choice is not None:
             out["chunk_choice"] = chunk_choice
+        if ar_choice is not None:
+            out["allreduce_choice"] = ar_choice
         if gpt_mode:
             out["tflops_paper_formula"] = gpt_flops_paper(T, h, a.seq) / (ms * 1e-3) / 1e12
             out["flops_note"] = ("value counts the FLOPs performed (linear 72Th^2 + causal core 7(s+1)Th); "

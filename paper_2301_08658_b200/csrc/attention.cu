@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_kernel(const __grid_constant_
         ptx::tma_load_2d(sV(s), &tm_qkv, kv_full(s), qcol + 2 * HD, kr);
         ptx::tma_load_2d(sV(s) + kHalf, &tm_qkv, kv_full(s), qcol + 2 * HD + 64, kr);
       }
+      for (int j = nkv; j < nkv + 2; ++j) ptx::mbar_wait(kv_empty(j & 1), ((j >> 1) & 1) ^ 1);  // tail
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
           for (int kk = 0; kk < BKV / 16; ++kk)
             ptx::mma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, adv(v_mnmaj[j & 1], kk * 2048), idesc_o,
                                (j | kk) != 0 ? 1u : 0u);
-          ptx::mma_commit_w(o_done(t));
+          if (j + 1 == n[t]) ptx::mma_commit_w(o_done(t));  // one phase: the final O (nobody waits on the others)
           if (j + 1 < n[t]) {
             need_kv(j + 1);
             issue_s(t, j + 1);
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
       ptx::mbar_arrive(p_full(t));
     }
     if (nt > 0) {
-      ptx::mbar_wait(o_done(t), (nt - 1) & 1);
+      ptx::mbar_wait(o_done(t), 0);
       ptx::tc_fence_after();
       const float inv = 1.f / l;
       const int qrow = row0 + qbt * BQ + r;
@@ -614,6 +615,7 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
         ptx::tma_load_2d(sdO, &tm_do, qdo_full, head * HD, qr);
         ptx::tma_load_2d(sdO + kHalf, &tm_do, qdo_full, head * HD + 64, qr);
       }
+      ptx::mbar_wait(qdo_empty, (n & 1) ^ 1);  // tail: the last Q/dO tile released
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -650,6 +652,7 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
         ptx::mma_commit(dq_full);
       }
       ptx::mma_commit(done);
+      if (n > 0) ptx::mbar_wait(s_free, (n - 1) & 1);  // tail: the last dQ tile read out
     }
   } else {
     // ---- warps 2-9: two threads per query row, columns [64*half, 64*half + 64)
@@ -894,6 +897,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
         ptx::bulk_load_1d(base + L::LD + q * BQ2 * 4, p.lse + lo, BQ2 * 4, q_full(q));
         ptx::bulk_load_1d(base + L::LD + (kQSlots + q) * BQ2 * 4, p.D + lo, BQ2 * 4, q_full(q));
       }
+      for (int t = n; t < n + kQSlots; ++t)  // tail: every slot released (each phase waited)
+        ptx::mbar_wait(q_empty(t % kQSlots), ((t / kQSlots) & 1) ^ 1);
     }
   } else if (warp == 1) {
     {  // the whole warp runs the issue loop; each tcgen05 op is issued by one elected lane
@@ -951,6 +956,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
         ptx::mma_commit_w(p_free(s));  // dS^T smem of block t may be overwritten
       }
       ptx::mma_commit_w(done);
+      for (int t = n; t < n + 2; ++t)  // tail: the last dQ^T read-outs (each phase waited)
+        if (t >= 2) ptx::mbar_wait(s_free(t & 1), ((t - 2) >> 1) & 1);
     }
   } else if (warp < 10) {
     // ---- softmax warps: lane = key row, 32 query columns each
@@ -999,6 +1006,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full(s));
     }
+    for (int t = n; t < n + 2; ++t)  // tail: the last dS^T buffers released (each phase waited)
+      if (t >= 2) ptx::mbar_wait(p_free(t & 1), ((t - 2) >> 1) & 1);
     // ---- dK (scaled), dV -> dqkv rows of this key block (TMEM lane = key row), 64 columns per thread
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();

@@ -324,6 +324,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      // producer tail: wait until the MMA has released every stage (each
+      // mbarrier phase gets a waiter; synccheck-clean, no early exit with
+      // stages still being read)
+      for (int i = 0; i < STAGES; ++i) {
+        ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     if (leader) {
@@ -374,6 +384,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           ptx::mma_commit_w(tfull_bar(acc));
         }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      // tail: both accumulators drained by the epilogue (every phase waited)
+      for (int i = 0; i < 2; ++i) {
+        ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
