@@ -485,27 +485,44 @@ def main() -> None:
     # steps.  The timings are max-reduced over ranks, so every rank chooses alike.
     ar_choice = None
     meshes = [mesh]
-    if world > 1 and not gpt_mode and not a.fused_ar and not a.nccl_only:
+    if world > 1 and not gpt_mode and not a.fused_ar and not a.nccl_only and not a.gated:
+        # candidates: NCCL (graph-captured) and the fused peer-memory all-reduce,
+        # each with and without chunk gating (§6); 10 timed steps each
         uid2 = atp.atp_get_unique_id() if rank == 0 else bytes(128)
         obj = [uid2]
         dist.broadcast_object_list(obj, src=0)
+        times, runners = {}, {}
         try:
+            times["nccl"], runners["nccl"] = timed(10, run), (mesh, call, run, False, graph_note)
+            mesh.set_gating(True)
+            run_g = as_graph(call)
+            for _ in range(2):
+                run_g(stream)
+            times["nccl+gated"] = timed(10, run_g)
+            runners["nccl+gated"] = (mesh, call, run_g, True, graph_note)
+            mesh.set_gating(False)
             mesh_f = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, obj[0], local_rank))
             meshes.append(mesh_f)
             mesh_f.set_gemm_ctas(ctas)
-            mesh_f.set_gating(a.gated)
             mesh_f.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
             call_f = atp.LayerCall(mesh_f, [bufs], T, h, F, heads, chunks, True)
-            for _ in range(3):
-                call_f(stream)
-            t_nccl, t_fused = timed(10, run), timed(10, call_f)
-            ar_choice = {"nccl_ms": t_nccl, "fused_peer_memory_ms": t_fused,
-                         "chosen": "fused" if t_fused < t_nccl else "nccl"}
-            if t_fused < t_nccl:
-                mesh, call, run = mesh_f, call_f, call_f
-                graph_note = "direct calls (fused peer-memory mesh keeps cross-rank state: no graph capture)"
-        except Exception as e:  # noqa: BLE001
-            ar_choice = {"error": str(e), "chosen": "nccl"}
+            note_f = "direct calls (fused peer-memory mesh keeps cross-rank state: no graph capture)"
+            for gated in (False, True):
+                mesh_f.set_gating(gated)
+                for _ in range(3):
+                    call_f(stream)
+                key = "fused+gated" if gated else "fused"
+                times[key] = timed(10, call_f)
+                runners[key] = (mesh_f, call_f, call_f, gated, note_f)
+        except Exception as e:  # noqa: BLE001  (keeps the NCCL step)
+            ar_choice = {"error": str(e)}
+            mesh.set_gating(False)
+        if times:
+            best = min(times, key=times.get)
+            ar_choice = dict(ar_choice or {}, timed_ms=times, chosen=best)
+            mesh, call, run, chosen_gating, graph_note = runners[best]
+            mesh.set_gating(chosen_gating)
+            a.gated = chosen_gating
 
     # ---- timed region (clocks sampled during it)
     sampler = ClockSampler(local_rank)
@@ -647,7 +664,7 @@ def main() -> None:
                                     f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}"),
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
-                       "allreduce": ("fused peer-memory kernel" if ((a.fused_ar or (ar_choice or {}).get("chosen") == "fused")
+                       "allreduce": ("fused peer-memory kernel" if ((a.fused_ar or str((ar_choice or {}).get("chosen", "")).startswith("fused"))
                                                                     and world > 1) else "nccl"),
                        "gated": bool(a.gated and world > 1), "mesh_source": mesh_source, "launch": graph_note,
                        **({"shared_gpu": "TEST ONLY: all ranks on cuda:0, NCCL over sockets; timings meaningless"}
