@@ -112,3 +112,39 @@ def test_graph_refusals():
             atp.Graph.capture(mesh, lambda s: None, st)
     finally:
         mesh.destroy()
+
+
+def test_profile_trace_timeline():
+    """atp_profile_trace: one record per bracketed launch, in enqueue order,
+    non-negative durations, and the per-class totals equal atp_profile_end's."""
+    import ctypes as C
+    import torch
+    import paper_2301_08658_b200 as atp
+    from paper_2301_08658_b200 import _abi
+
+    T, h, F, heads = 1024, 512, 2048, 8
+    mesh = atp.Mesh.virtual(2, 2)
+    try:
+        bufs = [atp.alloc_layer_rank(2, 2, r, T, h, F, "cuda", 5) for r in range(4)]
+        call = atp.LayerCall(mesh, bufs, T, h, F, heads, 2, True)
+        call()
+        torch.cuda.synchronize()
+        lib = _abi.lib()
+        _abi.check(lib.atp_profile_begin(mesh.handle))
+        call()
+        torch.cuda.synchronize()
+        recs = (_abi.TraceRec * 4096)()
+        n = C.c_int()
+        _abi.check(lib.atp_profile_trace(mesh.handle, recs, 4096, C.byref(n)))
+        prof = _abi.Profile()
+        _abi.check(lib.atp_profile_end(mesh.handle, C.byref(prof)))
+    finally:
+        mesh.destroy()
+    rs = list(recs[: n.value])
+    assert n.value == sum(prof.launches) and n.value > 0
+    assert all(r.t1_ms >= r.t0_ms >= 0.0 for r in rs)
+    assert sum(1 for r in rs if r.kind == 0) == prof.launches[0]  # GEMMs
+    for cls in range(4):  # event timestamps have ~0.5 us resolution: per-record slack
+        sel = [r for r in rs if r.cls == cls]
+        tot = sum(r.t1_ms - r.t0_ms for r in sel)
+        assert abs(tot - prof.ms[cls]) <= 2e-3 * (len(sel) + 1) + 1e-2 * prof.ms[cls], cls
