@@ -61,8 +61,10 @@ def parse():
     p.add_argument("--fused-ar", action="store_true",
                    help="N>1: fused peer-memory all-reduce (CUDA IPC) instead of NCCL on the data path")
     p.add_argument("--nccl-only", action="store_true",
-                   help="N>1 linear block: skip timing the fused peer-memory all-reduce against NCCL "
-                        "(default: both are timed on this box and the faster one runs the measured steps)")
+                   help="N>1 linear block: no variant selection (plain NCCL step)")
+    p.add_argument("--try-fused", action="store_true",
+                   help="N>1 linear block: also time the fused peer-memory all-reduce (± gating) against NCCL "
+                        "(± gating) and run the fastest; default: NCCL with / without chunk gating only")
     p.add_argument("--gated", action="store_true",
                    help="N>1: chunk-gated GEMMs (the next stage's GEMM waits per chunk for the all-reduce tail)")
     p.add_argument("--probe", action="store_true",
@@ -486,8 +488,8 @@ def main() -> None:
     ar_choice = None
     meshes = [mesh]
     if world > 1 and not gpt_mode and not a.fused_ar and not a.nccl_only and not a.gated:
-        # candidates: NCCL (graph-captured) and the fused peer-memory all-reduce,
-        # each with and without chunk gating (§6); 10 timed steps each
+        # candidates: NCCL (graph-captured) with and without chunk gating (§6), and
+        # with --try-fused the fused peer-memory all-reduce likewise; 10 timed steps each
         uid2 = atp.atp_get_unique_id() if rank == 0 else bytes(128)
         obj = [uid2]
         dist.broadcast_object_list(obj, src=0)
@@ -501,6 +503,8 @@ def main() -> None:
             times["nccl+gated"] = timed(10, run_g)
             runners["nccl+gated"] = (mesh, call, run_g, True, graph_note)
             mesh.set_gating(False)
+            if not a.try_fused:
+                raise StopIteration
             mesh_f = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, obj[0], local_rank))
             meshes.append(mesh_f)
             mesh_f.set_gemm_ctas(ctas)
@@ -514,6 +518,8 @@ def main() -> None:
                 key = "fused+gated" if gated else "fused"
                 times[key] = timed(10, call_f)
                 runners[key] = (mesh_f, call_f, call_f, gated, note_f)
+        except StopIteration:
+            pass
         except Exception as e:  # noqa: BLE001  (keeps the NCCL step)
             ar_choice = {"error": str(e)}
             mesh.set_gating(False)
