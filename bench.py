@@ -64,7 +64,10 @@ def parse():
                    help="N>1 linear block: no variant selection (plain NCCL step)")
     p.add_argument("--try-fused", action="store_true",
                    help="N>1 linear block: also time the fused peer-memory all-reduce (± gating) against NCCL "
-                        "(± gating) and run the fastest; default: NCCL with / without chunk gating only")
+                        "(± gating) and run the fastest")
+    p.add_argument("--try-gated", action="store_true",
+                   help="N>1 linear block: also time NCCL with chunk gating and run the faster "
+                        "(default: the plain NCCL step, no selection)")
     p.add_argument("--gated", action="store_true",
                    help="N>1: chunk-gated GEMMs (the next stage's GEMM waits per chunk for the all-reduce tail)")
     p.add_argument("--probe", action="store_true",
@@ -487,7 +490,8 @@ def main() -> None:
     # steps.  The timings are max-reduced over ranks, so every rank chooses alike.
     ar_choice = None
     meshes = [mesh]
-    if world > 1 and not gpt_mode and not a.fused_ar and not a.nccl_only and not a.gated:
+    if world > 1 and not gpt_mode and not a.fused_ar and not a.nccl_only and not a.gated and \
+            (a.try_gated or a.try_fused):
         # candidates: NCCL (graph-captured) with and without chunk gating (§6), and
         # with --try-fused the fused peer-memory all-reduce likewise; 10 timed steps each
         uid2 = atp.atp_get_unique_id() if rank == 0 else bytes(128)
