@@ -11,6 +11,8 @@
   cross-token op, so a row needs only its own input rows), plus a property that
   holds at any size for a weight gradient: dW2 = H^T dZ  ==>  dW2 @ 1 = H^T (dZ 1)
   evaluated with the GPU's own saved H.
+* cfg 5 shapes (h=12288, the largest GEMMs) on a 1-rank NCCL mesh: sampled
+  rows + the same dW2 property.
 """
 import numpy as np
 import pytest
@@ -88,3 +90,32 @@ def test_fullsize_cfg4_mesh42_sampled_rows():
         lhs = b["dw2"].double().sum(dim=1)
         rhs = b["h"].double().t() @ b["dz"].double().sum(dim=1)
         assert rel(lhs.cpu().numpy(), rhs.cpu().numpy()) <= TOL
+
+
+def test_fullsize_cfg5_mesh11_sampled_rows():
+    """cfg 5 shapes (h=12288, a=96, F=49152, T=8192: the largest GEMMs, K up to
+    49152) on a 1-rank NCCL mesh as bench.py runs it: sampled token rows of Z,
+    Y1 and dX against the oracle evaluated row by row, and the any-size dW2
+    property."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, seed = 8192, 12288, 49152, 96, 2301
+    mesh = atp.Mesh.distributed(1, 1, 0, atp.atp_get_unique_id(), 0)
+    try:
+        b = atp.alloc_layer_rank(1, 1, 0, T, h, F, "cuda", seed)
+        atp.LayerCall(mesh, [b], T, h, F, heads, 1, True)()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    rng = np.random.default_rng(5)
+    rows = np.sort(np.concatenate([rng.choice(T, 10, replace=False), [0, T - 1]]))
+    g = _globals32(T, h, F, seed, rows=rows)
+    c = olayer.dense_forward(g, heads)
+    d = olayer.dense_backward(g, c, g["dz"], heads)
+    rr = torch.as_tensor(rows, device="cuda")
+    for k, ref in (("z", c["z"]), ("y1", c["y1"]), ("dx", d["dx"])):
+        assert rel(to_np(b[k][rr]), ref) <= TOL, k
+    lhs = b["dw2"].double().sum(dim=1)
+    rhs = b["h"].double().t() @ b["dz"].double().sum(dim=1)
+    assert rel(lhs.cpu().numpy(), rhs.cpu().numpy()) <= TOL
