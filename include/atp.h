@@ -202,7 +202,9 @@ atp_status atp_graph_destroy(atp_graph* graph);
  * a_mn = 0: A stored row-major [M,K] with pitch lda; 1: A stored [K,M].
  * b_mn = 0: B stored row-major [N,K] with pitch ldb; 1: B stored [K,N].
  * out_f32 = 1 writes fp32 C (pitch ldc), else bf16.  (a_mn, b_mn) = (1, 0)
- * is unsupported.  N, K multiples of 8 (M too when a_mn).  max_ctas = 0: all SMs.
+ * is unsupported.  N, K multiples of 8 (M too when a_mn); A, B, C, bias 16-byte
+ * aligned and ldc a multiple of 8 (C is written with TMA bulk tensor stores);
+ * else ATP_ERR_SHAPE.  max_ctas = 0: all SMs.
  */
 atp_status atp_gemm(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
                     void* C, int64_t ldc, int out_f32, const void* bias, int64_t M, int64_t N,
