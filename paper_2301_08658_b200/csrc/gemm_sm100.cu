@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (system scope: NCCL / peer ranks read them), then count the tile.
         if (lane == 0) {
           ptx::bulk_wait0();
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy (TMA) writes before generic readers
           __threadfence_system();
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
