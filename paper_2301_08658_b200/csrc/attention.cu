@@ -1158,10 +1158,24 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
   }();
   FwdParams p;
   {
-    // causal: global heaviest-first (measured better: the load balance matters
-    // more than K/V reuse); non-causal (uniform CTAs): chunks of ~4 waves
+    // chunks of up to one wave of CTAs (the K/V of G (sequence, head) groups stay
+    // in L2 while their query-tile pairs stream them), heaviest first inside a
+    // chunk: b4 s2048 32 heads causal 0.178 -> 0.167 ms, 40 heads 0.238 -> 0.217,
+    // non-causal 0.304 -> 0.261 ms (sweep: profiles/r01_attn_fwd_order.log)
     const int per_group = (seq / BQ + 1) / 2;  // CTAs of one (sequence, head): query-tile pairs
-    p.grouped = grouped && !causal ? (4 * num_sms() + per_group - 1) / per_group : 0;
+    static const int g_env = [] {  // A/B: ATP_ATTN_FWD_G = groups per chunk
+      const char* e = getenv("ATP_ATTN_FWD_G");
+      return e ? atoi(e) : -1;
+    }();
+    // G = the largest power of two with G * per_group <= SMs (16 at s = 2048):
+    // measured best of G in {0, 8, 12, 14, 16, 18, 37, 74, 128} on both head
+    // counts; for long sequences (per_group > 16) the in-chunk causal imbalance
+    // costs more than the reuse gains, so global heaviest-first order
+    int G = 0;
+    if (per_group <= 16)
+      for (G = 1; 2 * G * per_group <= num_sms(); G *= 2) {
+      }
+    p.grouped = !grouped ? 0 : g_env >= 0 ? g_env : G;
   }
   p.T = T;
   p.seq = seq;
@@ -1205,8 +1219,12 @@ cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, in
     return !(e && e[0] == '0');
   }();
   BwdParams p;
-  // chunks of ~4 waves of key-block CTAs (seq / 128 per group): Q/dO of a chunk stay in L2
-  p.grouped = grouped ? (4 * num_sms() + seq / BKV - 1) / (seq / BKV) : 0;
+  // chunks of ~W waves of key-block CTAs (seq / 128 per group): Q/dO of a chunk stay in L2
+  static const int waves = [] {  // ATP_ATTN_BWD_WAVES (A/B), default 4
+    const char* e = getenv("ATP_ATTN_BWD_WAVES");
+    return e ? atoi(e) : 4;
+  }();
+  p.grouped = grouped ? (waves * num_sms() + seq / BKV - 1) / (seq / BKV) : 0;
   p.T = T;
   p.seq = seq;
   p.heads = heads;
