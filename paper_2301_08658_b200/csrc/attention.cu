@@ -1219,12 +1219,26 @@ cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, in
     return !(e && e[0] == '0');
   }();
   BwdParams p;
-  // chunks of ~W waves of key-block CTAs (seq / 128 per group): Q/dO of a chunk stay in L2
-  static const int waves = [] {  // ATP_ATTN_BWD_WAVES (A/B), default 4
-    const char* e = getenv("ATP_ATTN_BWD_WAVES");
-    return e ? atoi(e) : 4;
+  // chunks of G (sequence, head) groups of seq/128 key-block CTAs each, so the
+  // Q / dO / lse / D blocks of a chunk stay in L2: seq <= 2048, the largest power
+  // of two with G * CTAs-per-group <= SMs (like the forward); longer sequences
+  // ~4 waves of CTAs.  Sweep (G = 8..128, b4 s2048 / b1 s8192): G in 8..37 within
+  // 1% causal, G = 8 best non-causal (0.787 vs 0.811 ms at G = 37), 64+ worse.
+  static const int gb_env = [] {  // A/B: ATP_ATTN_BWD_G = groups per chunk
+    const char* e = getenv("ATP_ATTN_BWD_G");
+    return e ? atoi(e) : -1;
   }();
-  p.grouped = grouped ? (waves * num_sms() + seq / BKV - 1) / (seq / BKV) : 0;
+  {
+    const int per_group = seq / BKV;
+    int G = 0;
+    if (per_group <= 16) {
+      for (G = 1; 2 * G * per_group <= num_sms(); G *= 2) {
+      }
+    } else {
+      G = (4 * num_sms() + per_group - 1) / per_group;
+    }
+    p.grouped = !grouped ? 0 : gb_env >= 0 ? gb_env : G;
+  }
   p.T = T;
   p.seq = seq;
   p.heads = heads;
