@@ -39,3 +39,27 @@ def test_bench_json_contract_n1():
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] >= 1 and c["sample"]
     assert "workload" in d["config"]
+
+
+def test_bench_n2_shared_gpu():
+    """The N>1 bench path (torchrun, NCCL mesh from atp_search, chunk planner,
+    graph-captured step, max-over-ranks timing, one JSON line from rank 0) with
+    both ranks on the one GPU (--share-gpu: timings meaningless)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--share-gpu", "--steps", "3", "--warmup", "3", "--hidden", "1024",
+                          "--heads", "8", "--batch", "2", "--seq", "1024", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["mesh"] in ([2, 1], [1, 2])
+    assert d["search"]["chosen"] == d["config"]["mesh"] and "chunk_choice" in d
+    assert d["exposed_comm_ms"] >= 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
