@@ -263,17 +263,37 @@ __global__ void ln_param_part_kernel(const __nv_bfloat16* __restrict__ dy, int64
   reinterpret_cast<float4*>(pb)[1] = make_float4(sb[4], sb[5], sb[6], sb[7]);
 }
 
-__global__ void ln_param_final_kernel(const float* __restrict__ part, int64_t cols, float* __restrict__ dgamma,
-                                      float* __restrict__ dbeta) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (c >= cols) return;
+// Sum the kSegs partials per column: 32 columns x 8 segment groups per CTA
+// (coalesced 128-byte rows, 16 independent loads in flight per thread), then
+// the 8 group sums in a fixed order, so the result stays deterministic.
+constexpr int kFinCols = 32, kFinGroups = 8;
+__global__ void __launch_bounds__(kFinCols* kFinGroups) ln_param_final_kernel(const float* __restrict__ part,
+                                                                              int64_t cols, float* __restrict__ dgamma,
+                                                                              float* __restrict__ dbeta) {
+  __shared__ float red[2][kFinGroups][kFinCols];
+  const int lx = threadIdx.x % kFinCols, g = threadIdx.x / kFinCols;
+  const int64_t c = blockIdx.x * static_cast<int64_t>(kFinCols) + lx;
   float sg = 0.f, sb = 0.f;
-  for (int s = 0; s < kSegs; ++s) {
-    sg += part[s * cols + c];
-    sb += part[(kSegs + s) * cols + c];
+  if (c < cols) {
+#pragma unroll 16
+    for (int s = g; s < kSegs; s += kFinGroups) {
+      sg += part[s * cols + c];
+      sb += part[(kSegs + s) * cols + c];
+    }
   }
-  dgamma[c] = sg;
-  dbeta[c] = sb;
+  red[0][g][lx] = sg;
+  red[1][g][lx] = sb;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float tg = 0.f, tb = 0.f;
+#pragma unroll
+    for (int i = 0; i < kFinGroups; ++i) {
+      tg += red[0][i][lx];
+      tb += red[1][i][lx];
+    }
+    dgamma[c] = tg;
+    dbeta[c] = tb;
+  }
 }
 
 // [rows, p*w] (pitch ld) -> [p][rows][w]   (pack = 1), or back (pack = 0).
@@ -340,7 +360,7 @@ cudaError_t gpt_ew_launch(const EwDesc& e, cudaStream_t st) {
       ln_param_part_kernel<<<grid, 256, 0, st>>>(static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b),
                                                  e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
                                                  static_cast<const float*>(e.ws), part);
-      ln_param_final_kernel<<<static_cast<unsigned>((e.cols + 255) / 256), 256, 0, st>>>(
+      ln_param_final_kernel<<<static_cast<unsigned>((e.cols + kFinCols - 1) / kFinCols), kFinCols * kFinGroups, 0, st>>>(
           part, e.cols, static_cast<float*>(e.out), static_cast<float*>(e.res_out));
       break;
     }
