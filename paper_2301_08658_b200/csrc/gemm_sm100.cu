@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                       int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows, const uint32_t* gate,
-                      uint32_t gate_target, int group_m) {
+                      uint32_t gate_target, int group_m, int kserp) {
   using L = SmemLayout<CG, BN, STAGES>;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr int BNC = BN / CG;  // B rows loaded by this CTA
@@ -292,13 +292,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::wait_flag_geq(gate + chunk, gate_target);
           gated_chunk = chunk;
         }
+        // serpentine K: odd persistent rounds walk K backwards, so a round
+        // starts on the K-blocks the previous round (same A or B panels under
+        // the raster) touched last, which are still in L2
+        const bool k_rev = kserp && ((tile / n_units) & 1);
         for (int kb = 0; kb < num_k; ++kb) {
           ptx::mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sA = base + stage * L::kStageBytes;
           const uint32_t sB = sA + L::kABytes;
           const uint32_t fb = full_bar(stage);
           if (leader) ptx::mbar_arrive_expect_tx_w(fb, L::kStageBytes * CG);
-          const int k0 = kb * BK;
+          const int k0 = (k_rev ? num_k - 1 - kb : kb) * BK;
           auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1) {
             if constexpr (CG == 2) {
               ptx::tma_load_2d_cg2_w(dst, tm, fb, c0, c1);
@@ -533,6 +537,15 @@ bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int6
   return r == CUDA_SUCCESS;
 }
 
+// Serpentine K order across persistent rounds (ATP_KSERP=0 disables; A/B runs).
+int kserp() {
+  static const int v = [] {
+    const char* e = getenv("ATP_KSERP");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+
 template <int CG, int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   using L = SmemLayout<CG, BN, STAGES>;
@@ -562,7 +575,7 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = (pdl && d.pdl && d.gate == nullptr) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.tmC, d.tmC2, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate,
-                            d.gate_target, d.group_m > 0 ? d.group_m : 16);
+                            d.gate_target, d.group_m > 0 ? d.group_m : 16, kserp());
 }
 
 template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>
@@ -599,11 +612,13 @@ int gemm_mode() {
 }  // namespace
 
 // M-tiles per raster group (tiles sweep all N-tiles of a group before the next
-// group).  Default: the largest g <= 16 whose A panel (g M-tiles x K, bf16)
-// stays within ~40 MB of L2, so the group's A rows are read from HBM once
-// (256-row M-tiles: K = 16384 -> 4, 12288 -> 6, 8192 -> 9, <= 4096 -> 16).
-// ATP_GROUP_M=g > 0 fixes it (A/B runs:
-// profiles/r01_raster_ab.log; +0.8% step throughput over a fixed 16).
+// group).  Default: 16 when one M-tile's A panel (rows x K, bf16) is <= ~2 MB
+// (K <= 4096 at 256-row tiles), else 8: the ~74 tiles of a persistent round
+// then cover a near-square block of panels, and with the serpentine K order
+// consecutive rounds meet their shared panels in L2.  Measured per-GEMM DRAM
+// reads over g = 2..32 (profiles/r01_groupm_dram_sweep.log): 9.18 GB per
+// step vs 9.80 GB for the earlier rule (largest g whose panel group fits
+// ~40 MB of L2) and 9.57 GB for a fixed 16.  ATP_GROUP_M=g > 0 fixes it.
 int raster_group_m(int rows_per_mtile, int K) {
   static const int env = [] {
     const char* e = getenv("ATP_GROUP_M");
@@ -611,8 +626,7 @@ int raster_group_m(int rows_per_mtile, int K) {
   }();
   if (env > 0) return env;
   const double panel = static_cast<double>(rows_per_mtile) * K * 2.0;
-  int g = static_cast<int>(40e6 / panel);
-  return g < 1 ? 1 : (g > 16 ? 16 : g);
+  return panel <= 2.2e6 ? 16 : 8;
 }
 
 // Output map of the epilogue's TMA stores: [rows, cols] (pitch ld elements of
