@@ -68,6 +68,28 @@ def test_gemm_persistent_grid_caps(max_ctas):
     assert rel(C.cpu().numpy(), A.astype(np.float64) @ B.astype(np.float64).T) <= 1e-5
 
 
+@pytest.mark.parametrize("max_ctas", [2, 6, 10])
+@pytest.mark.parametrize("arr", ["fwd", "dx", "dw"])
+def test_gemm_serpentine_rounds_ragged_k(max_ctas, arr):
+    """Few CTAs -> many persistent rounds, so every other round of each CTA
+    walks K backwards (serpentine K) and starts on the ragged last K-block
+    (K = 200: three full 64-blocks + 8); fp32 output against the oracle."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    M, N, K = 520, 1032, 200
+    A, B, _ = _mats(M, N, K, 11)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    a_mn, b_mn = {"fwd": (False, True), "dx": (False, False), "dw": (True, True)}[arr]
+    At = torch.from_numpy(np.ascontiguousarray(A.T if a_mn else A)).cuda().to(torch.bfloat16)
+    Bt = torch.from_numpy(np.ascontiguousarray(B.T if b_mn else B)).cuda().to(torch.bfloat16)
+    C = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    atp.atp_gemm(At, Bt, C, a_mn=a_mn, b_mn=b_mn, max_ctas=max_ctas)
+    torch.cuda.synchronize()
+    got = C.cpu().numpy()
+    assert np.isfinite(got).all() and rel(got, ref) <= 1e-5
+
+
 def test_gemm_rejects_bad_shapes():
     import torch
     import paper_2301_08658_b200 as atp
