@@ -234,6 +234,131 @@ __global__ void ln_bwd_fused_kernel(const __nv_bfloat16* __restrict__ dy, int64_
   }
 }
 
+// d2 == 1, register-resident variant: one CTA of cols/16 threads per row
+// (grid-stride over rows), each thread holding 16 contiguous-in-chunks
+// columns of every operand, so each operand leaves HBM exactly once; the two
+// row sums go through a shared-memory table (double-buffered by row parity:
+// one __syncthreads per row) and every thread adds the warp partials in the
+// same order (deterministic).  Needs cols % 512 == 0 and cols <= 16384.
+constexpr int kRowV = 2;  // 8-column vectors per thread
+__device__ __forceinline__ void block_sum2(float& s, float& q, float (*red)[2][32], int par) {
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32, nw = blockDim.x / 32;
+  s = warp_sum(s);
+  q = warp_sum(q);
+  if (lane == 0) {
+    red[par][0][w] = s;
+    red[par][1][w] = q;
+  }
+  __syncthreads();
+  s = 0.f;
+  q = 0.f;
+  for (int i = 0; i < nw; ++i) {
+    s += red[par][0][i];
+    q += red[par][1][i];
+  }
+}
+
+__global__ void __launch_bounds__(1024) ln_fwd_row_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
+                                                          int64_t rows, int64_t cols,
+                                                          const __nv_bfloat16* __restrict__ gamma,
+                                                          const __nv_bfloat16* __restrict__ beta,
+                                                          __nv_bfloat16* __restrict__ y, int64_t ldy,
+                                                          float* __restrict__ saved) {
+  __shared__ float red[2][2][32];
+  const int64_t stride = 8 * static_cast<int64_t>(blockDim.x);
+  const int64_t c0 = 8 * static_cast<int64_t>(threadIdx.x);
+  F8 g[kRowV], b[kRowV];
+#pragma unroll
+  for (int v = 0; v < kRowV; ++v) {
+    g[v] = ld8(gamma + c0 + v * stride);
+    b[v] = ld8(beta + c0 + v * stride);
+  }
+  int par = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, par ^= 1) {
+    F8 xv[kRowV];
+    float s = 0.f, q = 0.f;
+#pragma unroll
+    for (int v = 0; v < kRowV; ++v) {
+      xv[v] = ld8(x + r * ldx + c0 + v * stride);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s += xv[v].v[i];
+        q += xv[v].v[i] * xv[v].v[i];
+      }
+    }
+    block_sum2(s, q, red, par);
+    const float mean = s / static_cast<float>(cols);
+    const float var = fmaxf(q / static_cast<float>(cols) - mean * mean, 0.f);
+    const float rstd = rsqrtf(var + kLnEps);
+#pragma unroll
+    for (int v = 0; v < kRowV; ++v) {
+      F8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o.v[i] = (xv[v].v[i] - mean) * rstd * g[v].v[i] + b[v].v[i];
+      st8(y + r * ldy + c0 + v * stride, o);
+    }
+    if (threadIdx.x == 0) {
+      saved[2 * r] = mean;
+      saved[2 * r + 1] = rstd;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) ln_bwd_row_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
+                                                          const __nv_bfloat16* __restrict__ x, int64_t ldx,
+                                                          int64_t rows, int64_t cols,
+                                                          const __nv_bfloat16* __restrict__ gamma,
+                                                          const float* __restrict__ saved,
+                                                          const __nv_bfloat16* res, int64_t ldres,
+                                                          __nv_bfloat16* out, int64_t ldo) {
+  __shared__ float red[2][2][32];
+  const int64_t stride = 8 * static_cast<int64_t>(blockDim.x);
+  const int64_t c0 = 8 * static_cast<int64_t>(threadIdx.x);
+  F8 g[kRowV];
+#pragma unroll
+  for (int v = 0; v < kRowV; ++v) g[v] = ld8(gamma + c0 + v * stride);
+  int par = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, par ^= 1) {
+    const float mean = saved[2 * r], rstd = saved[2 * r + 1];
+    F8 dg[kRowV], xh[kRowV];
+    float s = 0.f, q = 0.f;
+#pragma unroll
+    for (int v = 0; v < kRowV; ++v) {
+      const F8 d = ld8(dy + r * lddy + c0 + v * stride), xv = ld8(x + r * ldx + c0 + v * stride);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        dg[v].v[i] = d.v[i] * g[v].v[i];
+        xh[v].v[i] = (xv.v[i] - mean) * rstd;
+        s += dg[v].v[i];
+        q += dg[v].v[i] * xh[v].v[i];
+      }
+    }
+    block_sum2(s, q, red, par);
+    const float m1 = s / static_cast<float>(cols), m2 = q / static_cast<float>(cols);
+#pragma unroll
+    for (int v = 0; v < kRowV; ++v) {
+      const F8 rr = ld8(res + r * ldres + c0 + v * stride);
+      F8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o.v[i] = rr.v[i] + rstd * (dg[v].v[i] - m1 - xh[v].v[i] * m2);
+      st8(out + r * ldo + c0 + v * stride, o);
+    }
+  }
+}
+
+bool ln_row_ok(int64_t cols) {
+  static const bool on = [] {  // ATP_LN_ROW=0 keeps the warp-per-row kernels (A/B)
+    const char* e = getenv("ATP_LN_ROW");
+    return !(e && e[0] == '0');
+  }();
+  return on && cols % 512 == 0 && cols <= 16384;
+}
+unsigned ln_row_grid(int64_t rows, int64_t cols) {
+  const int64_t per_sm = 2048 / (cols / 16);  // resident CTAs per SM by threads
+  const int64_t cap = static_cast<int64_t>(num_sms()) * (per_sm > 0 ? per_sm : 1);
+  return static_cast<unsigned>(rows < cap ? (rows > 0 ? rows : 1) : cap);
+}
+
 // Partial column sums over row segment blockIdx.y: part[0][seg][c] = sum dy*xhat,
 // part[1][seg][c] = sum dy.  Eight columns per thread (16-byte loads, eight
 // independent accumulators); rows in order, so the sums are deterministic.
@@ -344,11 +469,24 @@ cudaError_t gpt_ew_launch(const EwDesc& e, cudaStream_t st) {
           static_cast<bf*>(e.out), ldo);
       break;
     case EW_LN_FWD:
+      if (ln_row_ok(e.cols)) {
+        ln_fwd_row_kernel<<<ln_row_grid(e.rows, e.cols), static_cast<unsigned>(e.cols / 16), 0, st>>>(
+            static_cast<const bf*>(e.a), lda, e.rows, e.cols, static_cast<const bf*>(e.b), static_cast<const bf*>(e.c),
+            static_cast<bf*>(e.out), ldo, static_cast<float*>(e.ws));
+        break;
+      }
       ln_fwd_fused_kernel<<<grid_for(e.rows), 256, 0, st>>>(
           static_cast<const bf*>(e.a), lda, e.rows, e.cols, static_cast<const bf*>(e.b), static_cast<const bf*>(e.c),
           static_cast<bf*>(e.out), ldo, static_cast<float*>(e.ws));
       break;
     case EW_LN_BWD:
+      if (ln_row_ok(e.cols)) {
+        ln_bwd_row_kernel<<<ln_row_grid(e.rows, e.cols), static_cast<unsigned>(e.cols / 16), 0, st>>>(
+            static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b), e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
+            static_cast<const bf*>(e.c), static_cast<const float*>(e.ws), static_cast<const bf*>(e.res),
+            e.ldres > 0 ? e.ldres : e.cols, static_cast<bf*>(e.out), ldo);
+        break;
+      }
       ln_bwd_fused_kernel<<<grid_for(e.rows), 256, 0, st>>>(
           static_cast<const bf*>(e.a), lda, static_cast<const bf*>(e.b), e.ldb > 0 ? e.ldb : e.cols, e.rows, e.cols,
           static_cast<const bf*>(e.c), static_cast<const float*>(e.ws), static_cast<const bf*>(e.res),
