@@ -96,6 +96,21 @@ def test_gpt_layer_matches_oracle(d1, d2, chunks):
                 assert bool((bufs[r][name] == ref).all()), (name, r)
 
 
+@pytest.mark.parametrize("h,heads,d1", [(1536, 12, 1), (1536, 12, 2), (640, 5, 1)])
+def test_gpt_layer_layernorm_widths(h, heads, d1):
+    """d2 = 1 LayerNorm paths at other widths: the register-resident row
+    kernels with 96 threads per row (h = 1536) and the warp-per-row fallback
+    (h = 640, not a multiple of 512)."""
+    T, F, seq = 512, 2 * h, 256
+    g, fw, bw = _oracle(T, h, F, heads, seq, 37)
+    bufs = run_gpt(d1, 1, 1, T, h, F, heads, seq, 37)
+    for r, b in enumerate(bufs):
+        for name in NAMES:
+            got = b[name].float().cpu().numpy()
+            exp = _expected(name, fw, bw, d1, 1, r, h, F)
+            assert rel(got.reshape(exp.shape), exp) < TOL, (name, r)
+
+
 def test_gpt_layer_noncausal_and_long_sequence():
     T, h, F, heads, seq = 1024, 512, 2048, 4, 512
     g, fw, bw = _oracle(T, h, F, heads, seq, 5, causal=False)
