@@ -56,6 +56,32 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Blackwell paired fp32 ops (FFMA2 / FADD2: two lanes of fp32 per instruction)
+// and the three-input max (FMNMX3), to halve the softmax's FMA/ALU issue.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -457,8 +483,9 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(u[i / 32][i % 32]);
 #pragma unroll
-      for (int c = 8; c < BKV; ++c) mx[c % 8] = fmaxf(mx[c % 8], __uint_as_float(u[c / 32][c % 32]));
-      float mb = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      for (int c = 8; c < BKV; c += 2)
+        mx[(c / 2) % 8] = fmax3(mx[(c / 2) % 8], __uint_as_float(u[c / 32][c % 32]), __uint_as_float(u[c / 32][c % 32 + 1]));
+      float mb = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
       mb *= p.scale_log2;
       // Lazy rescale (warp-uniform: tcgen05.ld/st are warp-collective).  P is
       // written with the new max first; O is corrected afterwards, once the
@@ -471,20 +498,26 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
         f = ex2(m_run - m_new);
         m_run = m_new;
       }
-      float rsv[4] = {0.f, 0.f, 0.f, 0.f};  // four partial row sums (short dependency chains)
+      // x = s * scale - m and the row sums on pairs of columns (FFMA2 / FADD2)
+      const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2), nm2 = f2pack(-m_run, -m_run);
+      uint64_t rsv[2] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f)};  // 2 x 2 partial row sums
 #pragma unroll
       for (int c = 0; c < BKV / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float e0 = ex2(fmaf(__uint_as_float(u[c][2 * i]), p.scale_log2, -m_run));
-          const float e1 = ex2(fmaf(__uint_as_float(u[c][2 * i + 1]), p.scale_log2, -m_run));
-          rsv[i % 4] += e0 + e1;
+          float x0, x1;
+          f2unpack(ffma2(f2pack(__uint_as_float(u[c][2 * i]), __uint_as_float(u[c][2 * i + 1])), sc2, nm2), x0, x1);
+          const float e0 = ex2(x0), e1 = ex2(x1);
+          rsv[i % 2] = fadd2(rsv[i % 2], f2pack(e0, e1));
           pk[i] = pack_bf16(e0, e1);
         }
         ptx::tmem_st_32x32b_x16(tS + c * 16, pk);  // P (bf16 pairs) over the S columns
       }
-      const float rs = (rsv[0] + rsv[1]) + (rsv[2] + rsv[3]);
+      float ra, rb, rc, rd;
+      f2unpack(rsv[0], ra, rb);
+      f2unpack(rsv[1], rc, rd);
+      const float rs = (ra + rb) + (rc + rd);
       l = l * f + rs;
       if (rescale && j > 0) {
 #pragma unroll
