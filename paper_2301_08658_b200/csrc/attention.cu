@@ -76,6 +76,16 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -1013,17 +1023,27 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
       const int qpos0 = i * BQ2 + c0;  // query position of column c0
       const bool need_mask = p.causal && qpos0 < key;  // some column of this thread is masked (q < key)
       uint32_t pk[16], dk[16];
+      // pairs of query columns on paired fp32 ops (FMUL2 / FFMA2 / FSUB2)
+      const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2);
+      const uint64_t nlog2e = f2pack(-1.4426950408889634f, -1.4426950408889634f);
 #pragma unroll
       for (int k = 0; k < 32; k += 2) {
-        float pv[2], ds[2];
+        const float2 l2 = *reinterpret_cast<const float2*>(lse_s + c0 + k);
+        const float2 d2 = *reinterpret_cast<const float2*>(D_s + c0 + k);
+        float x0, x1;
+        f2unpack(ffma2(f2pack(__uint_as_float(su[k]), __uint_as_float(su[k + 1])), sc2,
+                       fmul2(f2pack(l2.x, l2.y), nlog2e)),
+                 x0, x1);
+        float pv[2] = {ex2(x0), ex2(x1)};
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const float e = ex2(fmaf(__uint_as_float(su[k + u]), p.scale_log2, -lse_s[c0 + k + u] * 1.4426950408889634f));
-          pv[u] = (need_mask && qpos0 + k + u < key) ? 0.f : e;
-          ds[u] = pv[u] * (__uint_as_float(du[k + u]) - D_s[c0 + k + u]);
-        }
+        for (int u = 0; u < 2; ++u)
+          if (need_mask && qpos0 + k + u < key) pv[u] = 0.f;
+        const uint64_t pp = f2pack(pv[0], pv[1]);
+        float ds0, ds1;
+        f2unpack(fmul2(pp, fsub2(f2pack(__uint_as_float(du[k]), __uint_as_float(du[k + 1])), f2pack(d2.x, d2.y))), ds0,
+                 ds1);
         pk[k / 2] = pack_bf16(pv[0], pv[1]);
-        dk[k / 2] = pack_bf16(ds[0], ds[1]);
+        dk[k / 2] = pack_bf16(ds0, ds1);
       }
       ptx::tmem_st_32x32b_x16(tS(s) + lane_off + c0, pk);   // P^T over this thread's own S^T columns
       ptx::tmem_st_32x32b_x16(tdP(s) + lane_off + c0, dk);  // dS^T over its own dP^T columns (A of dK)
