@@ -74,7 +74,7 @@ cudaError_t gemm_launch_f32(const GemmDesc& d, cudaStream_t st);
 void gemm_plan_tile(int M, int N, int* bn, int* cg);
 int gemm_tiles(const GemmDesc& d);
 int num_sms();
-int raster_group_m(int rows_per_mtile, int K);
+int raster_group_m(int rows_per_mtile, int N, int K);
 // 2-D bf16 TMA map over a row-major [rows, cols] matrix (pitch ld elements),
 // box [box_rows, box_cols], 128B swizzle, out-of-bounds reads as zero.
 bool tmap_bf16_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,

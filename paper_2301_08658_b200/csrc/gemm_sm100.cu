@@ -612,19 +612,23 @@ int gemm_mode() {
 }  // namespace
 
 // M-tiles per raster group (tiles sweep all N-tiles of a group before the next
-// group).  Default: 16 when one M-tile's A panel (rows x K, bf16) is <= ~2 MB
-// (K <= 4096 at 256-row tiles), else 8: the ~74 tiles of a persistent round
-// then cover a near-square block of panels, and with the serpentine K order
-// consecutive rounds meet their shared panels in L2.  Measured per-GEMM DRAM
-// reads over g = 2..32 (profiles/r01_groupm_dram_sweep.log): 9.18 GB per
-// step vs 9.80 GB for the earlier rule (largest g whose panel group fits
-// ~40 MB of L2) and 9.57 GB for a fixed 16.  ATP_GROUP_M=g > 0 fixes it.
-int raster_group_m(int rows_per_mtile, int K) {
+// group).  Default: when the whole B operand (N x K, bf16) fits ~72 MB of L2,
+// 2 — every round sweeps all of B, which then stays L2-resident while A
+// streams through once; otherwise 16 when one M-tile's A panel (rows x K) is
+// <= ~2 MB (K <= 4096 at 256-row tiles), else 8: the ~74 tiles of a
+// persistent round then cover a near-square block of panels, and with the
+// serpentine K order consecutive rounds meet their shared panels in L2.
+// Measured per-GEMM DRAM reads over g = 2..32
+// (profiles/r01_groupm_dram_sweep.log): 8.97 GB per step predicted vs 9.80 GB
+// for the earlier rule (largest g whose panel group fits ~40 MB of L2) and
+// 9.57 GB for a fixed 16.  ATP_GROUP_M=g > 0 fixes it.
+int raster_group_m(int rows_per_mtile, int N, int K) {
   static const int env = [] {
     const char* e = getenv("ATP_GROUP_M");
     return e ? atoi(e) : -1;
   }();
   if (env > 0) return env;
+  if (static_cast<double>(N) * K * 2.0 <= 72e6) return 2;
   const double panel = static_cast<double>(rows_per_mtile) * K * 2.0;
   return panel <= 2.2e6 ? 16 : 8;
 }
@@ -696,7 +700,7 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
   d.a_mn = a_mn;
   d.b_mn = b_mn;
   if (d.bn != 128 && d.bn != 256) gemm_plan_tile(M, N, &d.bn, &d.cg);
-  d.group_m = raster_group_m(d.cg == 2 ? 256 : BM, K);
+  d.group_m = raster_group_m(d.cg == 2 ? 256 : BM, N, K);
   if (d.cg != 1 && d.cg != 2) d.cg = (d.bn == 256 && M >= 256 && gemm_mode() != 1) ? 2 : 1;
   if (d.cg == 2 && d.bn != 256) d.cg = 1;
   bool ok;
