@@ -7,12 +7,25 @@ One step = one GPT layer's linear block forward + backward on DeviceMesh(d1, d2)
 (F3..F12, B1..B6 of SURVEY.md §8(a)) through libatp's C ABI.  Prints ONE JSON
 line on rank 0.  Timing: W untimed warm-up steps, then K steps bracketed by
 barrier + cudaDeviceSynchronize, CUDA events on the launching stream, max over
-ranks.  The working set (weights 0.4 GB + activations > 1 GB at h=4096) is far
-larger than the 126 MB L2, so no explicit flush is done (stated in `config`).
+ranks.  The working set (weights + activations, GBs) is far larger than the
+126 MB L2, so no explicit flush is done (stated in `config`).
+
+Workload per N (BASELINE.json configs; override with --hidden/--heads):
+  N = 1      cfg 5 shape h=12288, a=96 (the largest single-GPU configuration)
+  N = 2, 4   cfg 2, h=4096, a=32
+  N = 8      cfg 4, h=5120, a=40 (the north_star target) on the atp_search mesh
+All: b=4, s=2048 (T=8192 tokens), F=4h, bf16.
+
+At N > 1 (default) the HCM probe (atp_probe_hcm, §3.4 / P:482) runs first: its
+calibrated bandwidths feed atp_search (the mesh) and its bus bandwidth feeds the
+chunk planner (atp_plan_chunks, §4.1), together with the measured compute-side
+time of each candidate chunk count.
 
 Extra passes after the timed region (reported, never mixed into `value`):
   * comm-disabled twin  -> exposed_comm_ms = t - t(no all-reduce)       (N > 1)
-  * profiled pass       -> per-kernel-class CUDA-event durations -> roofline
+  * Megatron-style baseline: the same library at DeviceMesh(N,1), 1 chunk (N > 1)
+  * CUPTI kernel trace of the same graph-launched step -> roofline (GEMM time
+    and share of the step), cross-checked by per-launch CUDA events
   * e2e pass            -> same step through the public API with the step's
                            inputs (X, dZ) copied H2D from pinned memory and its
                            result (the bias gradients) read D2H each step
@@ -32,32 +45,49 @@ import time
 # P:345 sets CUDA_DEVICE_MAX_CONNECTIONS=1 so that, in ONE hardware work queue, a
 # communication kernel enqueued before the next GEMM is launched first.  This
 # library's schedule instead gives the communication stream its own queue (high
-# priority, gated by device-side chunk counters) and caps the GEMM CTAs; with a
-# single queue the dW GEMM queued behind the dX GEMM would block the chunk
-# all-reduces (head-of-line), so the default connection count is kept
-# (DESIGN.md §6-7).  An explicit setting in the environment is respected.
+# priority, gated by device-side chunk counters); with a single queue the dW
+# GEMM queued behind the dX GEMM would block the chunk all-reduces
+# (head-of-line), so the default connection count is kept.
+# An explicit setting in the environment is respected.
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "TFLOP/s/GPU and exposed-comm ms per GPT layer fwd+bwd at 1/2/4/8 B200 per mesh"
+VALUE_SCOPE = "whole job: linear-block FLOPs of all N GPUs / step time (per GPU: tflops_per_gpu)"
+
+
+def default_shape(world: int) -> tuple[int, int, str]:
+    """(hidden, heads, BASELINE config) bench.py runs at N GPUs by default."""
+    if world == 1:
+        return 12288, 96, "cfg 5 shape (largest single-GPU configuration)"
+    if world == 8:
+        return 5120, 40, "cfg 4 (north_star target)"
+    return 4096, 32, "cfg 2"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="atp", choices=["atp", "reference"])
-    p.add_argument("--hidden", type=int, default=4096)
-    p.add_argument("--heads", type=int, default=32)
+    p.add_argument("--hidden", type=int, default=0, help="0 = the per-N default (see the module docstring)")
+    p.add_argument("--heads", type=int, default=0)
     p.add_argument("--ffn", type=int, default=0, help="default 4*hidden")
     p.add_argument("--batch", type=int, default=4)
     p.add_argument("--seq", type=int, default=2048)
     p.add_argument("--layer", default="linear", choices=["linear", "gpt"],
                    help="linear: the north_star linear block (default); gpt: the full pre-LN layer "
                         "(LayerNorm + causal softmax attention core, SURVEY NEXT #1)")
-    p.add_argument("--mesh", default="", help="d1xd2; default: atp_search (uniform NVSwitch HCM, or --probe)")
+    p.add_argument("--mesh", default="", help="d1xd2; default: atp_search on the probed HCM + calibration")
+    p.add_argument("--no-probe", action="store_true",
+                   help="N>1: skip atp_probe_hcm; search on the uniform 900 GB/s NVSwitch HCM, plan at --busbw")
+    p.add_argument("--probe-mib", type=int, default=256, help="largest probe message (MiB); 64 MiB and the "
+                   "layer's chunk size are also measured")
+    p.add_argument("--p2p-disable", action="store_true",
+                   help="N>1 topology stress (P:373, the paper's IC1): NCCL_P2P_DISABLE=1 before NCCL init, "
+                        "then probe -> calibrated search as usual")
     p.add_argument("--fused-ar", action="store_true",
                    help="N>1: fused peer-memory all-reduce (CUDA IPC) instead of NCCL on the data path")
     p.add_argument("--nccl-only", action="store_true",
@@ -66,16 +96,14 @@ def parse():
                    help="N>1 linear block: also time the fused peer-memory all-reduce (± gating) against NCCL "
                         "(± gating) and run the fastest")
     p.add_argument("--try-gated", action="store_true",
-                   help="N>1 linear block: also time NCCL with chunk gating and run the faster "
-                        "(default: the plain NCCL step, no selection)")
+                   help="N>1 linear block: also time NCCL with chunk gating and run the faster")
     p.add_argument("--gated", action="store_true",
                    help="N>1: chunk-gated GEMMs (the next stage's GEMM waits per chunk for the all-reduce tail)")
-    p.add_argument("--probe", action="store_true",
-                   help="N>1: measure the HCM + per-mesh calibration with atp_probe_hcm and search on that")
+    p.add_argument("--no-baseline", action="store_true", help="N>1: skip the DeviceMesh(N,1) c=1 baseline")
     p.add_argument("--chunks", type=int, default=0,
-                   help="0 = 1 at N=1; at N>1 chosen by the overlap model from measured compute (planner.py)")
+                   help="0 = 1 at N=1; at N>1 chosen by atp_plan_chunks from measured compute + probed busBW")
     p.add_argument("--busbw", type=float, default=725.0,
-                   help="all-reduce bus GB/s for the chunk planner (8-rank NCCL on this pool, B200_PROFILING.md)")
+                   help="all-reduce bus GB/s for the chunk planner when the probe does not run")
     p.add_argument("--gemm-ctas", type=int, default=-1, help="GEMM CTA cap (default: all SMs at N=1, SMs-16 else)")
     p.add_argument("--share-gpu", action="store_true",
                    help="TEST ONLY: N>1 ranks share cuda:0 (distinct NCCL_HOSTID per rank, NCCL over sockets); "
@@ -85,9 +113,11 @@ def parse():
     p.add_argument("--seed", type=int, default=2301)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-cupti", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-oracle sample duration")
     p.add_argument("--peaks", default=os.path.join(ROOT, "MEASURED_PEAKS.json"))
-    return p.parse_args()
+    a = p.parse_args()
+    return a
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -129,7 +159,7 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons, n = [], [], set(), 0
+        sm, mx, pw, reasons, n = [], [], [], set(), 0
         for (tw, line) in self.lines:
             if not (t0 - 0.15 <= tw <= t1 + 0.15):
                 continue
@@ -139,6 +169,7 @@ class ClockSampler:
             try:
                 sm.append(float(parts[1]))
                 mx.append(float(parts[2]))
+                pw.append(float(parts[3]))
             except ValueError:
                 continue
             n += 1
@@ -146,7 +177,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": n}
+                "reasons": sorted(reasons), "samples": n, "power_w_max": max(pw) if pw else None}
 
 
 def peaks(path: str) -> dict:
@@ -154,60 +185,66 @@ def peaks(path: str) -> dict:
         with open(path) as f:
             p = json.load(f)
         return {"bf16_tflops": p["bf16_tflops"], "bf16_tflops_sustained": p.get("bf16_tflops_sustained"),
-                "hbm_gbs": p["hbm_gbs"], "source": "measured"}
+                "hbm_gbs": p["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
     except (OSError, KeyError, ValueError):
         # /opt/skills/guides/B200_PROFILING.md fallback
-        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+                "source": "fallback (B200_PROFILING.md)"}
 
 
-def cpu_oracle_run(T_s: int, h: int, F: int, heads: int, seed: int, g_full=None):
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        return os.cpu_count()
+
+
+def oracle_weights(h: int, F: int, seed: int) -> dict:
+    """The layer's global weights and biases in float64 (generated once, not timed)."""
+    import numpy as np
+    import datagen
+
+    shapes = datagen.layer_shapes(8, h, F)
+    return {k: datagen.tensor(k, s, seed=seed).astype(np.float64) for k, s in shapes.items() if k not in ("x", "dz")}
+
+
+def cpu_oracle_run(w: dict, T_s: int, h: int, heads: int, seed: int) -> float:
     """Time the CPU oracle (fp64 NumPy SPMD simulation at mesh (1,1)) on T_s tokens."""
     import numpy as np
     import datagen
     from oracle import layer as olayer
 
-    if g_full is None:
-        g_full = {k: datagen.tensor(k, s, seed=seed, rows=(np.arange(T_s) if k in ("x", "dz") else None))
-                  for k, s in datagen.layer_shapes(T_s, h, F).items()}
-    g = {k: v.astype(np.float64) for k, v in g_full.items()}
+    g = dict(w, x=datagen.tensor("x", (T_s, h), seed=seed).astype(np.float64),
+             dz=datagen.tensor("dz", (T_s, h), seed=seed).astype(np.float64))
     t0 = time.perf_counter()
     olayer.run_layer(g, 1, 1, heads, 1)
     return time.perf_counter() - t0
 
 
+def sample_tokens(w, h, heads, seed, target_s: float) -> tuple[int, float, float]:
+    """Token count whose oracle run takes ~target_s (the time is affine in the
+    tokens: fixed weight copies + per-token GEMMs); two calibration points."""
+    t_a = cpu_oracle_run(w, 16, h, heads, seed)
+    t_b = cpu_oracle_run(w, 80, h, heads, seed)
+    per_tok = max((t_b - t_a) / 64.0, 1e-6)
+    fixed = max(t_a - 16 * per_tok, 0.0)
+    T_s = int(max(16, min(8192, (target_s - fixed) / per_tok)) // 8 * 8)
+    return T_s, fixed, per_tok
+
+
 def cpu_baseline(h: int, F: int, heads: int, seed: int, target_s: float) -> dict:
-    import numpy as np
-    import datagen
-
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
-    except Exception:  # noqa: BLE001
-        threads = os.cpu_count()
-    # weights once (not timed), then a short calibration sample and the bounded sample
-    shapes = datagen.layer_shapes(8, h, F)
-    g = {k: datagen.tensor(k, s, seed=seed) for k, s in shapes.items() if k not in ("x", "dz")}
-
-    def with_rows(n):
-        gg = dict(g)
-        gg["x"] = datagen.tensor("x", (n, h), seed=seed)
-        gg["dz"] = datagen.tensor("dz", (n, h), seed=seed)
-        return gg
-
-    # the oracle's time is affine in the token count (fixed weight copies + per-token GEMMs):
-    # two calibration points, then the sample that lands near target_s
-    t_a = cpu_oracle_run(64, h, F, heads, seed, with_rows(64))
-    t_b = cpu_oracle_run(256, h, F, heads, seed, with_rows(256))
-    per_tok = max((t_b - t_a) / 192.0, 1e-6)
-    T_s = int(max(64, min(8192, (target_s - max(t_a - 64 * per_tok, 0.0)) / per_tok)) // 8 * 8)
-    t = cpu_oracle_run(T_s, h, F, heads, seed, with_rows(T_s))
+    w = oracle_weights(h, F, seed)
+    T_s, _, _ = sample_tokens(w, h, heads, seed, target_s)
+    t = cpu_oracle_run(w, T_s, h, heads, seed)
     fl = layer_flops(T_s, h, F)
-    return {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": f"{T_s} of {8192} tokens of the same layer (h={h}, F={F}), fp64 NumPy SPMD simulation at "
-                      f"DeviceMesh(1,1), {t:.1f} s", "seconds": t, "tokens": T_s}
+    return {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{T_s} of 8192 tokens of the same layer (h={h}, F={F}), fp64 NumPy SPMD simulation at "
+                      f"DeviceMesh(1,1) incl. its per-call weight shard copies, {t:.1f} s",
+            "seconds": t, "tokens": T_s}
 
 
-def traffic_for(peaks_path: str, h: int, T: int):
+def traffic_for(h: int, T: int):
     """Measured DRAM bytes (read + write) per GEMM launch of this workload's step,
     from the committed ncu --set full capture (profiles/*_gemm_traffic.json,
     written by scripts/ncu_traffic.py); None when there is none for (h, T)."""
@@ -243,19 +280,14 @@ def cpu_baseline_gpt(h: int, F: int, heads: int, seq: int, seed: int) -> dict:
     import datagen
     from oracle import gpt
 
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
-    except Exception:  # noqa: BLE001
-        threads = os.cpu_count()
     g = {k: v.astype("float64") for k, v in datagen.gpt_globals(seq, h, F, seed).items()}
     t0 = time.time()
     fw = gpt.dense_forward(g, heads, seq)
     gpt.dense_backward(g, fw, g["dz"], heads, seq)
     t = time.time() - t0
-    return {"value": gpt_flops(seq, h, F, seq) / t / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": f"1 sequence ({seq} tokens) of the full layer (h={h}, F={F}, {heads} heads, causal), "
-                      f"fp64 NumPy dense oracle, {t:.1f} s", "seconds": t, "tokens": seq}
+    return {"value": gpt_flops(seq, h, F, seq) / t / 1e12, "unit": "TFLOP/s", "cores": blas_threads(),
+            "kind": "oracle", "sample": f"1 sequence ({seq} tokens) of the full layer (h={h}, F={F}, {heads} heads, "
+                                        f"causal), fp64 NumPy dense oracle, {t:.1f} s", "seconds": t, "tokens": seq}
 
 
 def _quiet(fn):
@@ -276,43 +308,84 @@ def emit(obj: dict) -> None:
     print(json.dumps(obj), flush=True)
 
 
+def union_ms(iv) -> float:
+    """Length (ms) of the union of [start_ns, end_ns) intervals."""
+    tot, cur_s, cur_e = 0, None, None
+    for s, e in sorted(iv):
+        if cur_e is None or s > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    if cur_e is not None:
+        tot += cur_e - cur_s
+    return tot / 1e6
+
+
+def cupti_kernels(run, stream, n: int):
+    """Kernel records (name, start_ns, end_ns) of n launches of `run` (the
+    graph-launched step) from a CUPTI activity trace (torch.profiler/kineto).
+    Every record is a kernel of the step as it executes inside the graph."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(n):
+            run(stream)
+        torch.cuda.synchronize()
+    out = []
+    for e in prof.profiler.kineto_results.events():
+        if e.device_type() != torch.autograd.DeviceType.CUDA:
+            continue
+        nm = e.name()
+        if nm.startswith("Memcpy") or nm.startswith("Memset") or "cudaStream" in nm:
+            continue
+        out.append((nm, e.start_ns(), e.end_ns()))
+    return out
+
+
+def kernel_class(name: str) -> str:
+    if "gemm_sm100" in name or "gemm_f32" in name:
+        return "gemm"
+    if "attn" in name:
+        return "attention"
+    if "nccl" in name.lower():
+        return "nccl"
+    return "elementwise"
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(a) -> None:
     """The CPU oracle, as it stands, timed on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    h = a.hidden
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    dh, dheads, cfg = default_shape(world)
+    h = a.hidden or dh
+    heads = a.heads or dheads
     F = a.ffn or 4 * h
-    heads = a.heads
-    import numpy as np
-    import datagen
-
-    shapes = datagen.layer_shapes(8, h, F)
-    g = {k: datagen.tensor(k, s, seed=a.seed) for k, s in shapes.items() if k not in ("x", "dz")}
+    w = oracle_weights(h, F, a.seed)
     # one bounded sample per step, sized so the whole run stays within a few minutes
-    t_cal = cpu_oracle_run(64, h, F, heads, a.seed, dict(g, x=datagen.tensor("x", (64, h), seed=a.seed),
-                                                           dz=datagen.tensor("dz", (64, h), seed=a.seed)))
     budget = 150.0 / max(1, a.steps + a.warmup)
-    T_s = int(max(8, min(8192, budget / max(t_cal, 1e-3) * 64)) // 8 * 8)
-    gg = dict(g, x=datagen.tensor("x", (T_s, h), seed=a.seed), dz=datagen.tensor("dz", (T_s, h), seed=a.seed))
+    T_s, fixed, per_tok = sample_tokens(w, h, heads, a.seed, budget)
     for _ in range(a.warmup):
-        cpu_oracle_run(T_s, h, F, heads, a.seed, gg)
-    times = [cpu_oracle_run(T_s, h, F, heads, a.seed, gg) for _ in range(a.steps)]
+        cpu_oracle_run(w, T_s, h, heads, a.seed)
+    times = [cpu_oracle_run(w, T_s, h, heads, a.seed) for _ in range(a.steps)]
     t = sum(times) / len(times)
     v = layer_flops(T_s, h, F) / t / 1e12
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
-    except Exception:  # noqa: BLE001
-        threads = os.cpu_count()
+    threads = blas_threads()
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
           "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-          "config": {"workload": f"gpt-layer linear block h{h} a{heads} ffn{F}, {T_s}-token sample per step "
-                                 f"(of b{a.batch} s{a.seq})", "mesh": [1, 1], "tokens_per_step": T_s},
+          "config": {"workload": f"gpt-layer linear block h{h} a{heads} ffn{F} ({cfg}), {T_s}-token sample per step "
+                                 f"(of b{a.batch} s{a.seq})", "mesh": [1, 1], "tokens_per_step": T_s,
+                     "hidden": h, "heads": heads, "ffn": F},
           "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-                           "sample": f"{T_s} tokens per step, fp64 NumPy SPMD simulation"},
+                           "sample": f"{T_s} tokens per step, fp64 NumPy SPMD simulation at DeviceMesh(1,1) "
+                                     f"(fixed per-call cost ~{fixed:.1f} s: weight shard copies)"},
           "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
           "gpu_launches": 0})
 
@@ -324,90 +397,93 @@ def main() -> None:
         run_reference(a)
         return
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    if a.p2p_disable:
+        os.environ["NCCL_P2P_DISABLE"] = "1"  # read by NCCL at communicator init (IC1)
+    if a.share_gpu:
+        os.environ["NCCL_HOSTID"] = f"atp-shared-gpu-rank{rank}"  # NCCL rejects two ranks on one device of one host
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        local_rank = 0
+
     import torch
     import torch.distributed as dist
 
     import paper_2301_08658_b200 as atp
     from paper_2301_08658_b200 import _abi
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != a.gpus:
-        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
-    if a.share_gpu:
-        os.environ["NCCL_HOSTID"] = f"atp-shared-gpu-rank{rank}"  # NCCL rejects two ranks on one device of one host
-        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
-        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         _quiet(lambda: dist.init_process_group("nccl", device_id=dev))  # eager NCCL init prints its banner
 
-    h, heads = a.hidden, a.heads
+    dh, dheads, cfg_name = default_shape(world)
+    h = a.hidden or dh
+    heads = a.heads or dheads
+    if a.hidden and not a.heads:
+        heads = max(1, h // 128)
     F = a.ffn or 4 * h
     T = a.batch * a.seq
-    chunks = a.chunks or (1 if world == 1 else 4)  # N>1 with --chunks 0: replaced by the planner below
+    gpt_mode = a.layer == "gpt"
 
-    # ---- mesh: explicit, or ATP's search (§3.5) on the single-layer NVSwitch HCM
-    # (P:488, 900 GB/s per direction), or with --probe on the HCM measured by
-    # atp_probe_hcm (S1) plus the per-mesh calibration.
-    plan = None
-    mesh_source = "flag" if a.mesh else ("N=1" if world == 1 else "")
-    uid = atp.atp_get_unique_id() if rank == 0 else bytes(128)
-    if world > 1:
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-    if a.mesh:
-        d1, d2 = (int(v) for v in a.mesh.lower().split("x"))
-    elif world == 1:
-        d1, d2 = 1, 1
-    else:
-        layers, calib = [atp.HcmLayer(world, 900.0, 900.0)], None
-        mesh_source = "atp_search(uniform 900 GB/s HCM)"
-        if a.probe:
-            try:
-                pm = _quiet(lambda: atp.Mesh.distributed(world, 1, rank, uid, local_rank))
-                scratch = torch.empty((64 << 20) + 64, dtype=torch.bfloat16, device=dev)
-                chunk_bytes = 2 * (T // chunks) * (4 * h // max(1, world // 2))
-                layers, _, calib = atp.atp_probe_hcm(pm, scratch, msg_bytes=(64 << 20, max(1 << 20, chunk_bytes)),
-                                                    calib_bytes=max(1 << 20, chunk_bytes), iters=5)
-                pm.destroy()
-                del scratch
-                mesh_source = "atp_search(probed HCM + calibration)"
-            except Exception as e:  # noqa: BLE001
-                print(f"probe failed, using the uniform HCM: {e}", file=sys.stderr)
-            # fresh unique id for the layer mesh
-            uid = atp.atp_get_unique_id() if rank == 0 else bytes(128)
+    def new_uid() -> bytes:
+        uid = atp.atp_get_unique_id() if rank == 0 else bytes(128)
+        if world > 1:
             obj = [uid]
             dist.broadcast_object_list(obj, src=0)
             uid = obj[0]
-        plan = atp.atp_search(layers, 1, a.batch, a.seq, h, heads, 2, calibration=calib)
+        return uid
+
+    # ---- mesh: explicit, or ATP's search (§3.5) on the HCM measured by
+    # atp_probe_hcm (S1) with the per-mesh calibration, or with
+    # --no-probe on the single-layer NVSwitch HCM (P:488, 900 GB/s per direction).
+    plan = plan_hcm = None
+    probe = None
+    mesh_source = "flag" if a.mesh else ("N=1" if world == 1 else "")
+    busbw, busbw_source = a.busbw, "--busbw"
+    if world > 1 and not a.mesh:
+        layers, calib = [atp.HcmLayer(world, 900.0, 900.0)], None
+        mesh_source = "atp_search(uniform 900 GB/s HCM)"
+        if not a.no_probe:
+            try:
+                pm = _quiet(lambda: atp.Mesh.distributed(world, 1, rank, new_uid(), local_rank))
+                chunk_bytes = 2 * (T // 4) * (4 * h // max(1, world // 2))
+                big = a.probe_mib << 20
+                sizes = tuple(sorted({min(64 << 20, big), big, chunk_bytes}))
+                scratch = torch.empty(max(big, chunk_bytes) + 64, dtype=torch.uint8, device=dev)
+                t0 = time.time()
+                layers, matrix, calib = atp.atp_probe_hcm(pm, scratch, msg_bytes=sizes, calib_bytes=chunk_bytes,
+                                                          iters=10)
+                pm.destroy()
+                del scratch
+                probe = {"hcm": [vars(l) for l in layers], "p2p_matrix_gbps": matrix,
+                         "calibration_algbw_gbps": {f"{d1}x{d2}": v for (d1, d2), v in calib.items()},
+                         "msg_bytes": list(sizes), "calib_bytes": chunk_bytes, "seconds": time.time() - t0,
+                         "nccl_p2p_disable": bool(a.p2p_disable)}
+                busbw, busbw_source = layers[0].group_gbps, f"probe: {world}-rank all-reduce busBW (GroupBW)"
+                mesh_source = "atp_search(probed HCM + calibration, P:482)"
+            except Exception as e:  # noqa: BLE001
+                print(f"probe failed, using the uniform HCM: {e}", file=sys.stderr)
+                probe = {"error": str(e)}
+        plan_hcm = atp.atp_search(layers, 1, a.batch, a.seq, h, heads, 2)
+        plan = atp.atp_search(layers, 1, a.batch, a.seq, h, heads, 2, calibration=calib) if calib else plan_hcm
         d1, d2 = plan["chosen"]
+        if calib:
+            # bus bandwidth of the chosen mesh's own groups (B'_k = B_k 2(d_k-1)/d_k): the planner's comm rate
+            b1, b2 = calib.get((d1, d2), (None, None))
+            bus = [b * 2.0 * (d - 1) / d for b, d in ((b1, d1), (b2, d2)) if b and d > 1]
+            if bus:
+                busbw, busbw_source = min(bus), f"probe: calibrated busBW of DeviceMesh({d1},{d2})'s groups"
+    elif a.mesh:
+        d1, d2 = (int(v) for v in a.mesh.lower().split("x"))
+    else:
+        d1, d2 = 1, 1
     assert d1 * d2 == world
 
-    mesh = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, uid, local_rank))
     ctas = a.gemm_ctas if a.gemm_ctas >= 0 else (0 if world == 1 else 132)
-    mesh.set_gemm_ctas(ctas)
-    mesh.set_gating(a.gated)
-    if a.fused_ar and world > 1:
-        # one stage's partial sums [T, widest local output] in bf16
-        mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
-
-    gpt_mode = a.layer == "gpt"
-    if gpt_mode:
-        bufs = atp.alloc_gpt_rank(d1, d2, rank, T, h, F, heads, dev, a.seed)
-        if a.chunks == 0:
-            chunks = 1 if world == 1 else min(2, a.batch)  # whole sequences; "2 or 4" (2: attention occupancy)
-
-        def make_call(bb, c):
-            return atp.GptCall(mesh, [bb], T, h, F, heads, a.seq, c, True)
-    else:
-        bufs = atp.alloc_layer_rank(d1, d2, rank, T, h, F, dev, a.seed)
-
-        def make_call(bb, c):
-            return atp.LayerCall(mesh, [bb], T, h, F, heads, c, True)
     stream = torch.cuda.Stream(device=dev)  # a capturable (non-legacy) stream for every launch of the bench
     torch.cuda.set_stream(stream)
 
@@ -416,8 +492,14 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(n_steps: int, fn=None) -> float:
-        fn = fn or call
+    def maxrank(ms: float) -> float:
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    def timed(n_steps: int, fn) -> float:
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -427,20 +509,42 @@ def main() -> None:
         e1.synchronize()
         ms = e0.elapsed_time(e1) / n_steps
         barrier()
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return maxrank(ms)
 
-    # ---- chunk count (N>1, --chunks 0): measure the compute side of each
-    # candidate with the all-reduces disabled, predict the step with the overlap
-    # model (planner.py, §4.1/§4.2) at --busbw, take the fastest (same on every
-    # rank: the timings are max-reduced over ranks before the choice).
+    def make_mesh(m1, m2):
+        m = _quiet(lambda: atp.Mesh.distributed(m1, m2, rank, new_uid(), local_rank))
+        m.set_gemm_ctas(ctas)
+        return m
+
+    mesh = make_mesh(d1, d2)
+    mesh.set_gating(a.gated)
+    if a.fused_ar and world > 1:
+        mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)  # one stage's partials [T, widest], bf16
+
+    def alloc(m1, m2):
+        if gpt_mode:
+            return atp.alloc_gpt_rank(m1, m2, rank, T, h, F, heads, dev, a.seed)
+        return atp.alloc_layer_rank(m1, m2, rank, T, h, F, dev, a.seed)
+
+    def make_call(m, bb, c):
+        if gpt_mode:
+            return atp.GptCall(m, [bb], T, h, F, heads, a.seq, c, True)
+        return atp.LayerCall(m, [bb], T, h, F, heads, c, True)
+
+    bufs = alloc(d1, d2)
+
+    # ---- chunk count (N>1, --chunks 0): the compute side of each candidate is
+    # measured with the all-reduces disabled, then atp_plan_chunks (the overlap
+    # model of §4.1/§4.2 inside libatp) predicts each step at the probed bus
+    # bandwidth and picks the fastest (same on every rank: max over ranks first).
     chunk_choice = None
-    if world > 1 and a.chunks == 0 and (d1 > 1 or d2 > 1) and not gpt_mode:
-        from paper_2301_08658_b200 import planner
-
+    if a.chunks:
+        chunks = a.chunks
+    elif world == 1 or (d1 == 1 and d2 == 1):
+        chunks = 1
+    elif gpt_mode:
+        chunks = min(2, a.batch)  # whole sequences; "2 or 4" (2: attention occupancy)
+    else:
         comp = {}
         _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 0))
         for c in (1, 2, 4, 8):
@@ -451,9 +555,11 @@ def main() -> None:
                 cc(stream)
             comp[c] = timed(5, cc)
         _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 1))
-        chunks, pred = planner.choose_chunks(T, h, F, d1, d2, comp, a.busbw)
-        chunk_choice = {"compute_ms": comp, "predicted_ms": pred, "busbw_gbs": a.busbw, "chosen": chunks}
-    call = make_call(bufs, chunks)
+        chunks, pred = atp.atp_plan_chunks(T, h, F, d1, d2, comp, busbw)
+        chunk_choice = {"compute_ms": comp, "predicted_ms": {c: v[0] for c, v in pred.items()},
+                        "predicted_exposed_ms": {c: v[1] for c, v in pred.items()}, "busbw_gbs": busbw,
+                        "busbw_source": busbw_source, "chosen": chunks, "planner": "libatp atp_plan_chunks"}
+    call = make_call(mesh, bufs, chunks)
 
     for _ in range(max(3, a.warmup)):
         call(stream)
@@ -461,21 +567,21 @@ def main() -> None:
 
     # ---- the step as one CUDA graph (atp_graph_*): host cost per step = one
     # cudaGraphLaunch; direct calls stay in use for the comm-disabled twin and
-    # the profiled pass (per-launch events cannot be captured)
+    # the event-profiled pass (per-launch events cannot be captured)
     graphs, capture_errors = [], []
 
-    def as_graph(c):
+    def as_graph(m, c):
         if a.no_graph:
             return c
         try:
-            g = atp.Graph.capture(mesh, c, stream)
+            g = atp.Graph.capture(m, c, stream)
         except Exception as e:  # noqa: BLE001  (fused peer-memory meshes refuse capture)
             capture_errors.append(str(e))
             return c
         graphs.append(g)
         return g
 
-    run = as_graph(call)
+    run = as_graph(mesh, call)
     graph_note = ("direct calls (--no-graph)" if a.no_graph else
                   f"direct calls (graph capture unavailable: {capture_errors[0]})" if capture_errors else
                   "step captured once as a CUDA graph, one cudaGraphLaunch per step")
@@ -483,47 +589,36 @@ def main() -> None:
         run(stream)
     torch.cuda.synchronize()
 
-    # ---- N>1 linear block: NCCL all-reduce (graph-captured step) vs the fused
-    # peer-memory all-reduce (GEMM signalling per chunk + one kernel per chunk
-    # doing the grouped all-reduce over NVLink peer memory with the elementwise
-    # step applied; §5), timed on this box, the faster one runs the measured
-    # steps.  The timings are max-reduced over ranks, so every rank chooses alike.
+    # ---- N>1 linear block: NCCL all-reduce (graph-captured step) vs chunk gating
+    # and the fused peer-memory all-reduce, timed on this box; the faster one runs
+    # the measured steps.  Timings are max-reduced over ranks: every rank agrees.
     ar_choice = None
     meshes = [mesh]
     if world > 1 and not gpt_mode and not a.fused_ar and not a.nccl_only and not a.gated and \
             (a.try_gated or a.try_fused):
-        # candidates: NCCL (graph-captured) with and without chunk gating (§6), and
-        # with --try-fused the fused peer-memory all-reduce likewise; 10 timed steps each
-        uid2 = atp.atp_get_unique_id() if rank == 0 else bytes(128)
-        obj = [uid2]
-        dist.broadcast_object_list(obj, src=0)
         times, runners = {}, {}
         try:
             times["nccl"], runners["nccl"] = timed(10, run), (mesh, call, run, False, graph_note)
             mesh.set_gating(True)
-            run_g = as_graph(call)
+            run_g = as_graph(mesh, call)
             for _ in range(2):
                 run_g(stream)
             times["nccl+gated"] = timed(10, run_g)
             runners["nccl+gated"] = (mesh, call, run_g, True, graph_note)
             mesh.set_gating(False)
-            if not a.try_fused:
-                raise StopIteration
-            mesh_f = _quiet(lambda: atp.Mesh.distributed(d1, d2, rank, obj[0], local_rank))
-            meshes.append(mesh_f)
-            mesh_f.set_gemm_ctas(ctas)
-            mesh_f.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
-            call_f = atp.LayerCall(mesh_f, [bufs], T, h, F, heads, chunks, True)
-            note_f = "direct calls (fused peer-memory mesh keeps cross-rank state: no graph capture)"
-            for gated in (False, True):
-                mesh_f.set_gating(gated)
-                for _ in range(3):
-                    call_f(stream)
-                key = "fused+gated" if gated else "fused"
-                times[key] = timed(10, call_f)
-                runners[key] = (mesh_f, call_f, call_f, gated, note_f)
-        except StopIteration:
-            pass
+            if a.try_fused:
+                mesh_f = make_mesh(d1, d2)
+                meshes.append(mesh_f)
+                mesh_f.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
+                call_f = atp.LayerCall(mesh_f, [bufs], T, h, F, heads, chunks, True)
+                note_f = "direct calls (fused peer-memory mesh keeps cross-rank state: no graph capture)"
+                for gated in (False, True):
+                    mesh_f.set_gating(gated)
+                    for _ in range(3):
+                        call_f(stream)
+                    key = "fused+gated" if gated else "fused"
+                    times[key] = timed(10, call_f)
+                    runners[key] = (mesh_f, call_f, call_f, gated, note_f)
         except Exception as e:  # noqa: BLE001  (keeps the NCCL step)
             ar_choice = {"error": str(e)}
             mesh.set_gating(False)
@@ -549,6 +644,7 @@ def main() -> None:
     launches = int(n1.value - n0.value)
 
     fl = gpt_flops(T, h, F, a.seq) if gpt_mode else layer_flops(T, h, F)
+    gemm_fl = layer_flops(T, h, F) / world  # the GEMM FLOPs of one rank per step
     value = fl / (ms * 1e-3) / 1e12
     per_gpu = value / world
 
@@ -561,39 +657,103 @@ def main() -> None:
         _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mesh.handle, 1))
         exposed = max(0.0, ms - ms_nocomm)
 
-    # ---- profiled pass: per-class device time from CUDA events on the launching streams
-    prof = _abi.Profile()
-    n_prof = max(5, min(a.steps, 30))
-    _abi.check(_abi.lib().atp_profile_begin(mesh.handle))
-    ms_prof = timed(n_prof, call)
-    _abi.check(_abi.lib().atp_profile_end(mesh.handle, C.byref(prof)))
+    # ---- roofline of the dominant kernel (the tcgen05 GEMM): GEMM time and its
+    # share of the step from a CUPTI trace of the SAME graph-launched step
     pk = peaks(a.peaks)
-    gemm_ms = prof.ms[0] / n_prof
-    gemm_launch_ms = prof.ms[0] / max(1, prof.launches[0])
-    gemm_tflops = (prof.flops[0] / n_prof) / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
-    peak_tc = pk["bf16_tflops_sustained"] or pk["bf16_tflops"]
-    roofline = {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_tc, "unit": "TFLOP/s",
-                "frac": gemm_tflops / peak_tc,
-                "traffic": (lambda t: t["dram_bytes_per_gemm_launch"] if t else None)(traffic_for(a.peaks, h, T)),
-                "traffic_detail": traffic_for(a.peaks, h, T),
-                "kernel": "gemm_sm100_kernel (tcgen05, all GEMM launches of the step)",
-                "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside a long step)",
-                "gemm_share_of_step": gemm_ms / ms_prof if ms_prof > 0 else None,
-                "gemm_launches_per_step": prof.launches[0] / n_prof, "avg_gemm_launch_ms": gemm_launch_ms,
-                "elementwise_ms_per_step": prof.ms[1] / n_prof,
-                "elementwise_gbs": (prof.bytes[1] / max(prof.ms[1], 1e-9)) / 1e6,
-                "allreduce_ms_per_step": prof.ms[2] / n_prof,
-                "allreduce_busbw_gbs": (prof.bytes[2] / max(prof.ms[2], 1e-9)) / 1e6 if prof.ms[2] > 0 else None,
-                "profiled_ms_per_step": ms_prof,
-                "layer_roofline_frac": (fl / world / (peak_tc * 1e12)) / (ms * 1e-3)}
+    timed_s = ms * a.steps / 1e3
+    throttled = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and
+                     clocks["sm_mhz"] < 0.9 * clocks["sm_max_mhz"] and "sw_power_cap" in clocks.get("reasons", []))
+    use_sustained = throttled and timed_s >= 2.0 and pk["bf16_tflops_sustained"]
+    peak_tc = pk["bf16_tflops_sustained"] if use_sustained else pk["bf16_tflops"]
+    peak_rule = ("sustained: this run's timed region lasted %.1f s with SM clocks at %s of %s MHz under sw_power_cap"
+                 % (timed_s, clocks.get("sm_mhz"), clocks.get("sm_max_mhz")) if use_sustained else
+                 "burst: the timed region was not a seconds-long power-capped run (%.2f s, median %s of %s MHz)"
+                 % (timed_s, clocks.get("sm_mhz"), clocks.get("sm_max_mhz")))
+    n_prof = max(3, min(a.steps, 10))
+    roofline = {"bound": "tensor", "unit": "TFLOP/s", "peak": peak_tc, "peak_rule": peak_rule,
+                "peak_burst": pk["bf16_tflops"], "peak_sustained": pk["bf16_tflops_sustained"],
+                "peak_source": pk["source"], "kernel": "gemm_sm100_kernel (tcgen05; all GEMM launches of the step)",
+                "traffic": None}
+    cupti = None
+    if not a.no_cupti:
+        try:
+            ks = cupti_kernels(run, stream, n_prof)
+            by = {}
+            for nm, s, e in ks:
+                by.setdefault(kernel_class(nm), []).append((s, e))
+            span = (max(e for _, _, e in ks) - min(s for _, s, _ in ks)) / 1e6 / n_prof if ks else None
+            gemm_ms = union_ms(by.get("gemm", [])) / n_prof
+            cupti = {"kernels_per_step": len(ks) / n_prof,
+                     "gemm_launches_per_step": len(by.get("gemm", [])) / n_prof,
+                     "ms_per_step_by_class": {k: union_ms(v) / n_prof for k, v in by.items()},
+                     "traced_step_span_ms": span, "steps_traced": n_prof,
+                     "source": "CUPTI activity trace (torch.profiler/kineto) of the graph-launched step, "
+                               "kernel intervals merged per class (PDL overlap counted once)"}
+            if gemm_ms > 0:
+                roofline["achieved"] = gemm_fl / (gemm_ms * 1e-3) / 1e12
+                roofline["frac"] = roofline["achieved"] / peak_tc
+                roofline["frac_burst"] = roofline["achieved"] / pk["bf16_tflops"]
+                if pk["bf16_tflops_sustained"]:
+                    roofline["frac_sustained"] = roofline["achieved"] / pk["bf16_tflops_sustained"]
+                roofline["gemm_ms_per_step"] = gemm_ms
+                roofline["gemm_share_of_step"] = gemm_ms / ms
+                roofline["avg_gemm_launch_ms"] = gemm_ms / max(1e-9, cupti["gemm_launches_per_step"])
+        except Exception as e:  # noqa: BLE001
+            cupti = {"error": f"{type(e).__name__}: {e}"}
+    # cross-check: per-launch CUDA events recorded by the executor on the launching streams (direct calls)
+    prof = _abi.Profile()
+    n_ev = max(5, min(a.steps, 20))
+    _abi.check(_abi.lib().atp_profile_begin(mesh.handle))
+    ms_prof = timed(n_ev, call)
+    _abi.check(_abi.lib().atp_profile_end(mesh.handle, C.byref(prof)))
+    ev_gemm_ms = prof.ms[0] / n_ev
+    event_profile = {"gemm_ms_per_step": ev_gemm_ms,
+                     "gemm_tflops": (prof.flops[0] / n_ev) / (ev_gemm_ms * 1e-3) / 1e12 if ev_gemm_ms > 0 else None,
+                     "gemm_launches_per_step": prof.launches[0] / n_ev,
+                     "elementwise_ms_per_step": prof.ms[1] / n_ev,
+                     "elementwise_gbs": (prof.bytes[1] / max(prof.ms[1], 1e-9)) / 1e6,
+                     "allreduce_ms_per_step": prof.ms[2] / n_ev,
+                     "allreduce_busbw_gbs": (prof.bytes[2] / max(prof.ms[2], 1e-9)) / 1e6 if prof.ms[2] > 0 else None,
+                     "profiled_ms_per_step": ms_prof,
+                     "note": "direct calls with a CUDA event pair around every launch (no graph, no PDL)"}
+    if "achieved" not in roofline and ev_gemm_ms > 0:  # CUPTI unavailable: fall back to the events
+        roofline["achieved"] = event_profile["gemm_tflops"]
+        roofline["frac"] = roofline["achieved"] / peak_tc
+        roofline["gemm_share_of_step"] = ev_gemm_ms / ms_prof
+    tr = traffic_for(h, T) if world == 1 else None
+    if tr:
+        roofline["traffic"] = tr["dram_bytes_per_gemm_launch"]
+        roofline["traffic_detail"] = tr
+    roofline["layer_roofline_frac"] = (fl / world / (peak_tc * 1e12)) / (ms * 1e-3)
     if gpt_mode:
-        att_ms = prof.ms[3] / n_prof
+        att_ms = prof.ms[3] / n_ev
         roofline.update({
             "attention_ms_per_step": att_ms,
-            "attention_tflops": (prof.flops[3] / n_prof) / (att_ms * 1e-3) / 1e12 if att_ms > 0 else None,
-            "attention_share_of_step": att_ms / ms_prof if ms_prof > 0 else None,
-            "tensor_achieved_gemm_plus_attention": ((prof.flops[0] + prof.flops[3]) / n_prof)
-            / ((gemm_ms + att_ms) * 1e-3) / 1e12})
+            "attention_tflops": (prof.flops[3] / n_ev) / (att_ms * 1e-3) / 1e12 if att_ms > 0 else None,
+            "attention_share_of_step": att_ms / ms_prof if ms_prof > 0 else None})
+
+    # ---- Megatron-style baseline (north_star): the same library on DeviceMesh(N,1), 1 chunk
+    baseline = None
+    if world > 1 and not a.no_baseline and not gpt_mode and ((d1, d2) != (world, 1) or chunks != 1):
+        try:
+            mb = make_mesh(world, 1)
+            meshes.append(mb)
+            bb = alloc(world, 1)
+            cb = make_call(mb, bb, 1)
+            for _ in range(3):
+                cb(stream)
+            rb = as_graph(mb, cb)
+            ms_b = timed(a.steps, rb)
+            _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mb.handle, 0))
+            ms_b0 = timed(max(10, a.steps // 2), cb)
+            _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mb.handle, 1))
+            baseline = {"mesh": [world, 1], "chunks": 1, "ms_per_step": ms_b,
+                        "tflops_per_gpu": fl / (ms_b * 1e-3) / 1e12 / world,
+                        "exposed_comm_ms": max(0.0, ms_b - ms_b0), "ms_per_step_comm_disabled": ms_b0,
+                        "speedup_of_atp_step": ms_b / ms}
+            del bb
+        except Exception as e:  # noqa: BLE001
+            baseline = {"error": str(e)}
 
     # ---- e2e: every step's inputs (X, dZ) H2D from pinned host memory and its
     # result (the bias gradients) D2H, through the public API.  Inputs are
@@ -607,8 +767,8 @@ def main() -> None:
         h2d = hx.numel() * hx.element_size() + hdz.numel() * hdz.element_size()
         d2h = sum(r.numel() * r.element_size() for r in res)
         bufs_b = dict(bufs, x=torch.empty_like(bufs["x"]), dz=torch.empty_like(bufs["dz"]))
-        sets = [(bufs, run), (bufs_b, as_graph(make_call(bufs_b, chunks)) if run is not call else
-                                  make_call(bufs_b, chunks))]
+        sets = [(bufs, run), (bufs_b, as_graph(mesh, make_call(mesh, bufs_b, chunks)) if run is not call else
+                                  make_call(mesh, bufs_b, chunks))]
         copy_stream = torch.cuda.Stream()
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -635,23 +795,20 @@ def main() -> None:
 
         run_e2e(3)
         barrier()
-        n_e2e = max(5, min(a.steps, 50))
+        n_e2e = max(5, min(a.steps, 30))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         copy_stream.wait_event(e0)
         run_e2e(n_e2e)
         e1.record(stream)
         e1.synchronize()
-        ms_e2e = e0.elapsed_time(e1) / n_e2e
-        if world > 1:
-            t = torch.tensor([ms_e2e], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
-        e2e = {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
+        ms_e2e = maxrank(e0.elapsed_time(e1) / n_e2e)
+        e2e = {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": d2h * world, "ms_per_step": ms_e2e,
                "api": ("paper_2301_08658_b200.GptCall -> atp_gpt_layer_fwd_bwd (C ABI)" if gpt_mode else
                        "paper_2301_08658_b200.LayerCall -> atp_layer_fwd_bwd (C ABI)"),
-               "note": "X, dZ copied H2D every step (double-buffered on a copy stream), bias grads read D2H"}
+               "note": "every rank copies its X, dZ shards H2D every step (double-buffered on a copy stream) and "
+                       "reads its bias gradients D2H; bytes summed over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -664,37 +821,45 @@ def main() -> None:
         m.destroy()
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
-            "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "value_scope": VALUE_SCOPE, "n_gpus": world,
+            "steps": a.steps, "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": (f"full pre-LN GPT layer (LN + QKV + causal softmax attention + Out + LN + MLP, "
                                     f"fwd+bwd) h{h} a{heads} ffn{F} s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), "
                                     f"chunks {chunks}") if gpt_mode else
                                    (f"gpt-layer linear block (QKV/Out/FC1/FC2 fwd+bwd) h{h} a{heads} ffn{F} "
-                                    f"s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), chunks {chunks}"),
+                                    f"s{a.seq} b{a.batch} ({cfg_name}), DeviceMesh({d1},{d2}), chunks {chunks}"),
                        "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
                        "allreduce": ("fused peer-memory kernel" if ((a.fused_ar or str((ar_choice or {}).get("chosen", "")).startswith("fused"))
                                                                     and world > 1) else "nccl"),
                        "gated": bool(a.gated and world > 1), "mesh_source": mesh_source, "launch": graph_note,
+                       "nccl_p2p_disable": bool(a.p2p_disable),
                        **({"shared_gpu": "TEST ONLY: all ranks on cuda:0, NCCL over sockets; timings meaningless"}
                           if a.share_gpu else {}),
-                       "l2": "working set > 126 MB L2 (weights+activations ~1-2 GB), no flush"},
+                       "l2": "working set > 126 MB L2 (weights+activations, GBs), no flush"},
             "tflops_per_gpu": per_gpu, "exposed_comm_ms": exposed, "ms_per_step_comm_disabled": ms_nocomm,
+            "exposed_comm_frac": exposed / ms if ms > 0 else None,
             "flops_per_step": fl, "clocks": clocks, "gpu_launches": launches,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+            "kernel_trace": cupti, "event_profile": event_profile,
         }
         if chunk_choice is not None:
             out["chunk_choice"] = chunk_choice
         if ar_choice is not None:
             out["allreduce_choice"] = ar_choice
+        if baseline is not None:
+            out["megatron_baseline"] = baseline
+        if probe is not None:
+            out["probe"] = probe
         if gpt_mode:
             out["tflops_paper_formula"] = gpt_flops_paper(T, h, a.seq) / (ms * 1e-3) / 1e12
             out["flops_note"] = ("value counts the FLOPs performed (linear 72Th^2 + causal core 7(s+1)Th); "
                                  "tflops_paper_formula uses P:375's 72bsh^2 + 12bs^2h (non-causal core)")
         if plan is not None:
-            out["search"] = {"chosen": plan["chosen"], "ranked": [(r["d1"], r["d2"], r["t_comm"], r["calibrated"])
-                                                                   for r in plan["ranked"]]}
+            rk = lambda p: [(r["d1"], r["d2"], r["t_comm"], r["calibrated"]) for r in p["ranked"]]
+            out["search"] = {"chosen": plan["chosen"], "ranked": rk(plan),
+                             "hcm_only": {"chosen": plan_hcm["chosen"], "ranked": rk(plan_hcm)}}
         emit(out)
     if world > 1:
         dist.destroy_process_group()

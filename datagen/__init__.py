@@ -104,7 +104,21 @@ def tensor(name: str, shape, seed: int = BASE_SEED, bf16: bool = True,
     nr, nc = shape
     r = np.arange(nr) if rows is None else np.asarray(rows)
     c = np.arange(nc) if cols is None else np.asarray(cols)
-    return uniform_block(tid, (nr, nc), r, c, sc, seed, bf16, off)
+    if len(r) * len(c) < (1 << 22):
+        return uniform_block(tid, (nr, nc), r, c, sc, seed, bf16, off)
+    # large tensors: row blocks on a thread pool (numpy's integer ufuncs release the GIL)
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    out = np.empty((len(r), len(c)), dtype=np.float32)
+    step = max(1, (1 << 20) // max(1, len(c)))
+
+    def fill(i0):
+        out[i0:i0 + step] = uniform_block(tid, (nr, nc), r[i0:i0 + step], c, sc, seed, bf16, off)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        list(ex.map(fill, range(0, len(r), step)))
+    return out
 
 
 def layer_shapes(T: int, h: int, F: int) -> dict:

@@ -490,6 +490,29 @@ atp_status atp_comm_volume(int d1, int d2, int64_t T, int64_t h, int64_t F, int 
 atp_status atp_overlap_estimate(int n_stages, const double* comp, const double* dw, const double* comm, int chunks,
                                 int mode, double* makespan, double* exposed);
 
+/* Chunk-count planner (§4.1 P:332 fixes c by hand,
+ * "2 or 4"; Table 3 P:449 shows the best c depends on the interconnect).
+ * atp_layer_stages splits one layer fwd+bwd on DeviceMesh(d1, d2) into its 8
+ * linear stages in schedule order (QKV, Out, FC1, FC2 forward; FC2, FC1, Out,
+ * QKV backward): comp[i] = compute_ms x (stage GEMM FLOPs / all GEMM FLOPs),
+ * dw[i] = compute_ms x (dW GEMM FLOPs / all; backward stages only, §4.2),
+ * comm[i] = executed ring all-reduce bytes 2(p-1)/p x T x width x bytes_per_elem
+ * (the atp_comm_volume list, reading G4) / busbw_gbps, in ms; 0 on a size-1
+ * dimension.  Output arrays hold 8 doubles (caller-owned host memory).
+ * atp_plan_chunks evaluates atp_overlap_estimate (mode 0 signalled / 1
+ * per-chunk) on those stages for each candidate chunk count chunks[i]
+ * (ascending, dividing T) with its measured compute-side time compute_ms[i]
+ * (collectives elided), writes makespan_ms[i] / exposed_ms[i] (either may be
+ * NULL) and *chosen = the count with the smallest makespan (ties -> fewer
+ * chunks).  Pure host code, bit-identical to oracle/overlap.py layer_stages /
+ * plan_chunks.  Errors: ATP_ERR_INVALID (shapes not divisible by the mesh,
+ * busbw <= 0, bad candidates). */
+atp_status atp_layer_stages(int d1, int d2, int64_t T, int64_t h, int64_t F, int bytes_per_elem, double compute_ms,
+                            double busbw_gbps, double* comp, double* dw, double* comm);
+atp_status atp_plan_chunks(int d1, int d2, int64_t T, int64_t h, int64_t F, int bytes_per_elem, int n_cand,
+                           const int* chunks, const double* compute_ms, double busbw_gbps, int mode, int* chosen,
+                           double* makespan_ms, double* exposed_ms);
+
 /* ------------------------------------------------------------------ probe
  * Bandwidth probe feeding the HCM (§3.4) and the calibration, on a
  * distributed mesh spanning all ranks: times ncclAllReduce on each mesh

@@ -162,6 +162,11 @@ SIGNATURES = {
     "atp_overlap_estimate": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.c_int, C.c_int, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]),
+    "atp_layer_stages": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, C.c_int, C.c_double, C.c_double,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "atp_plan_chunks": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                  C.POINTER(C.c_double), C.c_double, C.c_int, C.POINTER(C.c_int),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "atp_probe_hcm": (C.c_int, [vp, C.POINTER(C.c_size_t), C.c_int, C.c_size_t, C.c_int, vp, C.POINTER(Hcm),
                                 C.POINTER(C.c_double), C.POINTER(Calib)]),
     "atp_probe_allreduce": (C.c_int, [vp, C.c_int, C.c_size_t, C.c_int, vp, C.POINTER(C.c_double),

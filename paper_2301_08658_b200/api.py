@@ -137,6 +137,8 @@ def atp_attn_core_bwd(qkv, ctx, lse, dctx, dqkv, seq: int, heads: int, causal: b
     nbytes = lib().atp_attn_core_workspace(T, heads)
     if workspace is None:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=qkv.device)
+        if stream is not None and stream != torch.cuda.current_stream(qkv.device):
+            workspace.record_stream(stream)  # the kernel runs on `stream`: keep the block alive until it finishes
     check(lib().atp_attn_core_bwd(qkv.data_ptr(), qkv.stride(0), ctx.data_ptr(), ctx.stride(0), lse.data_ptr(),
                                   dctx.data_ptr(), dctx.stride(0), T, seq, heads, head_dim, int(causal),
                                   dqkv.data_ptr(), dqkv.stride(0), workspace.data_ptr(), workspace.numel(),
@@ -199,11 +201,29 @@ def _dt(t) -> int:
     return _abi.ATP_FP32 if t.dtype == torch.float32 else _abi.ATP_BF16
 
 
+def _gen_block(name, shape, r0, nr, c0, nc, device, seed, bf16=True, host=False):
+    """One block of a seeded global input (datagen): generated on the device, or
+    with host=True on the host (numpy) and copied in (no device kernel besides the copy)."""
+    import numpy as np
+    import torch
+    import datagen
+
+    if not host:
+        return datagen.torch_block(name, shape, r0, nr, c0, nc, device, seed=seed, bf16=bf16)
+    cols = np.arange(c0, c0 + nc)
+    v = (datagen.tensor(name, shape, seed=seed, bf16=bf16, cols=cols) if len(shape) == 1 else
+         datagen.tensor(name, shape, seed=seed, bf16=bf16, rows=np.arange(r0, r0 + nr), cols=cols))
+    # cast on the host (exact: the values are bf16-representable), then one H2D copy
+    return torch.from_numpy(np.ascontiguousarray(v.reshape(nr, nc))).to(
+        dtype=torch.bfloat16 if bf16 else torch.float32).to(device=device)
+
+
 def alloc_layer_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, device, seed: int, with_bias: bool = True,
-                     inputs: bool = True, fp32: bool = False) -> dict:
+                     inputs: bool = True, fp32: bool = False, host_inputs: bool = False) -> dict:
     """Allocate one rank's layer buffers; fill inputs/weights from the seeded
-    counter-based generator (datagen) directly on the device.  fp32=True:
-    the ATP_FP32 check mode (fp32 storage, unrounded fp32 inputs)."""
+    counter-based generator (datagen) directly on the device (host_inputs=True:
+    on the host, then one copy).  fp32=True: the ATP_FP32 check mode (fp32
+    storage, unrounded fp32 inputs)."""
     import torch
     import datagen
 
@@ -216,7 +236,7 @@ def alloc_layer_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, device
     for name in ("x", "dz", "wqkv", "wo", "w1", "w2") + (("bqkv", "bo", "b1", "b2") if with_bias else ()):
         r0, nr, c0, nc = box[name]
         if inputs:
-            t = datagen.torch_block(name, shapes[name], r0, nr, c0, nc, device, seed=seed, bf16=not fp32)
+            t = _gen_block(name, shapes[name], r0, nr, c0, nc, device, seed, bf16=not fp32, host=host_inputs)
         else:
             t = torch.empty((nr, nc), dtype=bf, device=device)
         b[name] = t.reshape(-1) if name.startswith("b") else t
@@ -329,8 +349,9 @@ def gpt_boxes(d1: int, d2: int, rank: int, T: int, h: int, F: int) -> dict:
 
 
 def alloc_gpt_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, heads: int, device, seed: int,
-                   inputs: bool = True) -> dict:
-    """One rank's full-layer buffers (inputs from the seeded generator, on the device)."""
+                   inputs: bool = True, host_inputs: bool = False) -> dict:
+    """One rank's full-layer buffers (inputs from the seeded generator, on the
+    device, or with host_inputs=True on the host and copied in)."""
     import torch
     import datagen
 
@@ -339,7 +360,7 @@ def alloc_gpt_rank(d1: int, d2: int, rank: int, T: int, h: int, F: int, heads: i
     shapes = datagen.gpt_shapes(T, h, F)
     b = {}
     for name, (r0, nr, c0, nc) in gpt_boxes(d1, d2, rank, T, h, F).items():
-        t = (datagen.torch_block(name, shapes[name], r0, nr, c0, nc, device, seed=seed) if inputs
+        t = (_gen_block(name, shapes[name], r0, nr, c0, nc, device, seed, host=host_inputs) if inputs
              else torch.empty((nr, nc), dtype=torch.bfloat16, device=device))
         b[name] = t.reshape(-1) if len(shapes[name]) == 1 else t
     bf, f32 = torch.bfloat16, torch.float32
@@ -463,3 +484,24 @@ def atp_overlap_estimate(stages, chunks: int, mode: str = "signalled"):
     check(lib().atp_overlap_estimate(n, arr(0), arr(1), arr(2), chunks, 0 if mode == "signalled" else 1,
                                      C.byref(mk), C.byref(ex)))
     return mk.value, ex.value
+
+
+def atp_layer_stages(T, h, F, d1, d2, compute_ms, busbw_gbps, bytes_per_elem=2):
+    """[(comp_ms, dw_ms, comm_ms)] x 8 stages of one layer fwd+bwd (libatp's planner decomposition)."""
+    a, b, c = (C.c_double * 8)(), (C.c_double * 8)(), (C.c_double * 8)()
+    check(lib().atp_layer_stages(d1, d2, T, h, F, bytes_per_elem, compute_ms, busbw_gbps, a, b, c))
+    return [(a[i], b[i], c[i]) for i in range(8)]
+
+
+def atp_plan_chunks(T, h, F, d1, d2, compute_ms_by_c: dict, busbw_gbps: float, mode: str = "signalled",
+                    bytes_per_elem: int = 2):
+    """Chunk count with the smallest predicted step (libatp atp_plan_chunks).
+    Returns (chosen c, {c: (makespan_ms, exposed_ms)})."""
+    cs = sorted(compute_ms_by_c)
+    n = len(cs)
+    ch = (C.c_int * n)(*cs)
+    cm = (C.c_double * n)(*[float(compute_ms_by_c[c]) for c in cs])
+    mk, ex, chosen = (C.c_double * n)(), (C.c_double * n)(), C.c_int()
+    check(lib().atp_plan_chunks(d1, d2, T, h, F, bytes_per_elem, n, ch, cm, busbw_gbps,
+                                0 if mode == "signalled" else 1, C.byref(chosen), mk, ex))
+    return chosen.value, {c: (mk[i], ex[i]) for i, c in enumerate(cs)}

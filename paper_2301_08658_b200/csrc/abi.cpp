@@ -641,12 +641,24 @@ extern "C" atp_status atp_probe_hcm(atp_mesh* world, const size_t* msg_bytes, in
     const double t = time_allreduce(c, scratch, bytes, iters, st, &r);
     return p > 1 ? (static_cast<double>(bytes) / t) * 2.0 * (p - 1) / p / 1e9 : 0.0;
   };
-  // group bandwidth: N-rank all-reduce on the world communicator
+  // group bandwidth: N-rank all-reduce on the world communicator; every rank
+  // takes the slowest rank's figure (min over ranks, exchanged as an exact
+  // double) so all ranks hold the same HCM and search alike
   double group = 0.0;
   for (int i = 0; i < n_msgs && N > 1; ++i) {
     const double b = busbw(world->world, N, msg_bytes[i]);
     if (r != ncclSuccess) return nccl_fail("probe group");
     group = b > group ? b : group;
+  }
+  if (N > 1) {
+    double v = -group;  // max of -bw = min of bw
+    double* d = static_cast<double*>(scratch);
+    cudaMemcpyAsync(d, &v, sizeof(v), cudaMemcpyHostToDevice, st);
+    r = ncclAllReduce(d, d, 1, ncclFloat64, ncclMax, world->world, st);
+    if (r != ncclSuccess) return nccl_fail("probe group exchange");
+    cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    group = -v;
   }
   // P2P: round-robin tournament (circle method) over N (or N+1 with a bye) slots
   const int slots = N + (N & 1);

@@ -289,3 +289,79 @@ extern "C" atp_status atp_overlap_estimate(int n_stages, const double* comp, con
   if (exposed) *exposed = mk - total;
   return ATP_OK;
 }
+
+// ---------------------------------------------------------------- chunk planner
+// Stage decomposition of one layer fwd+bwd (reading G36) and the
+// argmin over candidate chunk counts; same operations in the same order as
+// oracle/overlap.py layer_stages / plan_chunks.
+namespace {
+bool layer_dims_ok(int d1, int d2, int64_t T, int64_t h, int64_t F) {
+  return d1 >= 1 && d2 >= 1 && T > 0 && h > 0 && F > 0 && h % d1 == 0 && h % d2 == 0 && (3 * h) % d1 == 0 &&
+         F % d1 == 0;
+}
+
+void stages8(int d1, int d2, int64_t T, int64_t h, int64_t F, int bytes, double compute_ms, double busbw,
+             double* comp, double* dw, double* comm) {
+  const int64_t hc = h / d2, h1 = h / d1, q1 = 3 * h / d1, F1 = F / d1;
+  struct St { int64_t n, k; bool dw; int dim; int64_t width; };
+  const St st[8] = {{q1, hc, false, 2, q1}, {hc, h1, false, 1, hc}, {F1, hc, false, 2, F1}, {hc, F1, false, 1, hc},
+                    {F1, hc, true, 2, F1},  {hc, F1, true, 1, hc},  {h1, hc, true, 2, h1},  {hc, q1, true, 1, hc}};
+  double g[8], w[8], tot = 0.0;
+  for (int i = 0; i < 8; ++i) {
+    g[i] = 2.0 * (double)T * (double)st[i].n * (double)st[i].k;
+    w[i] = st[i].dw ? 2.0 * (double)st[i].n * (double)st[i].k * (double)T : 0.0;
+  }
+  for (int i = 0; i < 8; ++i) tot = tot + (g[i] + w[i]);
+  for (int i = 0; i < 8; ++i) {
+    const int p = st[i].dim == 1 ? d1 : d2;
+    const int64_t elems = T * st[i].width;
+    comm[i] = p > 1 ? (2.0 * (p - 1) / p * (double)elems * (double)bytes) / (busbw * 1e9) * 1e3 : 0.0;
+    comp[i] = compute_ms * g[i] / tot;
+    dw[i] = compute_ms * w[i] / tot;
+  }
+}
+}  // namespace
+
+extern "C" atp_status atp_layer_stages(int d1, int d2, int64_t T, int64_t h, int64_t F, int bytes_per_elem,
+                                       double compute_ms, double busbw_gbps, double* comp, double* dw,
+                                       double* comm) {
+  if (!layer_dims_ok(d1, d2, T, h, F) || bytes_per_elem < 1 || !(compute_ms >= 0.0) || !(busbw_gbps > 0.0) ||
+      comp == nullptr || dw == nullptr || comm == nullptr) {
+    atp::set_error("atp_layer_stages: invalid arguments");
+    return ATP_ERR_INVALID;
+  }
+  stages8(d1, d2, T, h, F, bytes_per_elem, compute_ms, busbw_gbps, comp, dw, comm);
+  return ATP_OK;
+}
+
+extern "C" atp_status atp_plan_chunks(int d1, int d2, int64_t T, int64_t h, int64_t F, int bytes_per_elem,
+                                      int n_cand, const int* chunks, const double* compute_ms, double busbw_gbps,
+                                      int mode, int* chosen, double* makespan_ms, double* exposed_ms) {
+  if (!layer_dims_ok(d1, d2, T, h, F) || bytes_per_elem < 1 || n_cand < 1 || chunks == nullptr ||
+      compute_ms == nullptr || !(busbw_gbps > 0.0) || (mode != 0 && mode != 1) || chosen == nullptr) {
+    atp::set_error("atp_plan_chunks: invalid arguments");
+    return ATP_ERR_INVALID;
+  }
+  for (int i = 0; i < n_cand; ++i) {
+    if (chunks[i] < 1 || T % chunks[i] || !(compute_ms[i] >= 0.0) || (i > 0 && chunks[i] <= chunks[i - 1])) {
+      atp::set_error("atp_plan_chunks: candidates must be ascending chunk counts dividing T with compute >= 0");
+      return ATP_ERR_INVALID;
+    }
+  }
+  int best = -1;
+  double best_mk = 0.0;
+  for (int i = 0; i < n_cand; ++i) {
+    double comp[8], dw[8], comm[8], mk = 0.0, ex = 0.0;
+    stages8(d1, d2, T, h, F, bytes_per_elem, compute_ms[i], busbw_gbps, comp, dw, comm);
+    const atp_status st = atp_overlap_estimate(8, comp, dw, comm, chunks[i], mode, &mk, &ex);
+    if (st != ATP_OK) return st;
+    if (makespan_ms) makespan_ms[i] = mk;
+    if (exposed_ms) exposed_ms[i] = ex;
+    if (best < 0 || mk < best_mk) {
+      best = i;
+      best_mk = mk;
+    }
+  }
+  *chosen = chunks[best];
+  return ATP_OK;
+}

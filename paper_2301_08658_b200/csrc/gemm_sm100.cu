@@ -700,9 +700,9 @@ const char* gemm_prepare(GemmDesc& d, const void* A, int64_t lda, bool a_mn, con
   d.a_mn = a_mn;
   d.b_mn = b_mn;
   if (d.bn != 128 && d.bn != 256) gemm_plan_tile(M, N, &d.bn, &d.cg);
-  d.group_m = raster_group_m(d.cg == 2 ? 256 : BM, N, K);
   if (d.cg != 1 && d.cg != 2) d.cg = (d.bn == 256 && M >= 256 && gemm_mode() != 1) ? 2 : 1;
   if (d.cg == 2 && d.bn != 256) d.cg = 1;
+  d.group_m = raster_group_m(d.cg == 2 ? 256 : BM, N, K);  // after cg is final (rows per M-tile)
   bool ok;
   if (!a_mn)
     ok = make_tmap(&d.tmA, A, M, K, lda, BM, BK);

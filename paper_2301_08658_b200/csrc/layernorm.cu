@@ -169,20 +169,25 @@ __global__ void ln_fwd_fused_kernel(const __nv_bfloat16* __restrict__ x, int64_t
   const int lane = threadIdx.x % 32;
   for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; r < rows;
        r += (static_cast<int64_t>(gridDim.x) * blockDim.x) / 32) {
+    // shifted one-pass moments: sums of (x - K) with K = the row's first
+    // element, so var = E[(x-K)^2] - E[x-K]^2 does not cancel when |mean| >> std
+    const float K = __bfloat162float(x[r * ldx]);
     float s = 0.f, q = 0.f;
 #pragma unroll 4
     for (int64_t c = 8 * lane; c < cols; c += 256) {
       const F8 v = ld8(x + r * ldx + c);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        s += v.v[i];
-        q += v.v[i] * v.v[i];
+        const float t = v.v[i] - K;
+        s += t;
+        q += t * t;
       }
     }
     s = warp_sum(s);
     q = warp_sum(q);
-    const float mean = s / static_cast<float>(cols);
-    const float var = fmaxf(q / static_cast<float>(cols) - mean * mean, 0.f);
+    const float ms = s / static_cast<float>(cols);
+    const float mean = K + ms;
+    const float var = fmaxf(q / static_cast<float>(cols) - ms * ms, 0.f);
     const float rstd = rsqrtf(var + kLnEps);
 #pragma unroll 4
     for (int64_t c = 8 * lane; c < cols; c += 256) {
@@ -273,22 +278,32 @@ __global__ void __launch_bounds__(1024) ln_fwd_row_kernel(const __nv_bfloat16* _
     g[v] = ld8(gamma + c0 + v * stride);
     b[v] = ld8(beta + c0 + v * stride);
   }
-  int par = 0;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, par ^= 1) {
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    // two-pass moments from the register-resident row (no extra HBM traffic):
+    // mean first, then sum (x - mean)^2 -- no cancellation when |mean| >> std.
+    // The two reductions use the two halves of `red`, so a row's first
+    // reduction never overwrites values the previous row's second one reads.
     F8 xv[kRowV];
-    float s = 0.f, q = 0.f;
+    float s = 0.f, z = 0.f;
 #pragma unroll
     for (int v = 0; v < kRowV; ++v) {
       xv[v] = ld8(x + r * ldx + c0 + v * stride);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        s += xv[v].v[i];
-        q += xv[v].v[i] * xv[v].v[i];
-      }
+      for (int i = 0; i < 8; ++i) s += xv[v].v[i];
     }
-    block_sum2(s, q, red, par);
+    block_sum2(s, z, red, 0);
     const float mean = s / static_cast<float>(cols);
-    const float var = fmaxf(q / static_cast<float>(cols) - mean * mean, 0.f);
+    float q = 0.f;
+    z = 0.f;
+#pragma unroll
+    for (int v = 0; v < kRowV; ++v)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float t = xv[v].v[i] - mean;
+        q += t * t;
+      }
+    block_sum2(q, z, red, 1);
+    const float var = q / static_cast<float>(cols);
     const float rstd = rsqrtf(var + kLnEps);
 #pragma unroll
     for (int v = 0; v < kRowV; ++v) {

@@ -475,6 +475,11 @@ int debug_counters(atp_mesh* m, int rank, uint32_t* out, int n) {
 }
 
 int enable_fused_ar(atp_mesh* m, size_t part_bytes) {
+  // the peer tables (RankState::peers, FusedArArgs::peer_base) hold 16 members per group
+  if (m->d1 > 16 || m->d2 > 16) {
+    set_error("fused all-reduce: mesh dimensions above 16 are not supported (peer tables hold 16 members)");
+    return 1;
+  }
   part_bytes = (part_bytes + 255) & ~static_cast<size_t>(255);
   const size_t flag_bytes = 3 * static_cast<size_t>(kSigSlots) * sizeof(uint32_t);
   const int n_local = static_cast<int>(m->rs.size());

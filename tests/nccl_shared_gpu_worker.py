@@ -87,6 +87,43 @@ def _gpt(atp, mesh, d1, d2, rank, chunks, seed):
     return worst
 
 
+def _probe_search(atp, mesh, world):
+    """S1 -> S2 ("run S" of SURVEY §8(d)): atp_probe_hcm on the world mesh, its
+    HCM written as SPEC's topology document plus the calibration
+    table, read back, and ranked by libatp's atp_search and by the oracle's
+    search on the SAME parsed numbers: rankings and doubles must agree bit for
+    bit, with and without the calibration."""
+    import json
+
+    import torch
+    from oracle import costmodel as cm
+
+    scratch = torch.empty((4 << 20) + 64, dtype=torch.uint8, device="cuda:0")
+    layers, matrix, calib = atp.atp_probe_hcm(mesh, scratch, msg_bytes=(1 << 20, 4 << 20), calib_bytes=1 << 20,
+                                              iters=3)
+    doc = json.dumps({"name": f"probe-{world}", "layers": [{"ranks": l.ranks, "p2p_gbps": l.p2p_gbps,
+                                                            "group_gbps": l.group_gbps} for l in layers],
+                      "calibration": [[d1, d2, b1, b2] for (d1, d2), (b1, b2) in sorted(calib.items())]})
+    d = json.loads(doc)
+    lay = [atp.HcmLayer(l["ranks"], l["p2p_gbps"], l["group_gbps"]) for l in d["layers"]]
+    cal = {(c[0], c[1]): (c[2], c[3]) for c in d["calibration"]}
+    hcm = cm.Hcm([cm.HcmLayer(l["ranks"], l["p2p_gbps"], l["group_gbps"]) for l in d["layers"]])
+    assert hcm.n_devices == world and len(matrix) == world
+    assert all(matrix[i][j] > 0 for i in range(world) for j in range(world) if i != j)
+    n_cmp = 0
+    for h, heads in ((4096, 32), (5120, 40), (12288, 96)):
+        m = cm.Model(L=1, b=4, s=2048, h=h, a=heads)
+        for c in (None, cal):
+            lib_plan = atp.atp_search(lay, 1, 4, 2048, h, heads, 2, calibration=c)
+            o = cm.search(hcm, m, c)
+            assert [(r["d1"], r["d2"]) for r in lib_plan["ranked"]] == [(r.d1, r.d2) for r in o.ranked]
+            for a_, b_ in zip(lib_plan["ranked"], o.ranked):
+                assert a_["t_comm"] == b_.t_comm and a_["t_f"] == list(b_.t), (a_, b_)
+            assert lib_plan["chosen"] == (o.chosen.d1, o.chosen.d2)
+            n_cmp += 1
+    return 0.0, {"plans_compared": n_cmp, "group_gbps": layers[0].group_gbps, "n_calib": len(cal)}
+
+
 def worker(rank: int, world: int, port: int, jobs: list, results) -> None:
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -116,7 +153,9 @@ def worker(rank: int, world: int, port: int, jobs: list, results) -> None:
                     mesh.set_gating(True)
                 if opts.get("fused"):
                     mesh.enable_fused_ar(opts["fused"])  # CUDA IPC peer buffers, opened across processes
-                if kind == "layer":
+                if kind == "probe":
+                    worst, dig = _probe_search(atp, mesh, world)
+                elif kind == "layer":
                     worst, dig = _layer(atp, mesh, d1, d2, rank, chunks, 43, bool(opts.get("graph")))
                 else:
                     worst, dig = _gpt(atp, mesh, d1, d2, rank, chunks, 47), {}

@@ -101,6 +101,18 @@ def test_search_calibration_p482():
     assert abs(t[(2, 4)] / t[(8, 1)] - 0.545) < 0.001
 
 
+def test_search_exact_tie_break():
+    """G8: the C++ search resolves the exact (4,1)/(2,2) tie like the oracle (larger d1)."""
+    layers = [atp.HcmLayer(4, 1e9, 1e9)]
+    cal = {(4, 1): (64.0, None), (2, 2): (64.0, 224.0), (1, 4): (1e-3, 1e-3)}
+    p = atp.atp_search(layers, calibration=cal)
+    _same_plan(p, _oracle_plan(layers, cm.Model(), cal))
+    t = {(r["d1"], r["d2"]): r["t_comm"] for r in p["ranked"]}
+    assert t[(4, 1)] == t[(2, 2)] and p["chosen"] == (4, 1)
+    cal[(2, 2)] = (64.0, 225.0)
+    assert atp.atp_search(layers, calibration=cal)["chosen"] == (2, 2)
+
+
 def test_search_errors():
     with pytest.raises(atp.AtpError) as e:
         atp.atp_search([atp.HcmLayer(4, -1.0, 1.0)])

@@ -30,9 +30,16 @@ def test_bench_json_contract_n1():
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3 and d["value"] > 0
     assert d["gpu_launches"] >= 5 * 12  # at least the 12 GEMMs of every timed step
     r = d["roofline"]
-    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "peak_burst", "peak_sustained", "peak_rule",
+              "gemm_share_of_step"):
         assert k in r, k
     assert r["bound"] == "tensor" and 0 < r["frac"] < 1.5 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-6
+    assert r["peak"] in (r["peak_burst"], r["peak_sustained"])
+    # the GEMM time comes from a CUPTI trace of the graph-launched step
+    kt = d["kernel_trace"]
+    assert "error" not in kt, kt
+    assert kt["gemm_launches_per_step"] == 12 and 0.5 < r["gemm_share_of_step"] <= 1.0
+    assert d["config"]["hidden"] == 12288 and d["config"]["heads"] == 96  # N=1 default: cfg 5 shape
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
@@ -54,7 +61,7 @@ def test_bench_n2_shared_gpu():
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                           "--gpus", "2", "--share-gpu", "--steps", "3", "--warmup", "3", "--hidden", "1024",
-                          "--heads", "8", "--batch", "2", "--seq", "1024", "--no-cpu-baseline"],
+                          "--heads", "8", "--batch", "2", "--seq", "1024", "--no-cpu-baseline", "--probe-mib", "4"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.strip()]
@@ -63,3 +70,9 @@ def test_bench_n2_shared_gpu():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["mesh"] in ([2, 1], [1, 2])
     assert d["search"]["chosen"] == d["config"]["mesh"] and "chunk_choice" in d
     assert d["exposed_comm_ms"] >= 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    # the probe ran and fed the search (calibrated) and the chunk planner (busBW)
+    assert "error" not in d["probe"] and d["probe"]["hcm"][0]["ranks"] == 2
+    assert d["chunk_choice"]["busbw_source"].startswith("probe") and d["chunk_choice"]["busbw_gbs"] > 0
+    assert "hcm_only" in d["search"]
+    mb = d.get("megatron_baseline")
+    assert mb is None or "error" not in mb, mb

@@ -131,6 +131,46 @@ def test_cfg1_mlp_2x2():
         assert rel(to_np(b["z"]), fw["z"][r]) <= TOL
 
 
+@pytest.mark.parametrize("chunks", [1, 2])
+def test_cfg1_fp32_check_mode_2x2(chunks):
+    """BASELINE.json configs[0] in its own precision: h=64, ffn=256, tokens=32,
+    fp32, DeviceMesh(2,2) -- the whole layer (fwd+bwd) and the MLP block alone
+    in the ATP_FP32 check mode, every tensor of every rank <= 1e-4 relF
+    against the fp64 oracle on the same unrounded fp32 inputs."""
+    import torch
+    import paper_2301_08658_b200 as atp
+    from gpu_util import assert_close, oracle_layer_fp32
+
+    T, h, F, heads, seed, d1, d2 = 32, 64, 256, 2, 5, 2, 2
+    g, sh, fw, bw, _ = oracle_layer_fp32(T, h, F, heads, d1, d2, chunks, seed)
+    bufs = run_gpu_layer(d1, d2, T, h, F, heads, chunks, seed, fp32=True)
+    for r, b in enumerate(bufs):
+        for k, ok in list(FWD_MAP.items()) + list(BWD_MAP.items()):
+            src = fw if k in FWD_MAP else bw
+            assert_close((r, k), to_np(b[k]), src[ok][r], FP32_TOL, tile=(32, 32))
+    check_replicas(bufs, d1, d2)
+    # the MLP block alone (atp_mlp_fwd / atp_mlp_bwd), fed the oracle's Y1 shards
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        mb = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed, fp32=True) for r in range(4)]
+        for r, b in enumerate(mb):
+            b["y1"].copy_(torch.from_numpy(fw["y1"][r]).to(torch.float32))
+            for k in ("u", "h", "z", "dy1", "dw1", "db1", "dw2", "db2"):
+                b[k].fill_(float("nan"))
+        atp.atp_mlp_fwd(mesh, mb, T, h, F, chunks)
+        atp.atp_mlp_bwd(mesh, mb, T, h, F, chunks)
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    for r, b in enumerate(mb):
+        for k in ("u", "h", "z"):
+            assert_close((r, k), to_np(b[k]), fw[k][r], FP32_TOL, tile=(32, 32))
+        for k in ("dw1", "db1", "dw2", "db2"):
+            assert_close((r, k), to_np(b[k]), bw[k][r], FP32_TOL, tile=(32, 32))
+        # dY1 from the MLP alone = dZ + dU W1^T (the attention block's input gradient comes later)
+        assert_close((r, "dy1"), to_np(b["dy1"]), bw["dy1"][r], FP32_TOL, tile=(32, 32))
+
+
 @pytest.mark.parametrize("d1,d2", [(2, 2), (4, 2), (1, 1)])
 def test_ragged_chunk_and_odd_sizes(d1, d2):
     # T/chunks = 72 rows (not a multiple of the 128-row tile), head dim 16

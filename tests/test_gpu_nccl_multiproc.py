@@ -91,6 +91,19 @@ def test_nccl_four_ranks():
             _check_replicas(res, job[1], job[2], key)
 
 
+def test_probe_to_search_four_ranks():
+    """Run S: the HCM + calibration the probe measures on a
+    4-process NCCL world, serialised as SPEC's topology JSON and read back,
+    ranked identically (bit for bit) by libatp's atp_search and the oracle's
+    search; every rank's probe agrees on the chosen mesh."""
+    res = _spawn(4, [("probe", 4, 1, 1, {})])
+    key = str(("probe", 4, 1, 1))
+    for r in range(4):
+        assert res[r][key]["digests"][r]["plans_compared"] == 6
+    digs = res[0][key]["digests"]
+    assert all(dg["group_gbps"] == digs[0]["group_gbps"] for dg in digs)  # one HCM for every rank
+
+
 def test_nccl_eight_ranks():
     """The four 8-GPU meshes of cfgs 3-5 (1x8, 2x4, 4x2, 8x1) as 8 processes."""
     jobs = [("layer", 8, 1, 2, {}), ("layer", 4, 2, 4, {"gemm_ctas": 32, "gated": True}), ("layer", 2, 4, 2, {}),

@@ -148,21 +148,33 @@ def test_scale_invariance_and_determinism():
             assert p1.chosen.t_comm <= r.t_comm
 
 
+TIE_CAL = {(4, 1): (64.0, None), (2, 2): (64.0, 224.0), (1, 4): (1e-3, 1e-3)}
+
+
 def test_tie_break_larger_d1():
-    # identical times -> larger d1 (G8): a model with h tiny makes nothing tie
-    # naturally, so force a tie via calibration
+    """G8 (P:316 is silent): exact double ties go to the larger d1.
+
+    The calibrated bandwidths are chosen so the two Eq. 2 sums tie bit for bit:
+    (4,1) with B1 = 64 GB/s gives 2Lbs*2h/B1; (2,2) with B1 = 64, B2 = 224 =
+    3.5*64 gives 2Lbs(3h/(2B2) + h/(2B1) + 4h/(2B2) + h/(2B1)) = the same value
+    mathematically, and (with h = 4096, scale 2Lbs*2 = 2^15, B1 doubled exactly)
+    the same double (asserted, not assumed).  A strictly faster (2,2) must win.
+    """
     m = cm.Model()
-    cal = {(4, 1): (100.0, None), (2, 2): None}
     hcm = flat(4, 1e9)
-    _, t41 = cm.comm_time(m, 4, 1, 100.0, None)
-    # (2,2) with B1=B2=x such that its time equals (4,1)'s: solve 7h/(2x)+2h/(2x) = 2h/100
-    x = (9 * m.h / 2) / (2 * m.h / 100.0)
-    cal = {(4, 1): (100.0, None), (2, 2): (x, x), (1, 4): (1e-3, 1e-3)}
-    plan = cm.search(hcm, m, cal)
-    _, t22 = cm.comm_time(m, 2, 2, x, x)
-    if t22 == t41:
-        assert (plan.chosen.d1, plan.chosen.d2) == (4, 1)
-    assert plan.chosen.d1 >= 2
+    _, t41 = cm.comm_time(m, 4, 1, 64.0, None)
+    _, t22 = cm.comm_time(m, 2, 2, 64.0, 224.0)
+    assert t22 == t41  # an exact tie in float64
+    plan = cm.search(hcm, m, TIE_CAL)
+    assert (plan.chosen.d1, plan.chosen.d2) == (4, 1)
+    assert [(r.d1, r.d2) for r in plan.ranked][:2] == [(4, 1), (2, 2)]
+    # break the tie by a hair in (2,2)'s favour: it must now be chosen
+    faster = dict(TIE_CAL)
+    faster[(2, 2)] = (64.0, 225.0)
+    _, t22f = cm.comm_time(m, 2, 2, 64.0, 225.0)
+    assert t22f < t41
+    plan = cm.search(hcm, m, faster)
+    assert (plan.chosen.d1, plan.chosen.d2) == (2, 2)
 
 
 def test_table2_formulas_p386():

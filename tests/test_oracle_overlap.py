@@ -74,24 +74,62 @@ def test_library_estimate_bit_exact():
             assert atp.atp_overlap_estimate(st, c, mode) == ov.simulate(st, c, mode)
 
 
-def test_chunk_planner():
-    """planner: per-stage split conserves the measured compute and the executed
-    all-reduce bytes (oracle comm_volume); more chunks win when compute is
-    chunk-invariant; the per-chunk compute penalty can make fewer chunks win."""
+def test_chunk_planner_oracle_pins():
+    """oracle.overlap.layer_stages / plan_chunks against independent facts:
+    the split conserves the measured compute; forward = 1/3 of the GEMM FLOPs
+    (fwd 24Th^2 of 72Th^2 at F = 4h, P:375 / G24); the communication equals
+    the executed ring bytes of costmodel.comm_volume (another function) at the
+    bus bandwidth; with no communication the makespan is the compute and
+    nothing is exposed; more chunks win when compute is chunk-invariant."""
     from oracle import costmodel as cm
-    from paper_2301_08658_b200 import build, planner
 
-    build.build()
     T, h, F = 8192, 4096, 16384
-    for d1, d2 in [(8, 1), (4, 2), (2, 4), (1, 1)]:
-        st = planner.layer_stages(T, h, F, d1, d2, 2.0, 725.0)
+    for d1, d2 in [(8, 1), (4, 2), (2, 4), (1, 8), (1, 1), (2, 2)]:
+        st = ov.layer_stages(T, h, F, d1, d2, 2.0, 725.0)
+        assert len(st) == 8
         assert abs(sum(s[0] + s[1] for s in st) - 2.0) < 1e-12
+        assert abs(sum(s[0] for s in st[:4]) - 2.0 / 3.0) < 1e-12
+        assert all(s[1] == 0.0 for s in st[:4]) and all(s[1] == s[0] for s in st[4:])  # dW = dX GEMM FLOPs
         ring = cm.ring_bytes_per_gpu(cm.comm_volume(d1, d2, T, h, 1))
         assert abs(sum(s[2] for s in st) - ring / 725e9 * 1e3) < 1e-9
-    c, pred = planner.choose_chunks(T, h, F, 4, 2, {1: 1.3, 2: 1.3, 4: 1.3, 8: 1.3}, 725.0)
-    assert c == 8 and pred[8] <= pred[4] <= pred[2] <= pred[1]
-    c, pred = planner.choose_chunks(T, h, F, 4, 2, {1: 1.2, 2: 1.25, 4: 1.6, 8: 2.5}, 725.0)
+        # size-1 dimensions move nothing
+        assert all(s[2] == 0.0 for i, s in enumerate(st) if (d2 == 1 and i in (0, 2, 4, 6)) or
+                   (d1 == 1 and i in (1, 3, 5, 7)))
+    c, pred = ov.plan_chunks(T, h, F, 4, 2, {1: 1.3, 2: 1.3, 4: 1.3, 8: 1.3}, 725.0)
+    assert c == 8 and pred[8][0] <= pred[4][0] <= pred[2][0] <= pred[1][0]
+    c, pred = ov.plan_chunks(T, h, F, 4, 2, {1: 1.2, 2: 1.25, 4: 1.6, 8: 2.5}, 725.0)
     assert c == 2
-    # no communication (1,1): chunking cannot help
-    c, _ = planner.choose_chunks(T, h, F, 1, 1, {1: 1.0, 2: 1.0}, 725.0)
-    assert c == 1
+    c, pred = ov.plan_chunks(T, h, F, 1, 1, {1: 1.0, 2: 1.0, 4: 0.9}, 725.0)
+    assert c == 4 and pred[1][0] == pytest.approx(1.0, rel=1e-12) and pred[4][0] == pytest.approx(0.9, rel=1e-12)
+    assert abs(pred[1][1]) < 1e-12 and abs(pred[4][1]) < 1e-12
+    c, pred = ov.plan_chunks(T, h, F, 1, 1, {1: 1.0, 2: 1.0}, 725.0)
+    assert c == 1  # tie -> fewer chunks
+
+
+def test_chunk_planner_library_bit_exact():
+    """libatp atp_layer_stages / atp_plan_chunks == the oracle, bit for bit."""
+    import paper_2301_08658_b200 as atp
+    from paper_2301_08658_b200 import build
+
+    build.build()
+    rnd = random.Random(8)
+    for _ in range(200):
+        h = rnd.choice([1024, 4096, 5120, 12288])
+        F = rnd.choice([4 * h, 2 * h])
+        T = rnd.choice([2048, 8192])
+        d1, d2 = rnd.choice([(8, 1), (4, 2), (2, 4), (1, 8), (2, 2), (1, 1), (4, 1), (1, 2)])
+        bw = rnd.choice([725.0, 900.0, 1.2, 0.97, 333.3])
+        comp = rnd.uniform(0.1, 50.0)
+        for bpe in (2, 4):
+            assert atp.atp_layer_stages(T, h, F, d1, d2, comp, bw, bpe) == ov.layer_stages(T, h, F, d1, d2, comp,
+                                                                                             bw, bpe)
+        cands = {c: rnd.uniform(0.5, 3.0) for c in rnd.sample([1, 2, 4, 8], rnd.randint(1, 4))}
+        for mode in ("signalled", "per_chunk"):
+            assert atp.atp_plan_chunks(T, h, F, d1, d2, cands, bw, mode) == ov.plan_chunks(T, h, F, d1, d2, cands,
+                                                                                          bw, mode)
+    with pytest.raises(atp.AtpError):
+        atp.atp_plan_chunks(8192, 4096, 16384, 3, 1, {1: 1.0}, 900.0)  # 4096 % 3
+    with pytest.raises(atp.AtpError):
+        atp.atp_plan_chunks(8192, 4096, 16384, 2, 1, {3: 1.0}, 900.0)  # 8192 % 3
+    with pytest.raises(atp.AtpError):
+        atp.atp_plan_chunks(8192, 4096, 16384, 2, 1, {1: 1.0}, 0.0)
