@@ -77,6 +77,10 @@ def parse():
     p.add_argument("--ffn", type=int, default=0, help="default 4*hidden")
     p.add_argument("--batch", type=int, default=4)
     p.add_argument("--seq", type=int, default=2048)
+    p.add_argument("--layers", type=int, default=0,
+                   help="linear block: stack of L layers as one pipeline (atp_layer_stack_fwd_bwd; SURVEY §8(d) "
+                        "L_bench) -- 0 = 4 at N>1 (a layer's last all-reduce overlaps the next layer's GEMM), "
+                        "1 at N=1 (no communication to overlap)")
     p.add_argument("--layer", default="linear", choices=["linear", "gpt"],
                    help="linear: the north_star linear block (default); gpt: the full pre-LN layer "
                         "(LayerNorm + causal softmax attention core, SURVEY NEXT #1)")
@@ -428,6 +432,7 @@ def main() -> None:
     F = a.ffn or 4 * h
     T = a.batch * a.seq
     gpt_mode = a.layer == "gpt"
+    L = 1 if gpt_mode else (a.layers or (4 if world > 1 else 1))
 
     def new_uid() -> bytes:
         uid = atp.atp_get_unique_id() if rank == 0 else bytes(128)
@@ -521,15 +526,23 @@ def main() -> None:
     if a.fused_ar and world > 1:
         mesh.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)  # one stage's partials [T, widest], bf16
 
-    def alloc(m1, m2):
+    def alloc(m1, m2, n_layers=None):
+        n_layers = L if n_layers is None else n_layers
         if gpt_mode:
             return atp.alloc_gpt_rank(m1, m2, rank, T, h, F, heads, dev, a.seed)
+        if n_layers > 1:  # list of per-layer buffer dicts, chained (layer l+1's x is layer l's z)
+            return atp.alloc_layer_stack(m1, m2, rank, T, h, F, dev, a.seed, n_layers)
         return atp.alloc_layer_rank(m1, m2, rank, T, h, F, dev, a.seed)
 
     def make_call(m, bb, c):
         if gpt_mode:
             return atp.GptCall(m, [bb], T, h, F, heads, a.seq, c, True)
+        if isinstance(bb, list):
+            return atp.LayerStackCall(m, [[b] for b in bb], T, h, F, heads, c)
         return atp.LayerCall(m, [bb], T, h, F, heads, c, True)
+
+    first = lambda bb: bb[0] if isinstance(bb, list) else bb  # the stack's input layer
+    last = lambda bb: bb[-1] if isinstance(bb, list) else bb  # ... and output layer
 
     bufs = alloc(d1, d2)
 
@@ -550,7 +563,7 @@ def main() -> None:
         for c in (1, 2, 4, 8):
             if T % c or (T // c) % 8:
                 continue
-            cc = atp.LayerCall(mesh, [bufs], T, h, F, heads, c, True)
+            cc = make_call(mesh, bufs, c)
             for _ in range(2):
                 cc(stream)
             comp[c] = timed(5, cc)
@@ -610,7 +623,7 @@ def main() -> None:
                 mesh_f = make_mesh(d1, d2)
                 meshes.append(mesh_f)
                 mesh_f.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
-                call_f = atp.LayerCall(mesh_f, [bufs], T, h, F, heads, chunks, True)
+                call_f = make_call(mesh_f, bufs, chunks)
                 note_f = "direct calls (fused peer-memory mesh keeps cross-rank state: no graph capture)"
                 for gated in (False, True):
                     mesh_f.set_gating(gated)
@@ -643,8 +656,8 @@ def main() -> None:
     clocks = sampler.stop(t0, t1)
     launches = int(n1.value - n0.value)
 
-    fl = gpt_flops(T, h, F, a.seq) if gpt_mode else layer_flops(T, h, F)
-    gemm_fl = layer_flops(T, h, F) / world  # the GEMM FLOPs of one rank per step
+    fl = gpt_flops(T, h, F, a.seq) if gpt_mode else L * layer_flops(T, h, F)
+    gemm_fl = L * layer_flops(T, h, F) / world  # the GEMM FLOPs of one rank per step
     value = fl / (ms * 1e-3) / 1e12
     per_gpu = value / world
 
@@ -732,6 +745,21 @@ def main() -> None:
             "attention_tflops": (prof.flops[3] / n_ev) / (att_ms * 1e-3) / 1e12 if att_ms > 0 else None,
             "attention_share_of_step": att_ms / ms_prof if ms_prof > 0 else None})
 
+    # ---- the stack against one layer per call ("Headline =
+    # steady-state per layer; L=1 is also reported")
+    single = None
+    if L > 1:
+        try:
+            b1 = alloc(d1, d2, 1)
+            c1 = make_call(mesh, b1, chunks)
+            for _ in range(3):
+                c1(stream)
+            ms1 = timed(max(5, a.steps // 2), as_graph(mesh, c1))
+            single = {"ms_per_step": ms1, "ms_per_layer_in_stack": ms / L, "stack_gain": ms1 / (ms / L)}
+            del b1
+        except Exception as e:  # noqa: BLE001
+            single = {"error": str(e)}
+
     # ---- Megatron-style baseline (north_star): the same library on DeviceMesh(N,1), 1 chunk
     baseline = None
     if world > 1 and not a.no_baseline and not gpt_mode and ((d1, d2) != (world, 1) or chunks != 1):
@@ -747,7 +775,7 @@ def main() -> None:
             _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mb.handle, 0))
             ms_b0 = timed(max(10, a.steps // 2), cb)
             _abi.check(_abi.lib().atp_mesh_set_comm_enabled(mb.handle, 1))
-            baseline = {"mesh": [world, 1], "chunks": 1, "ms_per_step": ms_b,
+            baseline = {"mesh": [world, 1], "chunks": 1, "layers": L, "ms_per_step": ms_b,
                         "tflops_per_gpu": fl / (ms_b * 1e-3) / 1e12 / world,
                         "exposed_comm_ms": max(0.0, ms_b - ms_b0), "ms_per_step_comm_disabled": ms_b0,
                         "speedup_of_atp_step": ms_b / ms}
@@ -760,13 +788,18 @@ def main() -> None:
     # double-buffered: step i+1's copy runs on a copy stream while step i computes.
     e2e = None
     if not a.no_e2e:
-        hx = bufs["x"].cpu().pin_memory()
-        hdz = bufs["dz"].cpu().pin_memory()
-        res = [bufs[k] for k in ("dbqkv", "dbo", "db1", "db2")]
+        hx = first(bufs)["x"].cpu().pin_memory()
+        hdz = last(bufs)["dz"].cpu().pin_memory()
+        res = [first(bufs)[k] for k in ("dbqkv", "dbo", "db1", "db2")]
         hres = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res]
         h2d = hx.numel() * hx.element_size() + hdz.numel() * hdz.element_size()
         d2h = sum(r.numel() * r.element_size() for r in res)
-        bufs_b = dict(bufs, x=torch.empty_like(bufs["x"]), dz=torch.empty_like(bufs["dz"]))
+        if isinstance(bufs, list):  # second input set: own x (layer 0) and dz (last layer), the rest shared
+            bufs_b = [dict(b) for b in bufs]
+            bufs_b[0]["x"] = torch.empty_like(bufs[0]["x"])
+            bufs_b[-1]["dz"] = torch.empty_like(bufs[-1]["dz"])
+        else:
+            bufs_b = dict(bufs, x=torch.empty_like(bufs["x"]), dz=torch.empty_like(bufs["dz"]))
         sets = [(bufs, run), (bufs_b, as_graph(mesh, make_call(mesh, bufs_b, chunks)) if run is not call else
                                   make_call(mesh, bufs_b, chunks))]
         copy_stream = torch.cuda.Stream()
@@ -775,8 +808,8 @@ def main() -> None:
 
         def run_e2e(n):
             with torch.cuda.stream(copy_stream):
-                sets[0][0]["x"].copy_(hx, non_blocking=True)
-                sets[0][0]["dz"].copy_(hdz, non_blocking=True)
+                first(sets[0][0])["x"].copy_(hx, non_blocking=True)
+                last(sets[0][0])["dz"].copy_(hdz, non_blocking=True)
                 copied[0].record(copy_stream)
             for i in range(n):
                 cur, nxt = i % 2, (i + 1) % 2
@@ -789,8 +822,8 @@ def main() -> None:
                     with torch.cuda.stream(copy_stream):
                         if i >= 1:
                             copy_stream.wait_event(done[nxt])
-                        sets[nxt][0]["x"].copy_(hx, non_blocking=True)
-                        sets[nxt][0]["dz"].copy_(hdz, non_blocking=True)
+                        first(sets[nxt][0])["x"].copy_(hx, non_blocking=True)
+                        last(sets[nxt][0])["dz"].copy_(hdz, non_blocking=True)
                         copied[nxt].record(copy_stream)
 
         run_e2e(3)
@@ -828,8 +861,11 @@ def main() -> None:
                                     f"fwd+bwd) h{h} a{heads} ffn{F} s{a.seq} b{a.batch}, DeviceMesh({d1},{d2}), "
                                     f"chunks {chunks}") if gpt_mode else
                                    (f"gpt-layer linear block (QKV/Out/FC1/FC2 fwd+bwd) h{h} a{heads} ffn{F} "
-                                    f"s{a.seq} b{a.batch} ({cfg_name}), DeviceMesh({d1},{d2}), chunks {chunks}"),
-                       "mesh": [d1, d2], "chunks": chunks, "tokens": T, "hidden": h, "heads": heads, "ffn": F,
+                                    f"s{a.seq} b{a.batch} ({cfg_name}), DeviceMesh({d1},{d2}), chunks {chunks}"
+                                    + (f", stack of {L} layers as one pipeline (value counts all {L})" if L > 1
+                                       else "")),
+                       "mesh": [d1, d2], "chunks": chunks, "layers": L, "tokens": T, "hidden": h, "heads": heads,
+                       "ffn": F, "nccl_max_ctas": int(os.environ.get("ATP_NCCL_MAX_CTAS", "16")),
                        "parallelism": f"atp{d1}x{d2}", "gemm_ctas": ctas,
                        "allreduce": ("fused peer-memory kernel" if ((a.fused_ar or str((ar_choice or {}).get("chosen", "")).startswith("fused"))
                                                                     and world > 1) else "nccl"),
@@ -850,6 +886,9 @@ def main() -> None:
             out["allreduce_choice"] = ar_choice
         if baseline is not None:
             out["megatron_baseline"] = baseline
+        if single is not None:
+            out["single_layer"] = single
+        out["ms_per_layer"] = ms / L
         if probe is not None:
             out["probe"] = probe
         if gpt_mode:

@@ -116,17 +116,24 @@ atp_status atp_mesh_set_gemm_ctas(atp_mesh* mesh, int max_ctas);
  * Same results.  Errors: ATP_ERR_INVALID (NULL mesh). */
 atp_status atp_mesh_set_gating(atp_mesh* mesh, int enabled);
 
-/* Fused all-reduce over peer memory (opt-in).  Allocates this rank's
- * peer-visible buffer (`part_bytes` for one stage's partial sums [T, width]
- * bf16, plus counters) and maps the buffers of its dim-1 and dim-2 group
- * members (CUDA IPC handles all-gathered over the world communicator; a
- * virtual mesh uses the other virtual ranks' buffers).  Collective on a
- * distributed mesh.  Afterwards every communicating bf16 stage whose output
- * fits runs as: signalled GEMM into the buffer, then per chunk ONE kernel that
- * all-reduces over peer memory (reduce-scatter by row slice + pull
- * all-gather, 2(p-1)/p of the chunk per member) and applies the
- * post-all-reduce elementwise step — no NCCL call on the data path.
- * Errors: ATP_ERR_INVALID (already enabled), ATP_ERR_CUDA, ATP_ERR_NCCL. */
+/* Fused GEMM -> all-reduce -> elementwise stages over peer memory (opt-in;
+ * PAPER.md §4.1 P:337 names GEMM/all-reduce fusion as the alternative to
+ * chunking — here the two compose).  Allocates this rank's peer-visible
+ * buffer (two receive regions of `part_bytes` each — one stage's [T, width]
+ * bf16, laid out as p sender slots of T/p rows — plus counters) and maps the
+ * buffers of its dim-1 and dim-2 group members (CUDA IPC handles all-gathered
+ * over the world communicator; a virtual mesh uses the other virtual ranks'
+ * buffers).  Collective on a distributed mesh.  Afterwards every
+ * communicating bf16 stage whose chunk splits into p slices of whole 128-row
+ * tiles (p <= 8) runs as: the GEMM stores each output tile with TMA straight
+ * into the receive slot of the member owning the tile's row slice (the
+ * reduce-scatter's data movement, tile by tile, over NVLink) and counts it on
+ * that member's chunk counter; then per chunk ONE kernel per member sums its
+ * slice of the p partials, applies the post-all-reduce elementwise step, and
+ * pulls the other members' reduced slices with bulk copies (all-gather) —
+ * 2(p-1)/p of the chunk per member, no NCCL call on the data path.  Stages
+ * that do not qualify use the NCCL path.  Errors: ATP_ERR_INVALID (already
+ * enabled, or a mesh dimension above 16), ATP_ERR_CUDA, ATP_ERR_NCCL. */
 atp_status atp_mesh_enable_fused_ar(atp_mesh* mesh, size_t part_bytes);
 
 /* Measurement hooks (bench.py).  atp_mesh_set_comm_enabled(mesh, 0) replaces
@@ -352,6 +359,19 @@ typedef struct {
 atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t T, int64_t h,
                              int64_t F, int64_t heads, int chunks, int do_backward,
                              atp_dtype dtype, void* stream);
+
+/* A stack of n_layers identical-shape layers, forward 0..n-1 then backward
+ * n-1..0, as ONE chunk pipeline (SURVEY §8(d) L_bench; Fig. 7): layer
+ * l+1's first GEMM waits only on layer l's last stage, so a layer's last
+ * all-reduce overlaps the next layer's first GEMM instead of draining at a
+ * call boundary.  args = [n_layers][local ranks] (layer-major).  Chaining
+ * (checked, ATP_ERR_INVALID otherwise): layer l+1's attn.x is layer l's
+ * mlp.z, and layer l's mlp_b.dz is layer l+1's attn_b.dx (the gradient of
+ * its input); each layer also satisfies atp_layer_fwd_bwd's rules.  Same
+ * shapes / errors as atp_layer_fwd_bwd; backward always runs. */
+atp_status atp_layer_stack_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int n_layers, int64_t T,
+                                   int64_t h, int64_t F, int64_t heads, int chunks, atp_dtype dtype,
+                                   void* stream);
 
 /* ------------------------------------------------------------------ workspace sizes
  * Bytes of every caller-allocated workspace buffer of an op, in the order the

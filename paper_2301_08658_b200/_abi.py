@@ -154,6 +154,8 @@ SIGNATURES = {
     "atp_attn_proj_fwd": (C.c_int, [vp, C.POINTER(AttnFwdArgs), i64, i64, i64, C.c_int, C.c_int, C.c_int, vp]),
     "atp_attn_proj_bwd": (C.c_int, [vp, C.POINTER(AttnBwdArgs), i64, i64, i64, C.c_int, C.c_int, C.c_int, vp]),
     "atp_layer_fwd_bwd": (C.c_int, [vp, C.POINTER(LayerArgs), i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp]),
+    "atp_layer_stack_fwd_bwd": (C.c_int, [vp, C.POINTER(LayerArgs), C.c_int, i64, i64, i64, i64, C.c_int, C.c_int,
+                                          vp]),
     "atp_search": (C.c_int, [C.POINTER(Hcm), C.POINTER(Model), C.c_int, C.POINTER(Calib), C.POINTER(Plan)]),
     "atp_effective_bandwidth": (C.c_int, [C.POINTER(Hcm), C.c_int, C.c_int, C.POINTER(C.c_double),
                                           C.POINTER(C.c_double)]),

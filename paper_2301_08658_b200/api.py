@@ -325,6 +325,37 @@ def atp_layer_fwd_bwd(mesh, bufs, T, h, F, heads, chunks=1, backward=True, strea
     LayerCall(mesh, bufs, T, h, F, heads, chunks, backward)(stream)
 
 
+def alloc_layer_stack(d1: int, d2: int, rank: int, T: int, h: int, F: int, device, seed: int, n_layers: int,
+                      **kw) -> list[dict]:
+    """One rank's buffers of an n-layer stack (layer l's weights from seed + l):
+    layer l+1's input x IS layer l's output z, and layer l's upstream gradient
+    dz IS layer l+1's input gradient dx (atp_layer_stack_fwd_bwd's chaining)."""
+    st = [alloc_layer_rank(d1, d2, rank, T, h, F, device, seed + l, **kw) for l in range(n_layers)]
+    for l in range(1, n_layers):
+        st[l]["x"] = st[l - 1]["z"]
+    for l in range(n_layers - 1):
+        st[l]["dz"] = st[l + 1]["dx"]
+    return st
+
+
+class LayerStackCall:
+    """Pre-marshalled atp_layer_stack_fwd_bwd: stack[l][i] = layer l's buffers of local rank i."""
+
+    def __init__(self, mesh, stack, T, h, F, heads, chunks=1):
+        self.mesh = mesh
+        self.n_layers = len(stack)
+        self.args = _arr(_abi.LayerArgs, [_abi.LayerArgs(_attn_fwd(b), _mlp_fwd(b), _mlp_bwd(b), _attn_bwd(b))
+                                          for layer in stack for b in layer])
+        self.dims = (T, h, F, heads, chunks)
+        self.dtype = _dt(stack[0][0]["x"])
+        self._f = lib().atp_layer_stack_fwd_bwd
+
+    def __call__(self, stream=None):
+        T, h, F, heads, chunks = self.dims
+        check(self._f(self.mesh.handle, self.args, self.n_layers, T, h, F, heads, chunks, self.dtype,
+                      _stream(stream)))
+
+
 # ------------------------------------------------------------------ workspace sizes
 ATP_OP_MLP_BWD, ATP_OP_ATTN_BWD, ATP_OP_LAYER, ATP_OP_GPT_LAYER = 0, 1, 2, 3
 

@@ -505,6 +505,39 @@ atp_status atp_layer_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int64_t
   });
 }
 
+atp_status atp_layer_stack_fwd_bwd(atp_mesh* mesh, const atp_layer_args* args, int n_layers, int64_t T, int64_t h,
+                                   int64_t F, int64_t heads, int chunks, atp_dtype dtype, void* stream) {
+  atp_status s = check_mesh(mesh, args);
+  if (s) return s;
+  if (n_layers < 1) return fail(ATP_ERR_INVALID, "layer stack: n_layers must be >= 1");
+  if (dtype != ATP_BF16 && dtype != ATP_FP32) return fail(ATP_ERR_UNSUPPORTED, "layer stack: dtype must be ATP_BF16 or ATP_FP32");
+  if ((s = check_layer_shapes(mesh, T, h, F, heads, chunks, true, true))) return s;
+  const int n = n_ranks(mesh);
+  for (int l = 0; l < n_layers; ++l)
+    for (int r = 0; r < n; ++r) {
+      const auto& a = args[l * n + r];
+      if (a.mlp.x != a.attn.y || a.attn_b.dy != a.mlp_b.dx || a.mlp_b.x != a.attn.y)
+        return fail(ATP_ERR_INVALID, "layer stack: each layer must chain as in atp_layer_fwd_bwd");
+      if (l + 1 < n_layers) {
+        const auto& nx = args[(l + 1) * n + r];
+        if (nx.attn.x != a.mlp.z || a.mlp_b.dz != nx.attn_b.dx)
+          return fail(ATP_ERR_INVALID, "layer stack: layer l+1 attn.x must be layer l mlp.z and layer l mlp_b.dz "
+                                       "must be layer l+1 attn_b.dx");
+      }
+    }
+  return run(mesh, stream, [&](const atp::RankView& rv, int r, Sched& out) {
+    std::vector<atp::LayerParts> parts(n_layers);
+    for (int l = 0; l < n_layers; ++l) {
+      const auto& a = args[l * n + r];
+      parts[l].attn_fwd = &a.attn;
+      parts[l].mlp_fwd = &a.mlp;
+      parts[l].mlp_bwd = &a.mlp_b;
+      parts[l].attn_bwd = &a.attn_b;
+    }
+    return atp::build_layer_stack(rv, parts.data(), n_layers, T, h, F, heads, chunks, dtype, out);
+  });
+}
+
 // ---------------------------------------------------------------- workspace sizes
 atp_status atp_workspace_size(int op, int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq,
                               int chunks, size_t bytes[4]) {

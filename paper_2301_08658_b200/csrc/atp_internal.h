@@ -27,6 +27,20 @@ struct EpiParams {
   int64_t ldc2 = 0;
 };
 
+// Fused GEMM -> reduce-scatter (fused peer-memory all-reduce stages,
+// fused_ar.cu): instead of storing its partial sums locally, the epilogue
+// stores each 128-row CTA tile with TMA straight into the receive slot of the
+// member that owns the tile's row slice (slice j of a chunk = rows
+// [k*Mc + j*S, k*Mc + (j+1)*S), S = Mc / p), over NVLink for peers, and
+// counts the tile on that member's chunk counter (release, system scope).
+constexpr int kMaxPush = 8;
+struct PushArgs {
+  CUtensorMap tm[kMaxPush];      // member j's receive slot for this rank: [slot rows, N] bf16, 32-row store boxes
+  uint32_t* sig[kMaxPush] = {};  // member j's tile counter of this stage's chunk 0
+  int p = 0;                     // group size; 0 = ordinary stores into ep.C
+  int slice_rows = 0;            // S
+};
+
 struct GemmDesc {
   alignas(64) CUtensorMap tmA;
   alignas(64) CUtensorMap tmB;
@@ -54,6 +68,8 @@ struct GemmDesc {
   // sole dependency is the previous kernel of its stream and it spins on no
   // gate: an early-launched CTA must never hold SMs another stream needs).
   bool pdl = false;
+  // fused GEMM -> reduce-scatter (push.p > 0; needs sig / sig_rows)
+  PushArgs push;
   // fp32 check mode (gemm_f32.cu): dtype 1, raw operands instead of TMA maps
   int dtype = 0;
   const void* A = nullptr;
@@ -79,6 +95,9 @@ int raster_group_m(int rows_per_mtile, int N, int K);
 // box [box_rows, box_cols], 128B swizzle, out-of-bounds reads as zero.
 bool tmap_bf16_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                   int box_cols);
+// Epilogue TMA-store map: [rows, cols] (pitch ld elements of esz bytes), box
+// [32 rows][box_cols] with the swizzle of the box row (32 or 64 bytes).
+bool make_tmap_out(CUtensorMap* m, const void* ptr, int esz, int64_t rows, int64_t cols, int64_t ld, int box_cols);
 // Same for fp32 (box_cols * 4 <= 128 bytes).
 bool tmap_f32_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                  int box_cols);

@@ -1,28 +1,36 @@
-// Fused grouped all-reduce over peer memory (opt-in "fused" stages).
+// Fused grouped all-reduce over peer memory (opt-in "fused" stages), the
+// collective half of a fused GEMM -> all-reduce -> elementwise stage.
 //
-// One kernel per chunk k of a communicating stage, on the communication
-// stream, replaces ncclAllReduce(chunk k) + the post-all-reduce elementwise
-// step.  Every member of the mesh-dimension group has written its partial
-// sums of the stage into its peer-visible ("symmetric") buffer with the
-// signalled GEMM, which counts finished tiles per chunk.  With p members and
-// the chunk's rows cut into p row slices (slice j owned by member j):
+// PAPER.md §4.1 contrasts ATP's chunking with fusing the GEMM and its
+// all-reduce; on NVSwitch both compose: the stage's GEMM (gemm_sm100.cu,
+// PushArgs) already performs the reduce-scatter's data movement — each
+// 128-row output tile is TMA-stored straight into the receive slot of the
+// member that owns the tile's row slice and counted on that member's chunk
+// counter (release, system scope).  Then, per chunk k, ONE kernel per member j
+// on the communication stream (two launches: phase A, then B + C):
 //
-//   1. wait until every member's tile counter for chunk k is complete;
-//   2. reduce-scatter: member j sums slice j of all p partial buffers (fixed
-//      member order, fp32) and writes the bf16 sum in place into slice j of
-//      its own buffer, then bumps its `ready` counter;
-//   3. all-gather by pull: every member copies each slice j from member j's
-//      buffer into its own output rows and applies the stage's elementwise
-//      step (GeLU / dGeLU / residual / attention stand-in core) on the way;
-//   4. every CTA bumps every member's `done` counter; CTA 0 waits for all
-//      members' CTAs, so when the kernel retires nobody reads this member's
-//      buffer any more and the next GEMM may overwrite it.
+//   A. reduce: waits for chunk k's tiles from all p senders, streams its
+//      slice of the p partials (and the elementwise step's side input) through
+//      a shared-memory ring filled by 1-D bulk copies, sums them in member
+//      order (fp32, one bf16 rounding), writes the sum back in place (its own
+//      slot) for the peers to pull, applies the stage's elementwise step
+//      (GeLU / dGeLU / residual / stand-in core) and writes its slice of the
+//      outputs; publishes `ready`;
+//   B. all-gather by pull: for every other member, once it is ready, streams
+//      that member's reduced slice through the same ring (bulk copies over
+//      NVLink: kFusedStages x kFusedStageBytes in flight per CTA, so the pull
+//      is bandwidth- not latency-bound) and applies the elementwise step on
+//      the way into the local outputs;
+//   C. tells every member it is done reading; CTA 0 retires only when every
+//      member is done with this member's slice.
 //
-// Bytes moved over NVLink per member: 2(p-1)/p of the chunk (ring-optimal),
-// with the elementwise pass fused into the gather.  Peers are other GPUs'
-// buffers mapped with CUDA IPC (distributed mesh) or other virtual ranks'
-// buffers on the same GPU (virtual mesh).  Counters use cumulative targets
-// computed on the host, so they are never reset.
+// NVLink bytes per member and chunk: (p-1)/p of the chunk pushed by the GEMM
+// + (p-1)/p pulled = the ring all-reduce's 2(p-1)/p, with no NCCL call, no
+// local partial-sum round trip through HBM for the pushed tiles, and no
+// separate elementwise pass.  Peers are other GPUs' buffers mapped with CUDA
+// IPC (distributed mesh) or other virtual ranks' buffers on the same GPU
+// (virtual mesh).  Counters use cumulative targets computed on the host, so
+// they are never reset.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -32,13 +40,13 @@
 #include "elementwise.h"
 #include "fused_ar.h"
 #include "gelu.cuh"
+#include "sm100_ptx.cuh"
 
 namespace atp {
 
 namespace {
 
-__device__ __forceinline__ float gelu_f(float x) { return gelu::gelu(x); }  // bf16 path (gelu.cuh)
-__device__ __forceinline__ float gelu_grad_f(float x) { return gelu::gelu_grad(x); }
+using bf = __nv_bfloat16;
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
@@ -50,9 +58,11 @@ __device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t target) {
   while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) {
   }
 }
+__device__ __forceinline__ void red_release_sys(uint32_t* p) {
+  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
 
-__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
-  const uint4 u = *reinterpret_cast<const uint4*>(p);
+__device__ __forceinline__ void unpack8(const uint4 u, float (&f)[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -61,117 +71,257 @@ __device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
     f[2 * i + 1] = t.y;
   }
 }
-__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+__device__ __forceinline__ void lds8(uint32_t addr, float (&f)[8]) {
+  uint4 u;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(addr));
+  unpack8(u, f);
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   uint4 u;
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
-  *reinterpret_cast<uint4*>(p) = u;
+  return u;
+}
+__device__ __forceinline__ void store8(bf* p, const float (&f)[8]) { *reinterpret_cast<uint4*>(p) = pack8(f); }
+// the all-reduced value as the bf16 collective delivers it
+__device__ __forceinline__ void round8(float (&f)[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = __bfloat162float(__float2bfloat16_rn(f[e]));
 }
 
-__global__ void __launch_bounds__(512) fused_ar_kernel(FusedArArgs a) {
-  using bf = __nv_bfloat16;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t w8 = a.width / 8;
-  auto part = [&](int m, int64_t row) {  // member m's partial row (global row index)
-    return reinterpret_cast<bf*>(a.peer_base[m] + a.part_off) + row * a.ld;
+// The stage's elementwise step on 8 all-reduced values v at (global row g,
+// column c8); x = the step's side input at the same position (residual /
+// saved U), staged in shared memory with v.  Writes the stage output (`out`)
+// and the step's own output.
+__device__ __forceinline__ void finish8(const FusedArArgs& a, int64_t g, int64_t c8, float (&v)[8],
+                                        const float (&x)[8]) {
+  switch (a.ew_kind) {
+    case EW_GELU: {  // out = U (all-reduced), ew_out = H = GeLU(U)
+      float h[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) h[e] = gelu::gelu(v[e]);
+      store8(static_cast<bf*>(a.ew_out) + g * a.ew_ld + c8, h);
+      break;
+    }
+    case EW_DGELU:  // out = dU = dH * GeLU'(U)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] *= gelu::gelu_grad(x[e]);
+      break;
+    case EW_ADD:  // out = residual + all-reduced
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = x[e] + v[e];
+      break;
+    case EW_CORE_BWD: {  // dQ = dK = dV = dctx of the head
+      const int64_t hd = c8 / a.head_dim, jj = c8 % a.head_dim;
+      bf* dst = static_cast<bf*>(a.ew_out) + g * a.ew_ld + hd * 3 * a.head_dim + jj;
+      store8(dst, v);
+      store8(dst + a.head_dim, v);
+      store8(dst + 2 * a.head_dim, v);
+      break;
+    }
+    default:
+      break;
+  }
+  store8(static_cast<bf*>(a.out) + g * a.ld + c8, v);
+}
+
+// Stand-in core forward (ctx = Q + K + V per head): q, k, v vectors at column
+// col_q (q), +d (k), +2d (v) of row g.
+__device__ __forceinline__ void finish_core(const FusedArArgs& a, int64_t g, int64_t col_q, const float (&q)[8],
+                                            const float (&k)[8], const float (&v)[8]) {
+  const int64_t d = a.head_dim;
+  bf* orow = static_cast<bf*>(a.out) + g * a.ld;
+  store8(orow + col_q, q);
+  store8(orow + col_q + d, k);
+  store8(orow + col_q + 2 * d, v);
+  float c[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) c[e] = (q[e] + k[e]) + v[e];
+  const int64_t hd = col_q / (3 * d), jj = col_q % (3 * d);
+  store8(static_cast<bf*>(a.ew_out) + g * a.ew_ld + hd * d + jj, c);
+}
+
+// One pass over the byte range [b_lo, b_hi) of `nbuf` equally laid-out
+// sources, piece by piece through the shared-memory ring: thread 0 keeps
+// kFusedStages pieces in flight (one bulk copy per source and piece, one
+// mbarrier per stage); every thread runs process(stage, off, nbytes) on each
+// landed piece (source b's bytes at stage + b * piece).
+template <class F>
+__device__ __forceinline__ void stream_pieces(uint32_t sbase, uint32_t bar0, uint32_t& consumed, int nbuf,
+                                              const char* const* src, int64_t piece, int64_t b_lo, int64_t b_hi,
+                                              F&& process) {
+  const int np = b_hi > b_lo ? static_cast<int>((b_hi - b_lo + piece - 1) / piece) : 0;
+  const uint32_t base_count = consumed;
+  auto issue = [&](int q) {
+    const uint32_t st = (base_count + q) % kFusedStages;
+    const int64_t off = b_lo + static_cast<int64_t>(q) * piece;
+    const uint32_t bytes = static_cast<uint32_t>(min(piece, b_hi - off));
+    ptx::mbar_arrive_expect_tx(bar0 + 8u * st, bytes * static_cast<uint32_t>(nbuf));
+    for (int b = 0; b < nbuf; ++b)
+      ptx::bulk_load_1d(sbase + st * kFusedStageBytes + static_cast<uint32_t>(b * piece), src[b] + off, bytes,
+                        bar0 + 8u * st);
   };
-  auto slice_begin = [&](int j) { return a.row0 + (a.rows * j) / a.p; };
-
-  // ---- 1. every member's GEMM has finished chunk k
-  if (tid == 0)
-    for (int m = 0; m < a.p; ++m) spin_geq(reinterpret_cast<const uint32_t*>(a.peer_base[m] + a.flag_off) + a.sig_slot, a.sig_target);
-  __syncthreads();
-
-  // ---- 2. reduce-scatter: my slice, summed over members in member order, in place
-  {
-    const int64_t r0 = slice_begin(a.me), r1 = slice_begin(a.me + 1);
-    const int64_t n = (r1 - r0) * w8;
-    for (int64_t i = blockIdx.x * (int64_t)nt + tid; i < n; i += (int64_t)gridDim.x * nt) {
-      const int64_t row = r0 + i / w8, c8 = (i % w8) * 8;
-      float acc[8], v[8];
-      load8(part(0, row) + c8, acc);
-      for (int m = 1; m < a.p; ++m) {
-        load8(part(m, row) + c8, v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += v[e];
-      }
-      store8(part(a.me, row) + c8, acc);
-    }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < np && q < kFusedStages; ++q) issue(q);
+  for (int q = 0; q < np; ++q) {
+    const uint32_t st = consumed % kFusedStages;
+    ptx::mbar_wait(bar0 + 8u * st, (consumed / kFusedStages) & 1u);
+    const int64_t off = b_lo + static_cast<int64_t>(q) * piece;
+    process(sbase + st * kFusedStageBytes, off, min(piece, b_hi - off));
+    __syncthreads();  // every thread is done with this stage
+    if (threadIdx.x == 0 && q + kFusedStages < np) issue(q + kFusedStages);
+    ++consumed;
   }
-  __syncthreads();
+}
+
+// PHASE 0 = A (needs only the GEMMs' tiles), PHASE 1 = B + C (needs the
+// peers' phase A).  Two launches per chunk: a CTA that spins on a peer never
+// holds an SM that a phase-A CTA of its own rank needs, so partially resident
+// grids on different ranks cannot wait on each other in a cycle.
+template <int PHASE>
+__global__ void __launch_bounds__(kFusedThreads, 2) fused_ar_kernel(FusedArArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const bool core = a.ew_kind == EW_CORE_FWD;
+  const bool side = a.ew_kind == EW_ADD || a.ew_kind == EW_DGELU;  // side input staged with the values
+  const int64_t S = a.rows / a.p, w8 = a.width / 8, d = a.head_dim;
+  const int64_t row_bytes = a.ld * 2;
+  const uint32_t sbase = (ptx::smem_u32(smem_raw) + 127u) & ~127u;
+  const uint32_t bar0 = sbase + kFusedStages * kFusedStageBytes;
   uint32_t* my_flags = reinterpret_cast<uint32_t*>(a.peer_base[a.me] + a.flag_off);
+  const char* mine = a.peer_base[a.me] + a.part_off;
+  const int64_t r0 = a.chunk * S, g0 = a.row0 + static_cast<int64_t>(a.me) * S;
+  // this CTA's byte range of a slice (S rows): whole units (core: whole (q, k, v) head triples)
+  const int64_t unit = core ? 3 * d * 2 : 16;
+  const int64_t n_units = S * a.width * 2 / unit;
+  const int64_t b_lo = n_units * blockIdx.x / gridDim.x * unit;
+  const int64_t b_hi = n_units * (blockIdx.x + 1) / gridDim.x * unit;
+  const int nbuf_a = a.p + (side ? 1 : 0);
+  const int64_t piece = (kFusedStageBytes / nbuf_a / unit) * unit;
+  const char* ewa = static_cast<const char*>(a.ew_a);
+  uint32_t consumed = 0;
   if (tid == 0) {
-    __threadfence_system();
-    atomicAdd(my_flags + kSigSlots + a.sig_slot, 1u);  // ready
-  }
-
-  // ---- 3. all-gather by pull + the stage's elementwise step: a flat
-  // grid-stride loop over (row, 8-column vector) pairs of each slice.  For the
-  // stand-in core the loop runs over ctx vectors and pulls the q, k, v vectors
-  // of the head (each is written exactly once), so no intra-row sync is needed.
-  const bool core_fwd = a.ew_kind == EW_CORE_FWD;
-  const int64_t vec_per_row = core_fwd ? a.ew_width / 8 : w8;
-  for (int j = 0; j < a.p; ++j) {
-    if (tid == 0)
-      spin_geq(reinterpret_cast<const uint32_t*>(a.peer_base[j] + a.flag_off) + kSigSlots + a.sig_slot, a.ready_target);
-    __syncthreads();
-    const int64_t r0 = slice_begin(j), r1 = slice_begin(j + 1);
-    const int64_t n = (r1 - r0) * vec_per_row;
-    for (int64_t i = blockIdx.x * (int64_t)nt + tid; i < n; i += (int64_t)gridDim.x * nt) {
-      const int64_t row = r0 + i / vec_per_row, c8 = (i % vec_per_row) * 8;
-      bf* orow = static_cast<bf*>(a.out) + row * a.ld;
-      const bf* src = part(j, row);
-      if (core_fwd) {
-        const int64_t hd = c8 / a.head_dim, jj = c8 % a.head_dim;
-        const int64_t q = hd * 3 * a.head_dim + jj;
-        float x[8], k[8], v[8];
-        load8(src + q, x);
-        load8(src + q + a.head_dim, k);
-        load8(src + q + 2 * a.head_dim, v);
-        store8(orow + q, x);
-        store8(orow + q + a.head_dim, k);
-        store8(orow + q + 2 * a.head_dim, v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = (x[e] + k[e]) + v[e];
-        store8(static_cast<bf*>(a.ew_out) + row * a.ew_ld + c8, x);
-        continue;
-      }
-      float v[8];
-      load8(src + c8, v);  // the all-reduced (bf16) values
-      if (a.ew_kind == EW_GELU) {
-        float h[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) h[e] = gelu_f(v[e]);
-        store8(static_cast<bf*>(a.ew_out) + row * a.ew_ld + c8, h);
-      } else if (a.ew_kind == EW_DGELU) {
-        float u[8];
-        load8(static_cast<const bf*>(a.ew_a) + row * a.ew_lda + c8, u);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] *= gelu_grad_f(u[e]);
-      } else if (a.ew_kind == EW_ADD) {
-        float x[8];
-        load8(static_cast<const bf*>(a.ew_a) + row * a.ew_lda + c8, x);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = x[e] + v[e];
-      } else if (a.ew_kind == EW_CORE_BWD) {
-        // dQ = dK = dV = dctx of the head (row-local)
-        const int64_t hd = c8 / a.head_dim, jj = c8 % a.head_dim;
-        bf* dst = static_cast<bf*>(a.ew_out) + row * a.ew_ld + hd * 3 * a.head_dim + jj;
-        store8(dst, v);
-        store8(dst + a.head_dim, v);
-        store8(dst + 2 * a.head_dim, v);
-      }
-      store8(orow + c8, v);
+    for (int s = 0; s < kFusedStages; ++s) ptx::mbar_init(bar0 + 8u * s, 1);
+    ptx::fence_barrier_init();
+    if (PHASE == 0) {
+      spin_geq(my_flags + a.sig_slot, a.sig_target);  // every sender's tiles of my slice have landed
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
   }
+  __syncthreads();
 
-  // ---- 4. nobody reads my buffer once every member's CTAs are done
+  // ---- A. reduce my slice: the p partial slots (+ side input) staged together
+  if (PHASE == 0) {
+    const char* src[kMaxPush + 1];
+    for (int m = 0; m < a.p; ++m) src[m] = mine + (static_cast<int64_t>(m) * a.slot_rows + r0) * row_bytes;
+    if (side) src[a.p] = ewa + g0 * row_bytes;
+    bf* dst = reinterpret_cast<bf*>(const_cast<char*>(src[a.me]));  // the sum goes back in place (my slot)
+    stream_pieces(sbase, bar0, consumed, nbuf_a, src, piece, b_lo, b_hi, [&](uint32_t stg, int64_t off, int64_t nb) {
+      if (core) {
+        const int64_t per = d / 8, items = nb / unit * per;
+        for (int64_t it = tid; it < items; it += nt) {
+          const int64_t tt = it / per, jj = (it % per) * 8;
+          const uint32_t e0 = static_cast<uint32_t>((tt * 3 * d + jj) * 2);
+          float q[8], k[8], v[8], t[8];
+          lds8(stg + e0, q);
+          lds8(stg + e0 + 2 * d, k);
+          lds8(stg + e0 + 4 * d, v);
+          for (int m = 1; m < a.p; ++m) {
+            const uint32_t sm = stg + static_cast<uint32_t>(m * piece) + e0;
+            lds8(sm, t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) q[e] += t[e];
+            lds8(sm + 2 * d, t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) k[e] += t[e];
+            lds8(sm + 4 * d, t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] += t[e];
+          }
+          round8(q);
+          round8(k);
+          round8(v);
+          const int64_t pos = off / 2 + tt * 3 * d + jj;  // element of the slice
+          store8(dst + pos, q);
+          store8(dst + pos + d, k);
+          store8(dst + pos + 2 * d, v);
+          finish_core(a, g0 + pos / a.width, pos % a.width, q, k, v);
+        }
+      } else {
+        const int64_t items = nb / 16, v0 = off / 16;
+        for (int64_t it = tid; it < items; it += nt) {
+          const uint32_t e0 = static_cast<uint32_t>(it * 16);
+          float acc[8], t[8], x[8];
+          lds8(stg + e0, acc);
+          for (int m = 1; m < a.p; ++m) {
+            lds8(stg + static_cast<uint32_t>(m * piece) + e0, t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += t[e];
+          }
+          round8(acc);
+          const int64_t vi = v0 + it;
+          store8(dst + vi * 8, acc);
+          if (side) lds8(stg + static_cast<uint32_t>(a.p * piece) + e0, x);
+          finish8(a, g0 + vi / w8, (vi % w8) * 8, acc, x);
+        }
+      }
+    });
+  }
+  if (PHASE == 0) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      red_release_sys(my_flags + kSigSlots + a.sig_slot);  // ready
+    }
+    return;
+  }
+
+  // ---- B. all-gather by pull: every other member's reduced slice (+ side input)
+  const int nbuf_b = side ? 2 : 1;
+  for (int t = 1; t < a.p; ++t) {
+    const int j = (a.me + t) % a.p;
+    const int64_t gj = a.row0 + static_cast<int64_t>(j) * S;
+    const char* src[2] = {a.peer_base[j] + a.part_off + (static_cast<int64_t>(j) * a.slot_rows + r0) * row_bytes,
+                          side ? ewa + gj * row_bytes : nullptr};
+    if (tid == 0 && b_hi > b_lo) {
+      spin_geq(reinterpret_cast<const uint32_t*>(a.peer_base[j] + a.flag_off) + kSigSlots + a.sig_slot,
+               a.ready_target);
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> bulk-copy reads
+    }
+    stream_pieces(sbase, bar0, consumed, nbuf_b, src, piece, b_lo, b_hi, [&](uint32_t stg, int64_t off, int64_t nb) {
+      if (core) {
+        const int64_t per = d / 8, items = nb / unit * per;
+        for (int64_t it = tid; it < items; it += nt) {
+          const int64_t tt = it / per, jj = (it % per) * 8;
+          const uint32_t e0 = static_cast<uint32_t>((tt * 3 * d + jj) * 2);
+          float q[8], k[8], v[8];
+          lds8(stg + e0, q);
+          lds8(stg + e0 + 2 * d, k);
+          lds8(stg + e0 + 4 * d, v);
+          const int64_t pos = off / 2 + tt * 3 * d + jj;
+          finish_core(a, gj + pos / a.width, pos % a.width, q, k, v);
+        }
+      } else {
+        const int64_t items = nb / 16, v0 = off / 16;
+        for (int64_t it = tid; it < items; it += nt) {
+          const uint32_t e0 = static_cast<uint32_t>(it * 16);
+          float v[8], x[8];
+          lds8(stg + e0, v);
+          if (side) lds8(stg + static_cast<uint32_t>(piece) + e0, x);
+          const int64_t vi = v0 + it;
+          finish8(a, gj + vi / w8, (vi % w8) * 8, v, x);
+        }
+      }
+    });
+  }
+
+  // ---- C. nobody reads my slice once every member's CTAs are done
   __syncthreads();
   if (tid == 0) {
     __threadfence_system();
     for (int m = 0; m < a.p; ++m)
-      atomicAdd(reinterpret_cast<uint32_t*>(a.peer_base[m] + a.flag_off) + 2 * kSigSlots + a.sig_slot, 1u);
+      red_release_sys(reinterpret_cast<uint32_t*>(a.peer_base[m] + a.flag_off) + 2 * kSigSlots + a.sig_slot);
     if (blockIdx.x == 0) spin_geq(my_flags + 2 * kSigSlots + a.sig_slot, a.done_target);
   }
 }
@@ -179,7 +329,16 @@ __global__ void __launch_bounds__(512) fused_ar_kernel(FusedArArgs a) {
 }  // namespace
 
 cudaError_t fused_ar_launch(const FusedArArgs& a, cudaStream_t st) {
-  fused_ar_kernel<<<a.n_ctas, 512, 0, st>>>(a);
+  constexpr int smem = kFusedStages * kFusedStageBytes + kFusedStages * 8 + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fused_ar_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fused_ar_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  fused_ar_kernel<0><<<a.n_ctas, kFusedThreads, smem, st>>>(a);
+  fused_ar_kernel<1><<<a.n_ctas, kFusedThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

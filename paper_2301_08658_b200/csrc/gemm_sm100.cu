@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                       int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows, const uint32_t* gate,
-                      uint32_t gate_target, int group_m, int kserp) {
+                      uint32_t gate_target, int group_m, int kserp, int l2hint,
+                      const __grid_constant__ PushArgs push) {
   using L = SmemLayout<CG, BN, STAGES>;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr int BNC = BN / CG;  // B rows loaded by this CTA
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmB);
     ptx::prefetch_tmap(&tmC);
     if (EPI == EPI_BIAS_GELU) ptx::prefetch_tmap(&tmC2);
+    for (int j = 0; j < push.p; ++j) ptx::prefetch_tmap(&push.tm[j]);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), 1);
       ptx::mbar_init(empty_bar(s), 1);
@@ -283,6 +285,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int gated_chunk = -1;
+      // L2 policies (ATP_L2HINT bits): 1 = A evict_last, 2 = B evict_first, 4 = B evict_last
+      const uint64_t pol_last = ptx::policy_evict_last(), pol_first = ptx::policy_evict_first();
+      const bool hint_a = l2hint & 1, hint_b = l2hint & 6;
+      const uint64_t pol_b = (l2hint & 4) ? pol_last : pol_first;
       for (int tile = unit; tile < num_tiles; tile += n_units) {
         int mt, nt, chunk;
         tile_coords(tile, mt_chunk, num_n, group_m, mt, nt, chunk);
@@ -303,24 +309,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t fb = full_bar(stage);
           if (leader) ptx::mbar_arrive_expect_tx_w(fb, L::kStageBytes * CG);
           const int k0 = (k_rev ? num_k - 1 - kb : kb) * BK;
-          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1) {
+          auto load = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, bool hint, uint64_t pol) {
             if constexpr (CG == 2) {
-              ptx::tma_load_2d_cg2_w(dst, tm, fb, c0, c1);
+              if (hint) ptx::tma_load_2d_cg2_hint_w(dst, tm, fb, c0, c1, pol);
+              else ptx::tma_load_2d_cg2_w(dst, tm, fb, c0, c1);
             } else {
-              ptx::tma_load_2d_w(dst, tm, fb, c0, c1);
+              if (hint) ptx::tma_load_2d_hint_w(dst, tm, fb, c0, c1, pol);
+              else ptx::tma_load_2d_w(dst, tm, fb, c0, c1);
             }
           };
           if constexpr (!A_MN) {
-            load(sA, &tmA, k0, m0);
+            load(sA, &tmA, k0, m0, hint_a, pol_last);
           } else {
-            load(sA, &tmA, m0, k0);
-            load(sA + kBoxBytesMN, &tmA, m0 + 64, k0);
+            load(sA, &tmA, m0, k0, hint_a, pol_last);
+            load(sA + kBoxBytesMN, &tmA, m0 + 64, k0, hint_a, pol_last);
           }
           if constexpr (!B_MN) {
-            load(sB, &tmB, k0, nb);
+            load(sB, &tmB, k0, nb, hint_b, pol_b);
           } else {
 #pragma unroll
-            for (int j = 0; j < BNC / 64; ++j) load(sB + j * kBoxBytesMN, &tmB, nb + 64 * j, k0);
+            for (int j = 0; j < BNC / 64; ++j) load(sB + j * kBoxBytesMN, &tmB, nb + 64 * j, k0, hint_b, pol_b);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -417,6 +425,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    const bool hint_c = l2hint & 8;  // output stores evict_first: C is not re-read by this GEMM
+    const uint64_t pol_c = ptx::policy_evict_first();
+    // Chunk signalling, deferred by one tile: tile i is counted when tile i+1's
+    // accumulator is ready (its TMA stores have had a whole main loop to
+    // complete, so the wait below is free) or at the end.  Counting right after
+    // the stores stalled all 8 epilogue warps on the store round trip and the
+    // fences every tile: +60% on the K = 1280 Out GEMM of cfg 4 (4,2).
+    int pend_chunk = -1, pend_pj = 0;
+    auto flush_signal = [&]() {
+      if (pend_chunk < 0) return;
+      if (lane == 0) {
+        ptx::bulk_wait0();  // this warp's stores of the pending tile are complete ...
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and ordered before generic accesses
+        __threadfence_system();
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      if (warp == 2 && lane == 0) {
+        __threadfence_system();
+        if (push.p > 0) {
+          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(push.sig[pend_pj] + pend_chunk) : "memory");
+        } else {
+          atomicAdd(sig + pend_chunk, 1u);
+        }
+      }
+      pend_chunk = -1;
+    };
     for (int tile = unit; tile < num_tiles; tile += n_units) {
       int mt, nt, chunk;
       tile_coords(tile, mt_chunk, num_n, group_m, mt, nt, chunk);
@@ -424,7 +458,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = nt * BN;
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
       ptx::tc_fence_after();
+      if (sig != nullptr) flush_signal();  // the previous tile
       const int row = m0 + 32 * q + static_cast<int>(lane);
+      // fused reduce-scatter: this CTA's 128 rows go to the owner of their row
+      // slice (member pj), into its receive slot for this rank at row prow
+      int pj = 0, prow = m0;
+      if (push.p > 0) {
+        const int rin = m0 - chunk * sig_rows;
+        pj = rin / push.slice_rows;
+        prow = chunk * push.slice_rows + (rin - pj * push.slice_rows);
+      }
+      const CUtensorMap* tm_out = push.p > 0 ? &push.tm[pj] : &tmC;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
       const int c_begin = half * (BN / 2 / W), c_end = (half + 1) * (BN / 2 / W);
       // software pipeline: the TMEM slice and side inputs of slice c+1 are in
@@ -453,9 +497,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          ptx::tma_store_2d(&tmC, stg, col0, m0 + 32 * q);
-          if constexpr (EPI == EPI_BIAS_GELU)
-            ptx::tma_store_2d(&tmC2, stg + 32 * slice_row_bytes<EPI>(), col0, m0 + 32 * q);
+          if (hint_c) {
+            ptx::tma_store_2d_hint(tm_out, stg, col0, prow + 32 * q, pol_c);
+            if constexpr (EPI == EPI_BIAS_GELU)
+              ptx::tma_store_2d_hint(&tmC2, stg + 32 * slice_row_bytes<EPI>(), col0, m0 + 32 * q, pol_c);
+          } else {
+            ptx::tma_store_2d(tm_out, stg, col0, prow + 32 * q);
+            if constexpr (EPI == EPI_BIAS_GELU)
+              ptx::tma_store_2d(&tmC2, stg + 32 * slice_row_bytes<EPI>(), col0, m0 + 32 * q);
+          }
           ptx::bulk_commit();
         }
         sbuf ^= 1;
@@ -470,24 +520,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (sig != nullptr) {
-        // every epilogue warp's bulk stores of this tile complete and visible
-        // (system scope: NCCL / peer ranks read them), then count the tile.
-        if (lane == 0) {
-          ptx::bulk_wait0();
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy (TMA) writes before generic readers
-          __threadfence_system();
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-        if (warp == 2 && lane == 0) {
-          __threadfence_system();
-          atomicAdd(sig + chunk, 1u);
-        }
+        // counted once every epilogue warp's bulk stores of this tile are
+        // complete and visible (system scope: NCCL / peer ranks read them)
+        pend_chunk = chunk;
+        pend_pj = pj;
       }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (sig != nullptr) flush_signal();  // the last tile
     if (lane == 0) ptx::bulk_wait0();  // staging smem stays valid until the last stores completed
   }
 
@@ -537,6 +580,16 @@ bool make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int6
   return r == CUDA_SUCCESS;
 }
 
+// L2 cache hints of the TMA loads / stores (ATP_L2HINT bitmask, A/B runs):
+// 1 = A evict_last, 2 = B evict_first, 4 = B evict_last, 8 = C stores evict_first.
+int l2hint() {
+  static const int v = [] {
+    const char* e = getenv("ATP_L2HINT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 // Serpentine K order across persistent rounds (ATP_KSERP=0 disables; A/B runs).
 int kserp() {
   static const int v = [] {
@@ -575,7 +628,7 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = (pdl && d.pdl && d.gate == nullptr) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.tmC, d.tmC2, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate,
-                            d.gate_target, d.group_m > 0 ? d.group_m : 16, kserp());
+                            d.gate_target, d.group_m > 0 ? d.group_m : 16, kserp(), l2hint(), d.push);
 }
 
 template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>

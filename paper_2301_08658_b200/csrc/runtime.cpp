@@ -66,7 +66,7 @@ static cudaError_t launch_fused(atp_mesh* m, RankState& s, const Op& op, cudaStr
   a.sig_target = s.sig_total[a.sig_slot];
   a.ready_target = (s.ready_total[a.sig_slot] += static_cast<uint32_t>(a.n_ctas));
   a.done_target = (s.done_total[a.sig_slot] += static_cast<uint32_t>(a.p * a.n_ctas));
-  count_launch(1);
+  count_launch(2);  // phase A + phase B/C kernels
   return fused_ar_launch(a, st);
 }
 
@@ -194,6 +194,11 @@ RankView rank_view(const atp_mesh* m, int r) {
   v.sig_buf = m->rs[m->is_virtual ? r : 0].sig_buf;
   v.sym_base = m->rs[m->is_virtual ? r : 0].sym_base;
   v.sym_part_bytes = m->rs[m->is_virtual ? r : 0].sym_part_bytes;
+  for (int d = 0; d < 2; ++d) {
+    const RankState& s = m->rs[m->is_virtual ? r : 0];
+    for (int j = 0; j < 16; ++j) v.peers[d][j] = s.peers[d][j];
+    v.me_in[d] = s.me_in[d];
+  }
   v.signalled = m->signalled && stream_wait_available();
   {
     // Opt-in (ATP_GATED=1).  A gated GEMM spins on SMs it holds: only allowed
@@ -231,7 +236,10 @@ static int ensure_events(RankState& s, int n) {
 static cudaError_t launch_local(Op& op, cudaStream_t st, bool prev_kernel, bool profiling) {
   if (op.kind == OP_GEMM) {
     count_launch(1);
-    op.g.pdl = prev_kernel && !profiling && op.n_waits == 0 && op.g.gate == nullptr && op.g.sig == nullptr;
+    // A signalled GEMM may use PDL too: it touches no global memory (nor its
+    // chunk counters) before griddepcontrol.wait, and the per-call counter
+    // reset is a memset, never the kernel right before it.
+    op.g.pdl = prev_kernel && !profiling && op.n_waits == 0 && op.g.gate == nullptr;
     return gemm_launch(op.g, st);
   }
   count_launch(op.e.kind == EW_ATTN_BWD ? 3 : (op.e.kind == EW_LN_PARAM_GRAD ? 2 : 1));
@@ -645,8 +653,18 @@ int mesh_create(int d1, int d2, int world_rank, const uint8_t* uid, int device, 
     std::memcpy(&id, uid, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&m->world, n, id, world_rank);
     // dim-1 group: the d1 ranks sharing i2 (color i2, ordered by i1); dim-2: sharing i1.
-    if (r == ncclSuccess) r = ncclCommSplit(m->world, m->i2, m->i1, &m->dim1, nullptr);
-    if (r == ncclSuccess) r = ncclCommSplit(m->world, m->i1, m->i2, &m->dim2, nullptr);
+    // The dim communicators carry the data-path all-reduces, which overlap the
+    // persistent GEMMs: bound NCCL's SM footprint to the SMs the GEMM CTA cap
+    // leaves (bench: 132 of 148 -> 16; ATP_NCCL_MAX_CTAS overrides, 0 = NCCL's
+    // default), so the two never compete for the same SMs.
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    {
+      const char* e = getenv("ATP_NCCL_MAX_CTAS");
+      const int mx = e ? atoi(e) : 16;
+      if (mx > 0) cfg.maxCTAs = mx;
+    }
+    if (r == ncclSuccess) r = ncclCommSplit(m->world, m->i2, m->i1, &m->dim1, &cfg);
+    if (r == ncclSuccess) r = ncclCommSplit(m->world, m->i1, m->i2, &m->dim2, &cfg);
     if (r != ncclSuccess) {
       set_error(std::string("NCCL mesh init: ") + ncclGetErrorString(r));
       if (m->dim1) ncclCommDestroy(m->dim1);

@@ -65,6 +65,8 @@ struct RankView {
   bool signalled = true;        // use signalled stages when possible
   char* sym_base = nullptr;     // fused all-reduce: this rank's peer-visible buffer
   size_t sym_part_bytes = 0;    //   capacity of each of its two partial-sum regions
+  char* peers[2][16] = {};      //   the dim-1 / dim-2 group members' buffers (fused GEMM push targets)
+  int me_in[2] = {0, 0};        //   this rank's index in its dim-1 / dim-2 group
   bool gate_ok = false;         // chunk-gated GEMMs allowed (GEMM CTA cap leaves SMs free)
 };
 
@@ -133,6 +135,6 @@ void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes);
 bool stream_wait_available();
 int enable_fused_ar(atp_mesh* m, size_t part_bytes);
 int debug_counters(atp_mesh* m, int rank, uint32_t* out, int n);
-constexpr int kFusedCtas = 16;  // CTAs of one fused all-reduce kernel (fits the SMs the GEMM cap leaves)
+constexpr int kFusedCtas = 32;  // CTAs of one fused all-reduce kernel: 2 per SM on the 16 SMs the GEMM cap leaves
 
 }  // namespace atp

@@ -58,6 +58,25 @@ inline char* mptr(void* p, int64_t off_elems) { return static_cast<char*>(p) + o
 
 using EwList = std::vector<EwDesc>;
 
+// Where the post-all-reduce elementwise step of a signalled (NCCL) stage runs:
+// 1 (default) = ONE full-T launch on the compute stream once the stage's last
+// chunk is all-reduced, right before the next stage's GEMM; 0 = per chunk on
+// the communication stream (ATP_EW_COMPUTE=0, A/B runs).  Per chunk, the
+// elementwise kernels share the SMs with the running GEMM (a persistent grid
+// that leaves them few resources) and pile up behind it: measured with the
+// collectives elided at cfg 4 (4,2), c = 4, the adds alone took 0.43-0.60 ms
+// per step instead of 0.09-0.11 ms as full-width launches, and the compute
+// stream idled 0.23-0.33 ms waiting for that backlog
+// (profiles/r02_trace_42_cap*.txt).  The all-reduce of chunk k still overlaps
+// the GEMM's later chunks either way.
+bool ew_compute() {
+  static const bool on = [] {
+    const char* e = getenv("ATP_EW_COMPUTE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // ATP_AUX_COLSUM=0 keeps the bias-gradient column sums on the compute stream (A/B runs).
 bool aux_colsum() {
   static const bool on = [] {
@@ -114,13 +133,21 @@ struct Builder {
     def[k].clear();
     return w;
   }
-  // Every chunk's prologue; returns the distinct unconsumed waits.
+  // Every chunk's prologue; returns the distinct unconsumed waits.  An event
+  // some deferred op on the compute stream already waited for is satisfied for
+  // everything behind it on that stream (one signalled stage hands ALL chunks
+  // the same last-all-reduce event): dropping it leaves the GEMM without a
+  // stream wait, so it may use programmatic dependent launch.
   std::vector<int> prologue_all() {
-    std::vector<int> w;
+    std::vector<int> w, consumed;
     for (int k = 0; k < chunks; ++k) {
+      const int pk = pend[k];
+      const bool had_def = !def[k].empty();
       int e = prologue(k);
+      if (had_def && pk >= 0) consumed.push_back(pk);
       bool seen = false;
       for (int x : w) seen |= (x == e);
+      for (int x : consumed) seen |= (x == e);
       if (e >= 0 && !seen) w.push_back(e);
     }
     return w;
@@ -180,12 +207,6 @@ struct Builder {
   // (the GEMM's producer waits per chunk; no stream wait) or the usual events.
   // Returns the gate slot to use (-1 = not gated).
   int stage_entry(int64_t out_w, std::vector<int>& waits) {
-    if (next_independent) {
-      next_independent = false;
-      gate_slot = -1;
-      flush_to_comm();
-      return -1;
-    }
     int bn = 128, cg = 1;
     if (dtype == 0) gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
     if (rv.gate_ok && dtype == 0 && gate_slot >= 0 && chunks > 1 && Mc % (128 * cg) == 0) {
@@ -198,11 +219,19 @@ struct Builder {
     waits = prologue_all();
     return -1;
   }
-  // Pending per-chunk prologues of a per-chunk stage are not needed by an
-  // independent stage: emit them now (on the compute stream) and drop the waits.
+  // Pending deferred elementwise steps are not needed by an independent stage:
+  // emit them on the communication stream (behind the all-reduces they
+  // follow, so the compute stream does not wait for them) and drop the waits.
   void flush_to_comm() {
-    prologue_all();
-    for (int k = 0; k < chunks; ++k) pend[k] = -1;
+    for (int k = 0; k < chunks; ++k) {
+      int w = pend[k];
+      for (const EwDesc& e : def[k]) {
+        ew(e, 1, w);
+        w = -1;
+      }
+      def[k].clear();
+      pend[k] = -1;
+    }
   }
   void gate_gemm(Op* g, int gslot) {
     if (gslot < 0) return;
@@ -227,6 +256,14 @@ struct Builder {
   bool stage(int dim, const void* in, int64_t in_w, const void* w, int64_t ldw, bool b_mn, int64_t out_w, const void* bias,
              void* out, int fused_epi, Fused fused, AfterAR after_ar, Extra extra) {
     const bool comm = dim_size(dim) > 1;
+    if (next_independent) {
+      // consumed by THIS stage whatever way it is emitted (the per-chunk branch
+      // below never calls stage_entry): the previous stage's deferred steps go
+      // to the communication stream and nothing here waits for them
+      next_independent = false;
+      gate_slot = -1;
+      flush_to_comm();
+    }
     int bn = 128, cg = 1;  // fp32 check mode: 128 x 128 tiles
     if (dtype == 0) gemm_plan_tile(static_cast<int>(T), static_cast<int>(out_w), &bn, &cg);
     if (!comm) {
@@ -244,7 +281,12 @@ struct Builder {
       return extra();
     }
     const void* bias_here = coord0(dim) ? bias : nullptr;
-    const bool fused_ok = rv.sym_base != nullptr && dtype == 0 && Mc % (128 * cg) == 0 &&
+    // fused GEMM -> reduce-scatter -> all-gather: each member's slice of a chunk
+    // (S = Mc / p rows) must be whole 128-row CTA tiles, and every receive slot
+    // row a whole number of 16-byte vectors
+    const int p_grp = dim_size(dim);
+    const bool fused_ok = rv.sym_base != nullptr && dtype == 0 && Mc % (128 * cg) == 0 && p_grp <= kMaxPush &&
+                          (Mc / p_grp) % 128 == 0 && (out_w * 2) % 16 == 0 &&
                           static_cast<size_t>(T) * out_w * 2 <= rv.sym_part_bytes && next_slot + chunks <= kGateBase;
     const bool signalled_ok = rv.signalled && rv.sig_buf != nullptr && chunks > 1 && Mc % (128 * cg) == 0 &&
                               next_slot + chunks <= kGateBase;
@@ -269,8 +311,29 @@ struct Builder {
       g->g.sig = rv.sig_buf + slot0;
       g->g.sig_rows = static_cast<int>(Mc);
       const uint32_t per_chunk = static_cast<uint32_t>((Mc / 128) * ((out_w + g->g.bn - 1) / g->g.bn));
+      if (fused_ok) {
+        // the GEMM stores slice j of every chunk into member j's receive slot for
+        // this rank: [T/p rows, out_w] at part_off + me * (T/p) * out_w * 2
+        PushArgs& pa = g->g.push;
+        const int di = dim - 1, me = rv.me_in[di];
+        const int64_t slot_rows = T / p_grp;
+        pa.p = p_grp;
+        pa.slice_rows = static_cast<int>(Mc / p_grp);
+        for (int j = 0; j < p_grp; ++j) {
+          char* pb = rv.peers[di][j];
+          if (pb == nullptr || !make_tmap_out(&pa.tm[j], pb + part_off + me * slot_rows * out_w * 2, 2, slot_rows,
+                                              out_w, out_w, 32)) {
+            err = "fused stage: receive-slot tensor map";
+            return false;
+          }
+          pa.sig[j] = reinterpret_cast<uint32_t*>(pb + 2 * rv.sym_part_bytes) + slot0;
+        }
+      }
       if (!extra()) return false;
       const EwList post = fused_ok ? after_ar(0, 0, T) : EwList{};  // base pointers of the fused step
+      // NCCL stage, not gated: the elementwise step runs once over all T rows
+      // on the compute stream before the next stage (ew_compute()).
+      const bool ew_deferred = !fused_ok && !rv.gate_ok && ew_compute();
       for (int k = 0; k < chunks; ++k) {
         if (fused_ok) {
           Op& o = push(OP_FUSED_AR, 1);
@@ -284,6 +347,8 @@ struct Builder {
           f.width = out_w;
           f.row0 = k * Mc;
           f.rows = Mc;
+          f.chunk = k;
+          f.slot_rows = T / p_grp;
           f.sig_slot = slot0 + k;
           f.out = out;
           f.n_ctas = kFusedCtas;
@@ -302,13 +367,15 @@ struct Builder {
           wsig.sig_slot = slot0 + k;
           wsig.sig_inc = per_chunk;
           allreduce(dim, mptr(out, k * Mc * out_w), Mc * out_w, -1, -1);
-          for (const EwDesc& e : after_ar(k, k * Mc, Mc)) ew(e, 1);
+          if (!ew_deferred)
+            for (const EwDesc& e : after_ar(k, k * Mc, Mc)) ew(e, 1);
         }
         publish_gate(gslot0, k);
       }
       const int last = ev();
       s.ops.back().record = last;
       for (int k = 0; k < chunks; ++k) pend[k] = last;
+      if (ew_deferred) def[0] = after_ar(0, 0, T);
       gate_slot = rv.gate_ok ? gslot0 : -1;
       return true;
     }
@@ -419,9 +486,12 @@ int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int6
 }
 
 // ---------------------------------------------------------------- layer blocks
-int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
-                int chunks, int dtype, Sched& out) {
-  Builder b(rv, T, chunks, dtype);
+// Emit the forward (fwd) or backward (!fwd) blocks of one layer into `b`.
+// `first_bwd`: this is the first backward block of the pipeline (its first
+// stage reads only dZ and saved activations, so it waits for nothing of the
+// forward tail).
+static bool emit_layer(Builder& b, const RankView& rv, const LayerParts& p, bool fwd, bool first_bwd, int64_t T,
+                       int64_t h, int64_t F, int64_t heads) {
   const int64_t hc = h / rv.d2;      // activation column block
   const int64_t h1 = h / rv.d1;      // ctx width / Out input
   const int64_t q1 = 3 * h / rv.d1;  // local QKV width
@@ -430,13 +500,10 @@ int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, i
   auto rows = [](const void* base, int64_t r0, int64_t w) { return cptr(base, r0 * w); };
   auto mrows = [](void* base, int64_t r0, int64_t w) { return mptr(base, r0 * w); };
   auto aux = [](const void* p) { return static_cast<const void*>(p); };
-  auto fail = [&]() {
-    set_error(b.err);
-    return 2;
-  };
+  auto fail = [&]() { return false; };
   using E = Builder;
 
-  if (p.attn_fwd) {
+  if (fwd && p.attn_fwd) {
     const atp_attn_fwd_args& a = *p.attn_fwd;
     // F3/F4: QKV column-first, all-reduce on dim 2 (f1); F5 core after the sum
     if (!b.stage(2, a.x, hc, a.wqkv, q1, true, q1, a.bqkv, a.qkv, EPI_BF16, no_fuse,
@@ -460,7 +527,7 @@ int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, i
                  no_extra))
       return fail();
   }
-  if (p.mlp_fwd) {
+  if (fwd && p.mlp_fwd) {
     const atp_mlp_fwd_args& a = *p.mlp_fwd;
     // F8/F9/F10: FC1 column-first, all-reduce on dim 2 (f3), U saved, H = GeLU(U)
     if (!b.stage(2, a.x, hc, a.w1, F1, true, F1, a.b1, a.u, EPI_BIAS_GELU,
@@ -485,9 +552,10 @@ int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, i
                  no_extra))
       return fail();
   }
-  if (p.mlp_bwd) {
+  if (!fwd && p.mlp_bwd) {
     const atp_mlp_bwd_args& a = *p.mlp_bwd;
-    b.next_independent = true;  // B1 reads dZ and the saved H/U only
+    b.next_independent = first_bwd;  // B1 reads dZ and the saved H/U only (dZ of a stack's
+                                     // inner layer is the next layer's dX: a real dependency)
     // B1: dH = dZ W2^T, all-reduce on dim 2 (conjugate of f4); dU = dH * GeLU'(U); || dW2, db2
     if (!b.stage(2, a.dz, hc, a.w2, hc, false, F1, nullptr, a.ws_dh, EPI_DGELU,
                  [&](EpiParams& ep, int64_t, int64_t) {
@@ -511,7 +579,7 @@ int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, i
                  [&]() { return b.dw(a.x, hc, a.ws_dh, F1, a.dw1, a.db1); }))
       return fail();
   }
-  if (p.attn_bwd) {
+  if (!fwd && p.attn_bwd) {
     const atp_attn_bwd_args& a = *p.attn_bwd;
     // B4/B5: dctx = dY Wo^T, all-reduce on dim 2 (conjugate of f2); dQKV = expand(dctx); || dWo, dbo
     if (!b.stage(2, a.dy, hc, a.wo, hc, false, h1, nullptr, a.ws_dctx, EPI_BF16, no_fuse,
@@ -535,9 +603,35 @@ int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, i
                  [&]() { return b.dw(a.x, hc, a.ws_dqkv, q1, a.dwqkv, a.dbqkv); }))
       return fail();
   }
+  return true;
+}
+
+// A stack of n layers as ONE chunk pipeline (SURVEY §8(d) L_bench): forward
+// layer 0..n-1, then backward n-1..0.  Layer l+1's first GEMM waits only for
+// layer l's last stage (its chunk pipeline: per-chunk events / gates), so the
+// last all-reduce of a layer overlaps the next layer's first GEMM (Fig. 7,
+// P:328) instead of draining at a call boundary.
+int build_layer_stack(const RankView& rv, const LayerParts* parts, int n_layers, int64_t T, int64_t h, int64_t F,
+                      int64_t heads, int chunks, int dtype, Sched& out) {
+  Builder b(rv, T, chunks, dtype);
+  for (int l = 0; l < n_layers; ++l)
+    if (!emit_layer(b, rv, parts[l], true, false, T, h, F, heads)) {
+      set_error(b.err);
+      return 2;
+    }
+  for (int l = n_layers - 1; l >= 0; --l)
+    if (!emit_layer(b, rv, parts[l], false, l == n_layers - 1, T, h, F, heads)) {
+      set_error(b.err);
+      return 2;
+    }
   b.flush();
   out = std::move(b.s);
   return 0;
+}
+
+int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
+                int chunks, int dtype, Sched& out) {
+  return build_layer_stack(rv, &p, 1, T, h, F, heads, chunks, dtype, out);
 }
 
 

@@ -22,6 +22,9 @@ int build_linear_bwd(const RankView& rv, bool colfirst, const LinearBwd& a, int6
                      int chunks, int dtype, Sched& out);
 int build_layer(const RankView& rv, const LayerParts& p, int64_t T, int64_t h, int64_t F, int64_t heads,
                 int chunks, int dtype, Sched& out);
+// n layers as one pipeline: forward 0..n-1, backward n-1..0 (parts[l] = layer l).
+int build_layer_stack(const RankView& rv, const LayerParts* parts, int n_layers, int64_t T, int64_t h, int64_t F,
+                      int64_t heads, int chunks, int dtype, Sched& out);
 
 // Full pre-LN GPT layer: per-rank workspace bytes and schedule.
 size_t gpt_workspace_bytes(int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq, int chunks);

@@ -18,6 +18,8 @@ def main():
     p.add_argument("--d2", type=int, default=1)
     p.add_argument("--iters", type=int, default=20)
     p.add_argument("--mode", type=int, default=-1, help="ATP_GEMM_MODE env for the library (-1: leave)")
+    p.add_argument("--no-ref", action="store_true", help="skip the cuBLAS reference timing")
+    p.add_argument("--only", default="", help="comma-separated GEMM names to run")
     a = p.parse_args()
     import torch
     import paper_2301_08658_b200 as atp
@@ -37,6 +39,8 @@ def main():
     res = []
     tot_fl, tot_ms = 0.0, 0.0
     for name, M, N, K, amn, bmn, f32 in shapes:
+        if a.only and name not in a.only.split(","):
+            continue
         A = torch.randn((K, M) if amn else (M, K), device="cuda").to(torch.bfloat16)
         B = torch.randn((K, N) if bmn else (N, K), device="cuda").to(torch.bfloat16)
         C = torch.empty((M, N), device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
@@ -53,6 +57,10 @@ def main():
         fl = 2.0 * M * N * K
         tot_fl += fl
         tot_ms += ms
+        if a.no_ref:
+            res.append({"gemm": name, "M": M, "N": N, "K": K, "ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1)})
+            print(json.dumps(res[-1]), flush=True)
+            continue
         # torch reference for context (cuBLAS)
         At = A.t() if amn else A
         Bt = B if bmn else B.t()

@@ -40,6 +40,8 @@ def main():
     p.add_argument("--layer", default="linear", choices=["linear", "gpt"])
     p.add_argument("--seq", type=int, default=2048)
     p.add_argument("--ops", action="store_true", help="print every op")
+    p.add_argument("--fused-ar", action="store_true",
+                   help="fused GEMM -> reduce-scatter -> all-gather stages (dry run: every peer is this rank)")
     a = p.parse_args()
     import torch
     import paper_2301_08658_b200 as atp
@@ -49,6 +51,8 @@ def main():
     h, T, F = a.h, a.T, 4 * a.h
     mesh = atp.Mesh.local(d1, d2, 0) if d1 * d2 > 1 else atp.Mesh.virtual(1, 1)
     mesh.set_gemm_ctas(a.gemm_ctas if d1 * d2 > 1 else 0)
+    if a.fused_ar:
+        mesh.enable_fused_ar(T * max(3 * h // d1, 4 * h // d1, h // d2) * 2)
     if a.layer == "gpt":
         bufs = atp.alloc_gpt_rank(d1, d2, 0, T, h, F, a.heads, "cuda", 2301)
     else:

@@ -61,7 +61,8 @@ def test_bench_n2_shared_gpu():
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                           "--gpus", "2", "--share-gpu", "--steps", "3", "--warmup", "3", "--hidden", "1024",
-                          "--heads", "8", "--batch", "2", "--seq", "1024", "--no-cpu-baseline", "--probe-mib", "4"],
+                          "--heads", "8", "--batch", "2", "--seq", "1024", "--no-cpu-baseline", "--probe-mib", "4",
+                          "--try-fused"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.strip()]
@@ -76,3 +77,9 @@ def test_bench_n2_shared_gpu():
     assert "hcm_only" in d["search"]
     mb = d.get("megatron_baseline")
     assert mb is None or "error" not in mb, mb
+    # N>1 default: a 4-layer stack as one pipeline, with the one-layer call reported beside it
+    assert d["config"]["layers"] == 4 and "error" not in d["single_layer"], d.get("single_layer")
+    assert abs(d["ms_per_layer"] - d["ms_per_step"] / 4) < 1e-9
+    # --try-fused timed the fused GEMM -> reduce-scatter -> all-gather path (CUDA IPC peers) beside NCCL
+    ch = d["allreduce_choice"]
+    assert "error" not in ch and {"nccl", "fused"} <= set(ch["timed_ms"]), ch

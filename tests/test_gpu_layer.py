@@ -301,6 +301,63 @@ def test_layer_fused_peer_allreduce(d1, d2, chunks):
             assert torch.equal(b[k], v), k
 
 
+def _fused_launches(mesh, call):
+    """Run `call` under the executor's per-launch trace; returns the number of
+    fused all-reduce kernels (op kind 4) and of ordinary collectives (kind 2)."""
+    import ctypes as C
+
+    import torch
+    from paper_2301_08658_b200 import _abi
+
+    lib = _abi.lib()
+    _abi.check(lib.atp_profile_begin(mesh.handle))
+    call()
+    torch.cuda.synchronize()
+    recs = (_abi.TraceRec * 65536)()
+    n = C.c_int()
+    _abi.check(lib.atp_profile_trace(mesh.handle, recs, 65536, C.byref(n)))
+    _abi.check(lib.atp_profile_end(mesh.handle, C.byref(_abi.Profile())))
+    kinds = [r.kind for r in recs[: n.value]]
+    return kinds.count(4), kinds.count(2)
+
+
+@pytest.mark.parametrize("d1,d2", [(4, 2), (2, 4), (8, 1), (1, 8)])
+def test_layer_fused_push_every_stage(d1, d2):
+    """Fused GEMM -> reduce-scatter (TMA stores into the slice owners' receive
+    slots) -> pull all-gather with the elementwise step, at a size where every
+    communicating stage of the layer qualifies (slices of whole 128-row tiles):
+    all 8 stages x 4 chunks run as fused kernels on every rank (no collective
+    falls back), outputs poisoned with NaN beforehand, every output of every
+    rank vs the oracle, bit-identical replicas, a second call identical."""
+    import torch
+    import paper_2301_08658_b200 as atp
+
+    T, h, F, heads, chunks, seed = 4096, 512, 2048, 8, 4, 53
+    g, sh, fw, bw, _ = oracle_layer(T, h, F, heads, d1, d2, chunks, seed)
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        mesh.enable_fused_ar(T * F * 2)
+        bufs = [atp.alloc_layer_rank(d1, d2, r, T, h, F, "cuda", seed) for r in range(d1 * d2)]
+        for b in bufs:
+            for k in ("qkv", "ctx", "y1", "u", "h", "z", "dx", "dwqkv", "dbqkv", "dwo", "dbo", "dw1", "db1", "dw2",
+                      "db2"):
+                b[k].fill_(float("nan"))
+        call = atp.LayerCall(mesh, bufs, T, h, F, heads, chunks, True)
+        n_fused, n_coll = _fused_launches(mesh, call)
+        snap = [{k: b[k].clone() for k in ("z", "dx", "dw1", "dwqkv", "u", "h")} for b in bufs]
+        call()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    comm_stages = 4 * (d1 > 1) + 4 * (d2 > 1)  # a size-1 mesh dimension has no collective (G7)
+    assert n_coll == 0 and n_fused == comm_stages * chunks * d1 * d2, (n_fused, n_coll)
+    compare(bufs, fw, bw, d1, d2)
+    check_replicas(bufs, d1, d2)
+    for b, s in zip(bufs, snap):
+        for k, v in s.items():
+            assert torch.equal(b[k], v), k
+
+
 @pytest.mark.parametrize("d1,d2,cap", [(2, 2, 32), (4, 2, 16), (2, 4, 16), (8, 1, 16)])
 @pytest.mark.parametrize("fused", [False, True])
 def test_layer_chunk_gated(d1, d2, cap, fused):
@@ -396,3 +453,47 @@ def test_mesh_from_borrowed_comms():
     from paper_2301_08658_b200._abi import AtpError
     with pytest.raises(AtpError):
         atp.Mesh.from_comms(2, 1, 0, None, None, 0)
+
+
+@pytest.mark.parametrize("d1,d2,chunks", [(1, 1, 1), (2, 2, 2), (4, 2, 2), (1, 4, 2)])
+def test_layer_stack(d1, d2, chunks):
+    """atp_layer_stack_fwd_bwd: 3 layers as ONE pipeline (forward 0..2, backward
+    2..0; SURVEY §8(d) L_bench) vs the oracle run layer by layer: layer l's
+    input is the oracle's Z of layer l-1 and its upstream gradient the oracle's
+    dX of layer l+1.  Every output of every layer and rank is compared (all
+    outputs poisoned with NaN first), replicas bit-identical."""
+    import torch
+    import datagen
+    import paper_2301_08658_b200 as atp
+    from oracle import layer as olayer
+
+    L, T, h, F, heads, seed = 3, 512, 256, 1024, 4, 61
+    gs = [{k: v.astype(np.float64) for k, v in datagen.layer_globals(T, h, F, seed=seed + l).items()}
+          for l in range(L)]
+    xs = [gs[0]["x"]]
+    for l in range(L - 1):  # dense forward chain
+        xs.append(olayer.dense_forward(dict(gs[l], x=xs[l]), heads)["z"])
+    dzs = [None] * L
+    dzs[L - 1] = gs[L - 1]["dz"]
+    for l in range(L - 1, 0, -1):  # dense backward chain
+        gl = dict(gs[l], x=xs[l])
+        dzs[l - 1] = olayer.dense_backward(gl, olayer.dense_forward(gl, heads), dzs[l], heads)["dx"]
+    ref = [olayer.run_layer(dict(gs[l], x=xs[l], dz=dzs[l]), d1, d2, heads, chunks) for l in range(L)]
+
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        per_rank = [atp.alloc_layer_stack(d1, d2, r, T, h, F, "cuda", seed, L) for r in range(d1 * d2)]
+        stack = [[per_rank[r][l] for r in range(d1 * d2)] for l in range(L)]
+        for layer in stack:
+            for b in layer:
+                for k in ("qkv", "ctx", "y1", "u", "h", "z", "dy1", "dx", "dwqkv", "dbqkv", "dwo", "dbo", "dw1",
+                          "db1", "dw2", "db2"):
+                    b[k].fill_(float("nan"))
+        atp.LayerStackCall(mesh, stack, T, h, F, heads, chunks)()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    for l in range(L):
+        _, fw, bw, _ = ref[l]
+        compare(stack[l], fw, bw, d1, d2)
+        check_replicas(stack[l], d1, d2)
