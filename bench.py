@@ -97,8 +97,8 @@ def parse():
     p.add_argument("--nccl-only", action="store_true",
                    help="N>1 linear block: no variant selection (plain NCCL step)")
     p.add_argument("--try-fused", action="store_true",
-                   help="N>1 linear block: also time the fused peer-memory all-reduce (± gating) against NCCL "
-                        "(± gating) and run the fastest")
+                   help="N>1 linear block: also time the fused GEMM->reduce-scatter->all-gather path against NCCL "
+                        "and run the faster (with --try-gated: also both chunk-gated)")
     p.add_argument("--try-gated", action="store_true",
                    help="N>1 linear block: also time NCCL with chunk gating and run the faster")
     p.add_argument("--gated", action="store_true",
@@ -230,8 +230,8 @@ def sample_tokens(w, h, heads, seed, target_s: float) -> tuple[int, float, float
     """Token count whose oracle run takes ~target_s (the time is affine in the
     tokens: fixed weight copies + per-token GEMMs); two calibration points."""
     t_a = cpu_oracle_run(w, 16, h, heads, seed)
-    t_b = cpu_oracle_run(w, 80, h, heads, seed)
-    per_tok = max((t_b - t_a) / 64.0, 1e-6)
+    t_b = cpu_oracle_run(w, 208, h, heads, seed)  # a mid-size point: the per-token cost grows with T
+    per_tok = max((t_b - t_a) / 192.0, 1e-6)
     fixed = max(t_a - 16 * per_tok, 0.0)
     T_s = int(max(16, min(8192, (target_s - fixed) / per_tok)) // 8 * 8)
     return T_s, fixed, per_tok
@@ -306,6 +306,11 @@ def _quiet(fn):
         sys.stdout.flush()
         os.dup2(saved_fd, 1)
         os.close(saved_fd)
+
+
+def note(msg: str) -> None:
+    """Progress marker on stderr (rank-prefixed by the caller): localises a hang."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
 
 def emit(obj: dict) -> None:
@@ -488,6 +493,7 @@ def main() -> None:
         d1, d2 = 1, 1
     assert d1 * d2 == world
 
+    note(f"rank {rank}: mesh {d1}x{d2} ({mesh_source})")
     ctas = a.gemm_ctas if a.gemm_ctas >= 0 else (0 if world == 1 else 132)
     stream = torch.cuda.Stream(device=dev)  # a capturable (non-legacy) stream for every launch of the bench
     torch.cuda.set_stream(stream)
@@ -573,6 +579,7 @@ def main() -> None:
                         "predicted_exposed_ms": {c: v[1] for c, v in pred.items()}, "busbw_gbs": busbw,
                         "busbw_source": busbw_source, "chosen": chunks, "planner": "libatp atp_plan_chunks"}
     call = make_call(mesh, bufs, chunks)
+    note(f"rank {rank}: chunks {chunks}, layers {L}; warm-up")
 
     for _ in range(max(3, a.warmup)):
         call(stream)
@@ -611,21 +618,25 @@ def main() -> None:
             (a.try_gated or a.try_fused):
         times, runners = {}, {}
         try:
+            note(f"rank {rank}: variant nccl")
             times["nccl"], runners["nccl"] = timed(10, run), (mesh, call, run, False, graph_note)
-            mesh.set_gating(True)
-            run_g = as_graph(mesh, call)
-            for _ in range(2):
-                run_g(stream)
-            times["nccl+gated"] = timed(10, run_g)
-            runners["nccl+gated"] = (mesh, call, run_g, True, graph_note)
-            mesh.set_gating(False)
+            if a.try_gated:
+                note(f"rank {rank}: variant nccl+gated")
+                mesh.set_gating(True)
+                run_g = as_graph(mesh, call)
+                for _ in range(2):
+                    run_g(stream)
+                times["nccl+gated"] = timed(10, run_g)
+                runners["nccl+gated"] = (mesh, call, run_g, True, graph_note)
+                mesh.set_gating(False)
             if a.try_fused:
                 mesh_f = make_mesh(d1, d2)
                 meshes.append(mesh_f)
                 mesh_f.enable_fused_ar(T * max(3 * h // d1, F // d1, h // d2) * 2)
                 call_f = make_call(mesh_f, bufs, chunks)
                 note_f = "direct calls (fused peer-memory mesh keeps cross-rank state: no graph capture)"
-                for gated in (False, True):
+                for gated in ((False, True) if a.try_gated else (False,)):
+                    note(f"rank {rank}: variant fused gated={gated}")
                     mesh_f.set_gating(gated)
                     for _ in range(3):
                         call_f(stream)
@@ -643,6 +654,7 @@ def main() -> None:
             a.gated = chosen_gating
 
     # ---- timed region (clocks sampled during it)
+    note(f"rank {rank}: timed region")
     sampler = ClockSampler(local_rank)
     import ctypes as C
 
@@ -761,6 +773,7 @@ def main() -> None:
             single = {"error": str(e)}
 
     # ---- Megatron-style baseline (north_star): the same library on DeviceMesh(N,1), 1 chunk
+    note(f"rank {rank}: extra passes (baseline / e2e)")
     baseline = None
     if world > 1 and not a.no_baseline and not gpt_mode and ((d1, d2) != (world, 1) or chunks != 1):
         try:

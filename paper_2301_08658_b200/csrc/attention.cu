@@ -576,6 +576,255 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
   }
 }
 
+// ---------------------------------------------------------------- forward v3
+// As v2 (two 128-row query tiles per CTA, P through TMEM, MMA ping-pong), but
+// TWO softmax threads per query row: each tile has 8 softmax warps (warps
+// 2-9: tile 0, 10-17: tile 1); warp w reads TMEM lane quadrant w % 4 and
+// column half ((w - 2) % 8) / 4 of the score row.  The row max is combined
+// through shared memory (one named barrier per tile and step, double-buffered
+// by step parity); the row sums stay per half until the end.  Every SM
+// sub-partition then runs two softmax warps per tile instead of one, so the
+// exp / convert / TMEM-store chain of one warp hides behind the other's —
+// v2's softmax ran at about half the MUFU rate with one warp per
+// sub-partition.  The lazy-rescale decision is identical in both halves (same
+// row maxima, same history).
+constexpr int kFwd3Threads = 576;
+constexpr int kFwd3Smem = 6 * kTile + 128 + 4096 + 1024;
+
+__global__ void __launch_bounds__(kFwd3Threads, 1) attn_fwd3_kernel(const __grid_constant__ CUtensorMap tm_qkv, FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  auto sQ = [&](int t) { return base + t * kTile; };
+  auto sK = [&](int s) { return base + 2 * kTile + s * 2 * kTile; };
+  auto sV = [&](int s) { return base + 3 * kTile + s * 2 * kTile; };
+  const uint32_t bars = base + 6 * kTile;
+  const uint32_t q_full = bars;
+  auto kv_full = [&](int s) { return bars + 8 + 8 * s; };
+  auto kv_empty = [&](int s) { return bars + 24 + 8 * s; };
+  auto s_full = [&](int t) { return bars + 40 + 8 * t; };
+  auto p_full = [&](int t) { return bars + 56 + 8 * t; };
+  auto o_done = [&](int t) { return bars + 72 + 8 * t; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 88 - raw));
+  // row-max exchange: [tile][parity][half][128 rows] fp32
+  float* xbuf = reinterpret_cast<float*>(smem_raw + (bars + 128 - raw));
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nq = p.seq / BQ, nm = (nq + 1) / 2, nseq = p.T / p.seq;
+  const int per = p.heads * nseq;
+  int m, rest;
+  cta_order(p.grouped, per, nm, m, rest);
+  if (p.causal) m = nm - 1 - m;  // heaviest first
+  const int head = rest % p.heads, sq = rest / p.heads;
+  const int row0 = sq * p.seq;
+  int qblk[2], n[2];
+  for (int t = 0; t < 2; ++t) {
+    qblk[t] = 2 * m + t;
+    n[t] = qblk[t] < nq ? (p.causal ? qblk[t] + 1 : nq) : 0;
+  }
+  const int nkv = n[0] > n[1] ? n[0] : n[1];
+  const int qcol = head * 3 * HD;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(kv_full(s), 1);
+      ptx::mbar_init(kv_empty(s), 1);
+      ptx::mbar_init(s_full(s), 1);
+      ptx::mbar_init(p_full(s), 256);
+      ptx::mbar_init(o_done(s), 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tm_qkv);
+      ptx::mbar_arrive_expect_tx(q_full, (n[1] > 0 ? 2 : 1) * kTile);
+      for (int t = 0; t < 2; ++t) {
+        if (n[t] == 0) continue;
+        const int qr = row0 + qblk[t] * BQ;
+        ptx::tma_load_2d(sQ(t), &tm_qkv, q_full, qcol, qr);
+        ptx::tma_load_2d(sQ(t) + kHalf, &tm_qkv, q_full, qcol + 64, qr);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j & 1;
+        ptx::mbar_wait(kv_empty(s), ((j >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(kv_full(s), 2 * kTile);
+        const int kr = row0 + j * BKV;
+        ptx::tma_load_2d(sK(s), &tm_qkv, kv_full(s), qcol + HD, kr);
+        ptx::tma_load_2d(sK(s) + kHalf, &tm_qkv, kv_full(s), qcol + HD + 64, kr);
+        ptx::tma_load_2d(sV(s), &tm_qkv, kv_full(s), qcol + 2 * HD, kr);
+        ptx::tma_load_2d(sV(s) + kHalf, &tm_qkv, kv_full(s), qcol + 2 * HD + 64, kr);
+      }
+    }
+  } else if (warp == 1) {
+    {  // identical to v2: the whole warp runs the issue loop, one elected lane issues
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, 128, 0, 1);
+      auto adv = [](uint64_t d, uint32_t bytes) { return d + (bytes >> 4); };
+      const uint64_t q_kmaj[2] = {ptx::smem_desc_sw128(sQ(0), 16, 1024), ptx::smem_desc_sw128(sQ(1), 16, 1024)};
+      const uint64_t k_kmaj[2] = {ptx::smem_desc_sw128(sK(0), 16, 1024), ptx::smem_desc_sw128(sK(1), 16, 1024)};
+      const uint64_t v_mnmaj[2] = {ptx::smem_desc_sw128(sV(0), kHalf, 1024), ptx::smem_desc_sw128(sV(1), kHalf, 1024)};
+      int kv_seen = -1;
+      auto need_kv = [&](int j) {
+        if (j > kv_seen) {
+          ptx::mbar_wait(kv_full(j & 1), (j >> 1) & 1);
+          ptx::tc_fence_after();
+          kv_seen = j;
+        }
+      };
+      auto issue_s = [&](int t, int j) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ptx::mma_bf16_ss_w(tmem + 256 * t, adv(q_kmaj[t], (kk >> 2) * kHalf + (kk & 3) * 32),
+                             adv(k_kmaj[j & 1], (kk >> 2) * kHalf + (kk & 3) * 32), idesc_s, kk > 0 ? 1u : 0u);
+        ptx::mma_commit_w(s_full(t));
+      };
+      ptx::mbar_wait(q_full, 0);
+      need_kv(0);
+      for (int t = 0; t < 2; ++t)
+        if (n[t] > 0) issue_s(t, 0);
+      for (int j = 0; j < nkv; ++j) {
+        for (int t = 0; t < 2; ++t) {
+          if (j >= n[t]) continue;
+          ptx::mbar_wait(p_full(t), j & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            ptx::mma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, adv(v_mnmaj[j & 1], kk * 2048), idesc_o,
+                               (j | kk) != 0 ? 1u : 0u);
+          if (j + 1 == n[t]) ptx::mma_commit_w(o_done(t));
+          if (j + 1 < n[t]) {
+            need_kv(j + 1);
+            issue_s(t, j + 1);
+          }
+        }
+        ptx::mma_commit_w(kv_empty(j & 1));
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax of tile t, row r, column half hf
+    const int t = (warp - 2) / 8;
+    const int hf = ((warp - 2) % 8) / 4;
+    const int nt = t ? n[1] : n[0], qbt = t ? qblk[1] : qblk[0];
+    const int q4 = warp % 4;  // TMEM lane quarter this warp may access
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t tS = tmem + lane_off + 256 * t, tO = tS + 128;
+    constexpr int HC = BKV / 2;  // score columns per thread
+    float m_run = -INFINITY, l = 0.f;
+    for (int j = 0; j < nt; ++j) {
+      ptx::mbar_wait(s_full(t), j & 1);
+      ptx::tc_fence_after();
+      uint32_t u[HC / 32][32];
+#pragma unroll
+      for (int c = 0; c < HC / 32; ++c) ptx::tmem_ld_32x32b_x32(tS + HC * hf + c * 32, u[c]);
+      ptx::tmem_wait_ld();
+      if (p.causal && j == qbt) {  // diagonal block: keys after the query row are masked
+#pragma unroll
+        for (int c = 0; c < HC; ++c)
+          if (HC * hf + c > r) u[c / 32][c % 32] = __float_as_uint(-INFINITY);
+      }
+      float mx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(u[i / 32][i % 32]);
+#pragma unroll
+      for (int c = 8; c < HC; c += 2)
+        mx[(c / 2) % 8] = fmax3(mx[(c / 2) % 8], __uint_as_float(u[c / 32][c % 32]), __uint_as_float(u[c / 32][c % 32 + 1]));
+      float mb = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
+      // the other half's maximum (after this barrier every thread of the tile
+      // has also finished reading S, so P may overwrite any S column)
+      float* xb = xbuf + ((t * 2 + (j & 1)) * 2) * 128;
+      xb[hf * 128 + r] = mb;
+      ptx::named_bar_sync(1 + t, 256);
+      mb = fmaxf(mb, xb[(hf ^ 1) * 128 + r]) * p.scale_log2;
+      const bool rescale = __any_sync(0xffffffffu, mb > m_run + 8.f);
+      float f = 1.f;
+      if (rescale) {
+        const float m_new = fmaxf(m_run, mb);
+        f = ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2), nm2 = f2pack(-m_run, -m_run);
+      uint64_t rsv[2] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f)};
+#pragma unroll
+      for (int c = 0; c < HC / 32; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float x0, x1;
+          f2unpack(ffma2(f2pack(__uint_as_float(u[c][2 * i]), __uint_as_float(u[c][2 * i + 1])), sc2, nm2), x0, x1);
+          const float e0 = ex2(x0), e1 = ex2(x1);
+          rsv[i % 2] = fadd2(rsv[i % 2], f2pack(e0, e1));
+          pk[i] = pack_bf16(e0, e1);
+        }
+        ptx::tmem_st_32x32b_x16(tS + HC / 2 * hf + c * 16, pk);  // P (bf16 pairs) of this half
+      }
+      float ra, rb, rc, rd;
+      f2unpack(rsv[0], ra, rb);
+      f2unpack(rsv[1], rc, rd);
+      l = l * f + ((ra + rb) + (rc + rd));  // this half's partial row sum
+      if (rescale && j > 0) {
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          uint32_t o[32];
+          ptx::tmem_ld_32x32b_x32(tO + (HD / 2) * hf + c * 32, o);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+          ptx::tmem_st_32x32b_x32(tO + (HD / 2) * hf + c * 32, o);
+        }
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full(t));
+    }
+    if (nt > 0) {
+      // full row sum = both halves' partial sums (same rescale history)
+      float* xb = xbuf + ((t * 2 + (nt & 1)) * 2) * 128;
+      xb[hf * 128 + r] = l;
+      ptx::named_bar_sync(1 + t, 256);
+      l += xb[(hf ^ 1) * 128 + r];
+      ptx::mbar_wait(o_done(t), 0);
+      ptx::tc_fence_after();
+      const float inv = 1.f / l;
+      const int qrow = row0 + qbt * BQ + r;
+      __nv_bfloat16* orow = p.ctx + static_cast<int64_t>(qrow) * p.ld_ctx + head * HD + (HD / 2) * hf;
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        uint32_t u[32];
+        ptx::tmem_ld_32x32b_x32(tO + (HD / 2) * hf + c * 32, u);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + 8 * v) = w;
+        }
+      }
+      if (hf == 0) p.lse[static_cast<int64_t>(head) * p.T + qrow] = (m_run + log2f(l)) * kLn2;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 // ================================================================ backward
 // dV = P^T dO, dP = dO V^T, dS = P * (dP - D) with D = rowsum(dO * O),
 // dQ = dS K / sqrt(d), dK = dS^T Q / sqrt(d)   (FlashAttention-2 order).
@@ -1194,14 +1443,19 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
                             int64_t ld_ctx, float* lse, cudaStream_t st) {
   alignas(64) CUtensorMap tm;
   if (!tmap_bf16_2d(&tm, qkv, T, 3 * heads * HD, ld_qkv, 128, 64)) return cudaErrorInvalidValue;
-  static const bool v1 = [] {
+  // ATP_ATTN_FWD = 1 / 2 / 3: forward kernel version (default 2; v3, two
+  // softmax threads per row, measured 4-5% slower: profiles/r02_attn_fwd_v3.log)
+  static const int fwd_ver = [] {
     const char* e = getenv("ATP_ATTN_FWD");
-    return e && e[0] == '1';
+    return e ? atoi(e) : 2;
   }();
+  const bool v1 = fwd_ver == 1;
   static bool attr = [] {
     return cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem) ==
                cudaSuccess &&
            cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(attn_fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwd3Smem) ==
                cudaSuccess;
   }();
   (void)attr;
@@ -1240,8 +1494,10 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
   p.lse = lse;
   if (v1) {
     attn_fwd_kernel<<<(seq / BQ) * heads * (T / seq), 256, kFwdSmem, st>>>(tm, p);
-  } else {
+  } else if (fwd_ver == 2) {
     attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwdSmem, st>>>(tm, p);
+  } else {
+    attn_fwd3_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), kFwd3Threads, kFwd3Smem, st>>>(tm, p);
   }
   return cudaGetLastError();
 }

@@ -113,7 +113,8 @@ __device__ __forceinline__ void finish8(const FusedArArgs& a, int64_t g, int64_t
       for (int e = 0; e < 8; ++e) v[e] = x[e] + v[e];
       break;
     case EW_CORE_BWD: {  // dQ = dK = dV = dctx of the head
-      const int64_t hd = c8 / a.head_dim, jj = c8 % a.head_dim;
+      const uint32_t hd = static_cast<uint32_t>(c8) / static_cast<uint32_t>(a.head_dim);
+      const uint32_t jj = static_cast<uint32_t>(c8) - hd * static_cast<uint32_t>(a.head_dim);
       bf* dst = static_cast<bf*>(a.ew_out) + g * a.ew_ld + hd * 3 * a.head_dim + jj;
       store8(dst, v);
       store8(dst + a.head_dim, v);
@@ -138,7 +139,8 @@ __device__ __forceinline__ void finish_core(const FusedArArgs& a, int64_t g, int
   float c[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) c[e] = (q[e] + k[e]) + v[e];
-  const int64_t hd = col_q / (3 * d), jj = col_q % (3 * d);
+  const uint32_t hd = static_cast<uint32_t>(col_q) / static_cast<uint32_t>(3 * d);
+  const uint32_t jj = static_cast<uint32_t>(col_q) - hd * static_cast<uint32_t>(3 * d);
   store8(static_cast<bf*>(a.ew_out) + g * a.ew_ld + hd * d + jj, c);
 }
 
@@ -175,6 +177,22 @@ __device__ __forceinline__ void stream_pieces(uint32_t sbase, uint32_t bar0, uin
   }
 }
 
+// (row, column) of a thread's successive items inside a piece without a
+// 64-bit division per item: items advance by a fixed element stride, so the
+// cursor advances by precomputed (rows, columns) of that stride.
+struct Cursor {
+  uint32_t row, col;
+  __device__ __forceinline__ Cursor(uint32_t pos, uint32_t width) : row(pos / width), col(pos - (pos / width) * width) {}
+  __device__ __forceinline__ void step(uint32_t drow, uint32_t dcol, uint32_t width) {
+    row += drow;
+    col += dcol;
+    if (col >= width) {
+      col -= width;
+      ++row;
+    }
+  }
+};
+
 // PHASE 0 = A (needs only the GEMMs' tiles), PHASE 1 = B + C (needs the
 // peers' phase A).  Two launches per chunk: a CTA that spins on a peer never
 // holds an SM that a phase-A CTA of its own rank needs, so partially resident
@@ -185,7 +203,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_ar_kernel(FusedArArgs 
   const int tid = threadIdx.x, nt = blockDim.x;
   const bool core = a.ew_kind == EW_CORE_FWD;
   const bool side = a.ew_kind == EW_ADD || a.ew_kind == EW_DGELU;  // side input staged with the values
-  const int64_t S = a.rows / a.p, w8 = a.width / 8, d = a.head_dim;
+  const int64_t S = a.rows / a.p, d = a.head_dim;
   const int64_t row_bytes = a.ld * 2;
   const uint32_t sbase = (ptx::smem_u32(smem_raw) + 127u) & ~127u;
   const uint32_t bar0 = sbase + kFusedStages * kFusedStageBytes;
@@ -201,6 +219,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_ar_kernel(FusedArArgs 
   const int64_t piece = (kFusedStageBytes / nbuf_a / unit) * unit;
   const char* ewa = static_cast<const char*>(a.ew_a);
   uint32_t consumed = 0;
+  // per-thread item strides in elements: generic items are 8-element vectors
+  // (stride nt * 8); core items advance by nt / per whole (q, k, v) triples
+  const uint32_t W = static_cast<uint32_t>(a.width);
+  const uint32_t per = core ? static_cast<uint32_t>(d / 8) : 1u;  // ctx vectors per head triple
+  const uint32_t dstep = core ? (static_cast<uint32_t>(nt) / per) * static_cast<uint32_t>(3 * d)
+                              : static_cast<uint32_t>(nt) * 8u;
+  const uint32_t drow = dstep / W, dcol = dstep - drow * W;
   if (tid == 0) {
     for (int s = 0; s < kFusedStages; ++s) ptx::mbar_init(bar0 + 8u * s, 1);
     ptx::fence_barrier_init();
@@ -219,10 +244,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_ar_kernel(FusedArArgs 
     bf* dst = reinterpret_cast<bf*>(const_cast<char*>(src[a.me]));  // the sum goes back in place (my slot)
     stream_pieces(sbase, bar0, consumed, nbuf_a, src, piece, b_lo, b_hi, [&](uint32_t stg, int64_t off, int64_t nb) {
       if (core) {
-        const int64_t per = d / 8, items = nb / unit * per;
-        for (int64_t it = tid; it < items; it += nt) {
-          const int64_t tt = it / per, jj = (it % per) * 8;
-          const uint32_t e0 = static_cast<uint32_t>((tt * 3 * d + jj) * 2);
+        const uint32_t items = static_cast<uint32_t>(nb / unit) * per;
+        const uint32_t tt0 = static_cast<uint32_t>(tid) / per, jj = (static_cast<uint32_t>(tid) - tt0 * per) * 8u;
+        uint32_t e0 = (tt0 * 3u * static_cast<uint32_t>(d) + jj) * 2u;  // byte offset in the piece
+        Cursor cur(static_cast<uint32_t>(off / 2) + e0 / 2u, W);
+        for (uint32_t it = tid; it < items; it += nt, e0 += dstep * 2u, cur.step(drow, dcol, W)) {
           float q[8], k[8], v[8], t[8];
           lds8(stg + e0, q);
           lds8(stg + e0 + 2 * d, k);
@@ -242,16 +268,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_ar_kernel(FusedArArgs 
           round8(q);
           round8(k);
           round8(v);
-          const int64_t pos = off / 2 + tt * 3 * d + jj;  // element of the slice
-          store8(dst + pos, q);
-          store8(dst + pos + d, k);
-          store8(dst + pos + 2 * d, v);
-          finish_core(a, g0 + pos / a.width, pos % a.width, q, k, v);
+          bf* dq = dst + (off + e0) / 2;  // the sum back in place (element off/2 + e0/2 of the slice)
+          store8(dq, q);
+          store8(dq + d, k);
+          store8(dq + 2 * d, v);
+          finish_core(a, g0 + cur.row, cur.col, q, k, v);
         }
       } else {
-        const int64_t items = nb / 16, v0 = off / 16;
-        for (int64_t it = tid; it < items; it += nt) {
-          const uint32_t e0 = static_cast<uint32_t>(it * 16);
+        const uint32_t items = static_cast<uint32_t>(nb / 16);
+        Cursor cur(static_cast<uint32_t>(off / 2) + static_cast<uint32_t>(tid) * 8u, W);
+        for (uint32_t it = tid; it < items; it += nt, cur.step(drow, dcol, W)) {
+          const uint32_t e0 = it * 16u;
           float acc[8], t[8], x[8];
           lds8(stg + e0, acc);
           for (int m = 1; m < a.p; ++m) {
@@ -260,10 +287,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_ar_kernel(FusedArArgs 
             for (int e = 0; e < 8; ++e) acc[e] += t[e];
           }
           round8(acc);
-          const int64_t vi = v0 + it;
-          store8(dst + vi * 8, acc);
+          store8(dst + off / 2 + e0 / 2, acc);
           if (side) lds8(stg + static_cast<uint32_t>(a.p * piece) + e0, x);
-          finish8(a, g0 + vi / w8, (vi % w8) * 8, acc, x);
+          finish8(a, g0 + cur.row, cur.col, acc, x);
         }
       }
     });
@@ -291,26 +317,26 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_ar_kernel(FusedArArgs 
     }
     stream_pieces(sbase, bar0, consumed, nbuf_b, src, piece, b_lo, b_hi, [&](uint32_t stg, int64_t off, int64_t nb) {
       if (core) {
-        const int64_t per = d / 8, items = nb / unit * per;
-        for (int64_t it = tid; it < items; it += nt) {
-          const int64_t tt = it / per, jj = (it % per) * 8;
-          const uint32_t e0 = static_cast<uint32_t>((tt * 3 * d + jj) * 2);
+        const uint32_t items = static_cast<uint32_t>(nb / unit) * per;
+        const uint32_t tt0 = static_cast<uint32_t>(tid) / per, jj = (static_cast<uint32_t>(tid) - tt0 * per) * 8u;
+        uint32_t e0 = (tt0 * 3u * static_cast<uint32_t>(d) + jj) * 2u;
+        Cursor cur(static_cast<uint32_t>(off / 2) + e0 / 2u, W);
+        for (uint32_t it = tid; it < items; it += nt, e0 += dstep * 2u, cur.step(drow, dcol, W)) {
           float q[8], k[8], v[8];
           lds8(stg + e0, q);
           lds8(stg + e0 + 2 * d, k);
           lds8(stg + e0 + 4 * d, v);
-          const int64_t pos = off / 2 + tt * 3 * d + jj;
-          finish_core(a, gj + pos / a.width, pos % a.width, q, k, v);
+          finish_core(a, gj + cur.row, cur.col, q, k, v);
         }
       } else {
-        const int64_t items = nb / 16, v0 = off / 16;
-        for (int64_t it = tid; it < items; it += nt) {
-          const uint32_t e0 = static_cast<uint32_t>(it * 16);
+        const uint32_t items = static_cast<uint32_t>(nb / 16);
+        Cursor cur(static_cast<uint32_t>(off / 2) + static_cast<uint32_t>(tid) * 8u, W);
+        for (uint32_t it = tid; it < items; it += nt, cur.step(drow, dcol, W)) {
+          const uint32_t e0 = it * 16u;
           float v[8], x[8];
           lds8(stg + e0, v);
           if (side) lds8(stg + static_cast<uint32_t>(piece) + e0, x);
-          const int64_t vi = v0 + it;
-          finish8(a, gj + vi / w8, (vi % w8) * 8, v, x);
+          finish8(a, gj + cur.row, cur.col, v, x);
         }
       }
     });

@@ -44,7 +44,12 @@ def main():
 
     path = sys.argv[1]
     busbw = float(sys.argv[2]) if len(sys.argv) > 2 else 725.0
-    peak = 1400.8  # MEASURED_PEAKS.json bf16_tflops_sustained
+    try:
+        pk = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                         "MEASURED_PEAKS.json")))
+        burst, sustained = pk["bf16_tflops"], pk["bf16_tflops_sustained"]
+    except (OSError, KeyError, ValueError):
+        burst, sustained = 1590.0, 1400.0  # B200_PROFILING.md fallback
     T = 8192
     for line in open(path):
         r = json.loads(line)
@@ -54,12 +59,16 @@ def main():
         mk, ex = atp.atp_overlap_estimate(st, c, "signalled")
         comm = sum(s[2] for s in st)
         fl = 72.0 * T * h * h / (d1 * d2)
-        roof = max(fl / (peak * 1e9), comm)  # ms: tensor time at the sustained peak vs NVLink time
+        nvl = comm * busbw / 900.0  # the same ring bytes at NVLink's 900 GB/s per direction
+        roof = {  # ms: max(tensor time, NVLink time) -- SURVEY §8(d)'s definition, three tensor peaks
+            "survey_2.25PF": max(fl / 2.25e12, nvl), "burst": max(fl / (burst * 1e9), nvl),
+            "sustained": max(fl / (sustained * 1e9), nvl)}
         print(json.dumps({"cfg": r["cfg"], "h": h, "mesh": [d1, d2], "chunks": c,
                           "compute_ms": r["ms_compute_per_rank"], "comm_ms": round(comm, 4),
                           "predicted_ms": round(mk, 4), "predicted_exposed_ms": round(ex, 4),
                           "predicted_exposed_share": round(ex / mk, 3),
-                          "predicted_roofline_frac": round(roof / mk, 3), "model": f"overlap model, busBW {busbw} GB/s"}))
+                          "predicted_roofline_frac": {k: round(v / mk, 3) for k, v in roof.items()},
+                          "model": f"overlap model, busBW {busbw} GB/s"}))
 
 
 if __name__ == "__main__":

@@ -38,7 +38,8 @@ def test_bench_json_contract_n1():
     # the GEMM time comes from a CUPTI trace of the graph-launched step
     kt = d["kernel_trace"]
     assert "error" not in kt, kt
-    assert kt["gemm_launches_per_step"] == 12 and 0.5 < r["gemm_share_of_step"] <= 1.0
+    # (CUPTI GEMM time vs the event-timed step of another pass: equal within noise when GEMMs fill the step)
+    assert kt["gemm_launches_per_step"] == 12 and 0.5 < r["gemm_share_of_step"] <= 1.02
     assert d["config"]["hidden"] == 12288 and d["config"]["heads"] == 96  # N=1 default: cfg 5 shape
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     e = d["e2e"]
@@ -83,3 +84,32 @@ def test_bench_n2_shared_gpu():
     # --try-fused timed the fused GEMM -> reduce-scatter -> all-gather path (CUDA IPC peers) beside NCCL
     ch = d["allreduce_choice"]
     assert "error" not in ch and {"nccl", "fused"} <= set(ch["timed_ms"]), ch
+
+
+def test_bench_n2_shared_gpu_p2p_disable():
+    """The topology-stress path (the paper's IC1 method P:373):
+    --p2p-disable sets NCCL_P2P_DISABLE=1 before NCCL init, then the probe ->
+    calibrated search runs as usual and the line records the HCM-only and the
+    calibrated rankings and the probe's per-pair matrix (2 ranks sharing the
+    GPU: the numbers mean nothing, the path is what is checked)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--share-gpu", "--p2p-disable", "--steps", "3", "--warmup", "3",
+                          "--hidden", "1024", "--heads", "8", "--batch", "2", "--seq", "1024", "--layers", "1",
+                          "--no-cpu-baseline", "--no-baseline", "--no-e2e", "--probe-mib", "4"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    d = json.loads(lines[-1])
+    assert d["config"]["nccl_p2p_disable"] is True and d["probe"]["nccl_p2p_disable"] is True
+    assert len(d["probe"]["p2p_matrix_gbps"]) == 2 and d["probe"]["calibration_algbw_gbps"]
+    assert d["search"]["chosen"] == d["config"]["mesh"]
+    assert {tuple(r[:2]) for r in d["search"]["ranked"]} == {(2, 1), (1, 2)}
+    assert {tuple(r[:2]) for r in d["search"]["hcm_only"]["ranked"]} == {(2, 1), (1, 2)}
+    assert all(r[3] for r in d["search"]["ranked"]) and not any(r[3] for r in d["search"]["hcm_only"]["ranked"])

@@ -25,6 +25,7 @@ def _replay_matches(mesh, bufs, call, keys, stream, n_replays=3):
             for b in bufs:
                 for k in keys:
                     b[k].fill_(float("nan"))
+            torch.cuda.synchronize()  # the fills (default stream) must land before the replay (its own stream)
             g(stream)
             stream.synchronize()
             for b, r in zip(bufs, ref):
