@@ -438,16 +438,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         ptx::bulk_wait0();  // this warp's stores of the pending tile are complete ...
         asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and ordered before generic accesses
-        __threadfence_system();
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      // one release at system scope, cumulative over every epilogue warp's
+      // stores through the barrier (NCCL, the stream-wait engine or a peer
+      // rank reads them); a full fence.sc.sys per warp and tile stalled the
+      // epilogue for microseconds on the short-K GEMMs
       if (warp == 2 && lane == 0) {
-        __threadfence_system();
-        if (push.p > 0) {
-          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(push.sig[pend_pj] + pend_chunk) : "memory");
-        } else {
-          atomicAdd(sig + pend_chunk, 1u);
-        }
+        uint32_t* ctr = push.p > 0 ? push.sig[pend_pj] + pend_chunk : sig + pend_chunk;
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
       }
       pend_chunk = -1;
     };
