@@ -109,6 +109,14 @@ static cudaError_t wait_sig(RankState& s, const Op& op, cudaStream_t st) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
 }
 uint64_t launch_count() { return g_launches.load(); }
+int fused_ctas() {
+  static const int v = [] {
+    const char* e = getenv("ATP_FUSED_CTAS");
+    const int n = e ? atoi(e) : 0;
+    return n > 0 ? n : kFusedCtas;
+  }();
+  return v;
+}
 
 // Algorithmic cost of one op (class 0 = GEMM, 1 = elementwise, 2 = all-reduce).
 void op_cost(const Op& op, int p, int* cls, double* flops, double* bytes) {

@@ -136,5 +136,6 @@ bool stream_wait_available();
 int enable_fused_ar(atp_mesh* m, size_t part_bytes);
 int debug_counters(atp_mesh* m, int rank, uint32_t* out, int n);
 constexpr int kFusedCtas = 32;  // CTAs of one fused all-reduce kernel: 2 per SM on the 16 SMs the GEMM cap leaves
+int fused_ctas();                // kFusedCtas, or ATP_FUSED_CTAS (SM-budget A/B runs)
 
 }  // namespace atp

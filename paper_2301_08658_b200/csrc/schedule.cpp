@@ -351,7 +351,7 @@ struct Builder {
           f.slot_rows = T / p_grp;
           f.sig_slot = slot0 + k;
           f.out = out;
-          f.n_ctas = kFusedCtas;
+          f.n_ctas = fused_ctas();
           if (!post.empty()) {
             const EwDesc& e = post[0];
             f.ew_kind = e.kind;
