@@ -25,7 +25,10 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
+#include <cmath>
 #include <mutex>
+#include <vector>
 
 #include "atp_internal.h"
 #include "gelu.cuh"
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                       int M, int N, int K, EpiParams ep, uint32_t* sig, int sig_rows, const uint32_t* gate,
                       uint32_t gate_target, int group_m, int kserp, int l2hint,
-                      const __grid_constant__ PushArgs push) {
+                      const __grid_constant__ PushArgs push, const uint16_t* die_tab, int dpairs0, int dpairs1) {
   using L = SmemLayout<CG, BN, STAGES>;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr int BNC = BN / CG;  // B rows loaded by this CTA
@@ -233,10 +236,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_m = (M + BM * CG - 1) / (BM * CG);
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
-  const int num_tiles = num_m * num_n;
-  const int mt_chunk = sig_rows > 0 ? sig_rows / (BM * CG) : num_m;  // M-tiles per chunk
-  const int unit = blockIdx.x / CG;      // tile-processing unit (CTA or CTA pair)
-  const int n_units = gridDim.x / CG;
+  int num_tiles = num_m * num_n;
+  int mt_chunk = sig_rows > 0 ? sig_rows / (BM * CG) : num_m;  // M-tiles per chunk
+  int unit = blockIdx.x / CG;      // tile-processing unit (CTA or CTA pair)
+  int n_units = gridDim.x / CG;
+  int m_lo = 0;                    // first M-tile of this unit's tile space
+  uint32_t* die_slot = tmem_slot + 1;
+  if (die_tab != nullptr && leader && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    *die_slot = die_tab[smid];  // broadcast to the peer CTA after the cluster barrier below
+  }
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -271,6 +281,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (die_tab != nullptr) {
+    // Die-aware tiles (ATP_DIE_AWARE; CTA pairs, one CTA per SM, unsignalled):
+    // the pairs of each die work on their own share of the M-tiles, so the
+    // operand panels a die streams are not fetched into both dies' L2; the
+    // pair index within its die comes from the SM -> die table measured at
+    // start-up, read by the leader CTA and shared with its peer.
+    uint32_t e;
+    if (leader) {
+      e = *reinterpret_cast<volatile uint32_t*>(die_slot);
+    } else {
+      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(e) : "r"(ptx::mapa_shared(ptx::smem_u32(die_slot), 0)));
+    }
+    const int die = static_cast<int>(e >> 15);
+    const int m0 = static_cast<int>((static_cast<int64_t>(num_m) * dpairs0) / (dpairs0 + dpairs1));
+    unit = static_cast<int>(e & 0x7fffu);
+    n_units = die ? dpairs1 : dpairs0;
+    m_lo = die ? m0 : 0;
+    mt_chunk = die ? num_m - m0 : m0;
+    num_tiles = mt_chunk * num_n;
+  }
   // Programmatic dependent launch: the set-up above (barriers, TMEM, tensor-map
   // prefetch) overlapped the previous kernel's tail; the next GEMM may now be
   // scheduled onto SMs as this grid's CTAs retire, and nothing here touches
@@ -292,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int tile = unit; tile < num_tiles; tile += n_units) {
         int mt, nt, chunk;
         tile_coords(tile, mt_chunk, num_n, group_m, mt, nt, chunk);
+        mt += m_lo;
         const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
         const int nb = nt * BN + BNC * static_cast<int>(cta_rank);
         if (gate != nullptr && chunk > gated_chunk) {  // tiles are chunk-major: chunk only grows
@@ -453,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int tile = unit; tile < num_tiles; tile += n_units) {
       int mt, nt, chunk;
       tile_coords(tile, mt_chunk, num_n, group_m, mt, nt, chunk);
+      mt += m_lo;
       const int m0 = mt * BM * CG + BM * static_cast<int>(cta_rank);
       const int n0 = nt * BN;
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
@@ -549,6 +581,167 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- SM -> die map
+// B200 is two dies; each address is homed in one die's L2 (2 KB granularity)
+// and an SM reaches its own die's L2 ~30 cycles faster than the other's.  One
+// CTA per SM times dependent L2 (.cg) loads to 256 addresses 2 KB apart; SMs
+// of one die share the near/far pattern (profiles/r02_die_probe.md).
+constexpr int kDieAddrs = 256, kDieStride = 2048, kDieReps = 8;
+
+__global__ void die_latency_kernel(const uint32_t* buf, uint32_t* lat, int* smid_out) {
+  extern __shared__ uint8_t pad[];
+  if (threadIdx.x != 0) return;
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  smid_out[blockIdx.x] = static_cast<int>(smid);
+  pad[0] = 0;
+  uint32_t dep = 0;
+  for (int i = 0; i < kDieAddrs; ++i) {
+    const uint32_t* p = buf + (static_cast<size_t>(i) * kDieStride) / 4;
+    uint32_t idx = dep;  // the buffer holds zeros: every load's address depends on the previous value
+    long long t0, t1;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0)::"memory");
+#pragma unroll 1
+    for (int r = 0; r < kDieReps; ++r) asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(idx) : "l"(p + idx) : "memory");
+    asm volatile("add.u32 %0, %0, %1;" : "+r"(dep) : "r"(idx) : "memory");
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1)::"memory");
+    lat[blockIdx.x * kDieAddrs + i] = static_cast<uint32_t>((t1 - t0) / kDieReps);
+  }
+  if (dep == 0xdeadbeefu) smid_out[blockIdx.x] = -1;  // keeps the load chain live
+}
+
+// Which SMs the CTA pairs of a 2-CTA cluster occupy (one CTA per SM).
+__global__ void die_pair_kernel(int* out) {
+  extern __shared__ uint8_t pad[];
+  if (threadIdx.x != 0) return;
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  pad[0] = 0;
+  out[blockIdx.x] = static_cast<int>(smid);
+}
+
+std::atomic<bool> g_die_ready{false};
+bool die_table_ready() { return g_die_ready.load(); }
+
+struct DieTable {
+  uint16_t* dev = nullptr;  // [num SMs]: die << 15 | pair index within the die
+  int pairs[2] = {0, 0};
+  bool ok = false;
+};
+
+// Measured once per process (ATP_DIE_AWARE=1 only).  Any inconsistency (not
+// exactly two clusters of SMs, odd SM counts per die, a cluster pair spanning
+// dies or changing between launches) disables the die-aware tile order.
+const DieTable& die_table() {
+  static DieTable t;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const int nsm = num_sms();
+    uint32_t *buf = nullptr, *lat = nullptr;
+    int* ids = nullptr;
+    const size_t bytes = static_cast<size_t>(kDieAddrs) * kDieStride;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess || cudaMalloc(&lat, sizeof(uint32_t) * nsm * kDieAddrs) != cudaSuccess ||
+        cudaMalloc(&ids, sizeof(int) * 3 * nsm) != cudaSuccess)
+      return;
+    const int smem = 200 * 1024;  // one CTA per SM
+    cudaMemset(buf, 0, bytes);
+    cudaFuncSetAttribute(die_latency_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(die_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int it = 0; it < 2; ++it) die_latency_kernel<<<nsm, 32, smem>>>(buf, lat, ids);  // first pass warms L2
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nsm);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, die_pair_kernel, ids + nsm);
+    cudaLaunchKernelEx(&cfg, die_pair_kernel, ids + 2 * nsm);
+    std::vector<uint32_t> h(static_cast<size_t>(nsm) * kDieAddrs);
+    std::vector<int> hid(3 * nsm);
+    bool good = cudaDeviceSynchronize() == cudaSuccess &&
+                cudaMemcpy(h.data(), lat, h.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                cudaMemcpy(hid.data(), ids, hid.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(buf);
+    cudaFree(lat);
+    cudaFree(ids);
+    if (!good) {
+      cudaGetLastError();
+      return;
+    }
+    // correlate every SM's centred latency pattern with the lowest SM id's
+    std::vector<double> z(h.size());
+    for (int b = 0; b < nsm; ++b) {
+      double mean = 0;
+      for (int i = 0; i < kDieAddrs; ++i) mean += h[b * kDieAddrs + i];
+      mean /= kDieAddrs;
+      for (int i = 0; i < kDieAddrs; ++i) z[b * kDieAddrs + i] = h[b * kDieAddrs + i] - mean;
+    }
+    int ref = 0;
+    for (int b = 1; b < nsm; ++b)
+      if (hid[b] < hid[ref]) ref = b;
+    std::vector<int> die_of_sm(nsm, -1);
+    double nr = 0;
+    for (int i = 0; i < kDieAddrs; ++i) nr += z[ref * kDieAddrs + i] * z[ref * kDieAddrs + i];
+    for (int b = 0; b < nsm; ++b) {
+      double dot = 0, nb = 0;
+      for (int i = 0; i < kDieAddrs; ++i) {
+        dot += z[b * kDieAddrs + i] * z[ref * kDieAddrs + i];
+        nb += z[b * kDieAddrs + i] * z[b * kDieAddrs + i];
+      }
+      const double c = dot / std::sqrt(nr * nb + 1e-30);
+      if (std::fabs(c) < 0.3) return;  // no clear two-die structure
+      if (hid[b] < 0 || hid[b] >= nsm || die_of_sm[hid[b]] != -1) return;
+      die_of_sm[hid[b]] = c > 0 ? 0 : 1;
+    }
+    // cluster pairs: both launches identical (as sets), each pair inside one die
+    std::vector<int> partner(nsm, -1);
+    for (int l = 1; l <= 2; ++l)
+      for (int c = 0; c + 1 < nsm; c += 2) {
+        const int a = hid[l * nsm + c], b = hid[l * nsm + c + 1];
+        if (a < 0 || b < 0 || a >= nsm || b >= nsm || die_of_sm[a] != die_of_sm[b]) return;
+        if (l == 1) {
+          partner[a] = b;
+          partner[b] = a;
+        } else if (partner[a] != b) {
+          return;
+        }
+      }
+    std::vector<uint16_t> tab(nsm, 0);
+    int pairs[2] = {0, 0};
+    for (int sm = 0; sm < nsm; ++sm) {  // pair index = order of the pair's lower SM id within its die
+      const int p = partner[sm];
+      if (p < 0) return;
+      if (sm < p) {
+        const int d = die_of_sm[sm];
+        tab[sm] = tab[p] = static_cast<uint16_t>((d << 15) | pairs[d]);
+        ++pairs[d];
+      }
+    }
+    if (pairs[0] == 0 || pairs[1] == 0) return;
+    if (cudaMalloc(&t.dev, sizeof(uint16_t) * nsm) != cudaSuccess) return;
+    cudaMemcpy(t.dev, tab.data(), sizeof(uint16_t) * nsm, cudaMemcpyHostToDevice);
+    t.pairs[0] = pairs[0];
+    t.pairs[1] = pairs[1];
+    t.ok = true;
+  });
+  g_die_ready = true;
+  return t;
+}
+
+// ATP_DIE_AWARE=1: die-aware tile order for the all-SM CTA-pair GEMMs (A/B runs).
+bool die_aware() {
+  static const bool on = [] {
+    const char* e = getenv("ATP_DIE_AWARE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
@@ -626,8 +819,25 @@ cudaError_t launch_t(const GemmDesc& d, int grid, cudaStream_t st) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (pdl && d.pdl && d.gate == nullptr) ? 2 : 1;
+  // die-aware tile order: CTA pairs on every SM (one CTA per SM), no chunk
+  // signalling / gating / push (their tile order is chunk-major), >= 4 M-tiles
+  const uint16_t* die_tab = nullptr;
+  int dp0 = 0, dp1 = 0;
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  if (CG == 2 && die_aware()) cudaStreamIsCapturing(st, &capturing);
+  // (the table is measured outside any graph capture: the first uncaptured call sets it up)
+  if (CG == 2 && die_aware() && grid == num_sms() && d.sig == nullptr && d.gate == nullptr && d.push.p == 0 &&
+      (d.M + 255) / 256 >= 4 && (capturing == cudaStreamCaptureStatusNone || die_table_ready())) {
+    const DieTable& t = die_table();
+    if (t.ok && 2 * (t.pairs[0] + t.pairs[1]) == grid) {
+      die_tab = t.dev;
+      dp0 = t.pairs[0];
+      dp1 = t.pairs[1];
+    }
+  }
   return cudaLaunchKernelEx(&cfg, kern, d.tmA, d.tmB, d.tmC, d.tmC2, d.M, d.N, d.K, d.ep, d.sig, d.sig_rows, d.gate,
-                            d.gate_target, d.group_m > 0 ? d.group_m : 16, kserp(), l2hint(), d.push);
+                            d.gate_target, d.group_m > 0 ? d.group_m : 16, kserp(), l2hint(), d.push, die_tab, dp0,
+                            dp1);
 }
 
 template <int CG, int BN, int STAGES, bool A_MN, bool B_MN>
