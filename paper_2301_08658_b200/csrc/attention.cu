@@ -118,6 +118,13 @@ struct FwdParams {
   __nv_bfloat16* ctx;
   int64_t ld_ctx;
   float* lse;  // [heads][T], natural log
+  // split-KV (forward v2 on grids smaller than the GPU): kv_split CTAs per
+  // query-tile pair, each over a contiguous share of its KV blocks, writing
+  // unnormalised O (fp32) and (max, sum) per row to opart / mlpart; a combine
+  // kernel merges them.  kv_split == 1: the CTA normalises and writes ctx, lse.
+  int kv_split = 1;
+  float* opart = nullptr;   // [kv_split][T][heads * 128]
+  float* mlpart = nullptr;  // [kv_split][T][heads][2]: running max (log2 domain, scaled), row sum
 };
 
 // CTA order.  G == 0: heaviest work first across the whole grid.  G > 0: the
@@ -125,8 +132,8 @@ struct FwdParams {
 // whose K/V or Q/dO stay in L2 while every block of the chunk re-reads them),
 // heaviest first inside a chunk (so the tail stays light).  `per_group` =
 // CTAs of one group, `j` = heaviness rank inside the group (0 = heaviest).
-__device__ __forceinline__ void cta_order(int G, int n_groups, int per_group, int& j, int& group) {
-  const int b = static_cast<int>(blockIdx.x);
+__device__ __forceinline__ void cta_order(int G, int n_groups, int per_group, int& j, int& group,
+                                          int b = static_cast<int>(blockIdx.x)) {
   if (G <= 0) {
     j = b / n_groups;
     group = b % n_groups;
@@ -369,7 +376,8 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
   const int nq = p.seq / BQ, nm = (nq + 1) / 2, nseq = p.T / p.seq;
   const int per = p.heads * nseq;
   int m, rest;
-  cta_order(p.grouped, per, nm, m, rest);
+  const int split = static_cast<int>(blockIdx.x) % p.kv_split;
+  cta_order(p.grouped, per, nm, m, rest, static_cast<int>(blockIdx.x) / p.kv_split);
   if (p.causal) m = nm - 1 - m;  // heaviest first
   const int head = rest % p.heads, sq = rest / p.heads;
   const int row0 = sq * p.seq;
@@ -378,7 +386,13 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
     qblk[t] = 2 * m + t;
     n[t] = qblk[t] < nq ? (p.causal ? qblk[t] + 1 : nq) : 0;
   }
-  const int nkv = n[0] > n[1] ? n[0] : n[1];
+  const int nkv_all = n[0] > n[1] ? n[0] : n[1];
+  // this CTA's KV blocks [j0, j1); tile t runs [j0, min(j1, n[t])) -- nl[t] steps
+  const int kv_per = (nkv_all + p.kv_split - 1) / p.kv_split;
+  const int j0 = min(nkv_all, split * kv_per), j1 = min(nkv_all, j0 + kv_per);
+  const int nkv = j1 - j0;
+  int nl[2];
+  for (int t = 0; t < 2; ++t) nl[t] = max(0, min(j1, n[t]) - j0);
   const int qcol = head * 3 * HD;
 
   if (threadIdx.x == 0) {
@@ -404,18 +418,18 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
   if (warp == 0) {
     if (lane == 0) {
       ptx::prefetch_tmap(&tm_qkv);
-      ptx::mbar_arrive_expect_tx(q_full, (n[1] > 0 ? 2 : 1) * kTile);
+      ptx::mbar_arrive_expect_tx(q_full, ((nl[0] > 0 ? 1 : 0) + (nl[1] > 0 ? 1 : 0)) * kTile);
       for (int t = 0; t < 2; ++t) {
-        if (n[t] == 0) continue;
+        if (nl[t] == 0) continue;
         const int qr = row0 + qblk[t] * BQ;
         ptx::tma_load_2d(sQ(t), &tm_qkv, q_full, qcol, qr);
         ptx::tma_load_2d(sQ(t) + kHalf, &tm_qkv, q_full, qcol + 64, qr);
       }
-      for (int j = 0; j < nkv; ++j) {
+      for (int j = 0; j < nkv; ++j) {  // local step j = KV block j0 + j
         const int s = j & 1;
         ptx::mbar_wait(kv_empty(s), ((j >> 1) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(kv_full(s), 2 * kTile);
-        const int kr = row0 + j * BKV;
+        const int kr = row0 + (j0 + j) * BKV;
         ptx::tma_load_2d(sK(s), &tm_qkv, kv_full(s), qcol + HD, kr);
         ptx::tma_load_2d(sK(s) + kHalf, &tm_qkv, kv_full(s), qcol + HD + 64, kr);
         ptx::tma_load_2d(sV(s), &tm_qkv, kv_full(s), qcol + 2 * HD, kr);
@@ -445,21 +459,23 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
                              adv(k_kmaj[j & 1], (kk >> 2) * kHalf + (kk & 3) * 32), idesc_s, kk > 0 ? 1u : 0u);
         ptx::mma_commit_w(s_full(t));
       };
-      ptx::mbar_wait(q_full, 0);
-      need_kv(0);
+      if (nkv > 0) {
+        ptx::mbar_wait(q_full, 0);
+        need_kv(0);
+      }
       for (int t = 0; t < 2; ++t)
-        if (n[t] > 0) issue_s(t, 0);
-      for (int j = 0; j < nkv; ++j) {
+        if (nl[t] > 0) issue_s(t, 0);
+      for (int j = 0; j < nkv; ++j) {  // local steps; tile t is active for j < nl[t]
         for (int t = 0; t < 2; ++t) {
-          if (j >= n[t]) continue;
+          if (j >= nl[t]) continue;
           ptx::mbar_wait(p_full(t), j & 1);
           ptx::tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)
             ptx::mma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, adv(v_mnmaj[j & 1], kk * 2048), idesc_o,
                                (j | kk) != 0 ? 1u : 0u);
-          if (j + 1 == n[t]) ptx::mma_commit_w(o_done(t));  // one phase: the final O (nobody waits on the others)
-          if (j + 1 < n[t]) {
+          if (j + 1 == nl[t]) ptx::mma_commit_w(o_done(t));  // one phase: the final O (nobody waits on the others)
+          if (j + 1 < nl[t]) {
             need_kv(j + 1);
             issue_s(t, j + 1);
           }
@@ -470,7 +486,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
   } else {
     // ------------------------------------------------ softmax of tile t, row r
     const int t = (warp - 2) / 4;
-    const int nt = t ? n[1] : n[0], qbt = t ? qblk[1] : qblk[0];
+    const int nt = t ? nl[1] : nl[0], qbt = t ? qblk[1] : qblk[0];
     const int q4 = warp % 4;  // TMEM lane quarter this warp may access
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
@@ -483,7 +499,7 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
 #pragma unroll
       for (int c = 0; c < BKV / 32; ++c) ptx::tmem_ld_32x32b_x32(tS + c * 32, u[c]);
       ptx::tmem_wait_ld();
-      if (p.causal && j == qbt) {  // diagonal block: keys after the query row are masked
+      if (p.causal && j0 + j == qbt) {  // diagonal block: keys after the query row are masked
 #pragma unroll
         for (int c = 0; c < BKV; ++c)
           if (c > r) u[c / 32][c % 32] = __float_as_uint(-INFINITY);
@@ -544,11 +560,36 @@ __global__ void __launch_bounds__(320, 1) attn_fwd2_kernel(const __grid_constant
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full(t));
     }
-    if (nt > 0) {
+    const int qrow = row0 + qbt * BQ + r;
+    if (p.kv_split > 1 && (t ? n[1] : n[0]) > 0) {
+      // split-KV: this CTA's share, unnormalised (O relative to m_run, like l)
+      float* op = p.opart + (static_cast<int64_t>(split) * p.T + qrow) * (p.heads * HD) + head * HD;
+      float* ml = p.mlpart + ((static_cast<int64_t>(split) * p.T + qrow) * p.heads + head) * 2;
+      if (nt > 0) {
+        ptx::mbar_wait(o_done(t), 0);
+        ptx::tc_fence_after();
+      }
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t u[32];
+        if (nt > 0) {
+          ptx::tmem_ld_32x32b_x32(tO + c * 32, u);
+          ptx::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = 0u;
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          reinterpret_cast<float4*>(op + c * 32)[v] = make_float4(__uint_as_float(u[4 * v]), __uint_as_float(u[4 * v + 1]),
+                                                                 __uint_as_float(u[4 * v + 2]), __uint_as_float(u[4 * v + 3]));
+      }
+      ml[0] = nt > 0 ? m_run : -INFINITY;
+      ml[1] = nt > 0 ? l : 0.f;
+    } else if (nt > 0) {
       ptx::mbar_wait(o_done(t), 0);
       ptx::tc_fence_after();
       const float inv = 1.f / l;
-      const int qrow = row0 + qbt * BQ + r;
       __nv_bfloat16* orow = p.ctx + static_cast<int64_t>(qrow) * p.ld_ctx + head * HD;
 #pragma unroll
       for (int c = 0; c < HD / 32; ++c) {
@@ -1439,8 +1480,55 @@ const char* attn_check(int64_t T, int64_t seq, int heads, int head_dim, int64_t 
   return nullptr;
 }
 
+// Split-KV combine: one warp per (query row, head), 4 columns per lane.
+__global__ void attn_fwd_combine_kernel(FwdParams p) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= static_cast<int64_t>(p.T) * p.heads) return;
+  const int64_t row = w / p.heads;
+  const int head = static_cast<int>(w % p.heads);
+  float mx = -INFINITY;
+  for (int s = 0; s < p.kv_split; ++s) mx = fmaxf(mx, p.mlpart[((s * static_cast<int64_t>(p.T) + row) * p.heads + head) * 2]);
+  float L = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int s = 0; s < p.kv_split; ++s) {
+    const float* ml = p.mlpart + ((s * static_cast<int64_t>(p.T) + row) * p.heads + head) * 2;
+    if (ml[1] == 0.f) continue;  // empty share
+    const float f = ex2(ml[0] - mx);
+    L += f * ml[1];
+    const float4 v = reinterpret_cast<const float4*>(p.opart + (s * static_cast<int64_t>(p.T) + row) * (p.heads * HD) +
+                                                     head * HD)[lane];
+    o[0] += f * v.x;
+    o[1] += f * v.y;
+    o[2] += f * v.z;
+    o[3] += f * v.w;
+  }
+  const float inv = 1.f / L;
+  uint2 pk;
+  pk.x = pack_bf16(o[0] * inv, o[1] * inv);
+  pk.y = pack_bf16(o[2] * inv, o[3] * inv);
+  *reinterpret_cast<uint2*>(p.ctx + row * p.ld_ctx + head * HD + 4 * lane) = pk;
+  if (lane == 0) p.lse[static_cast<int64_t>(head) * p.T + row] = (mx + log2f(L)) * kLn2;
+}
+
+// KV splits of the forward v2 on this shape: enough CTAs for one wave when
+// the (sequence, head, query-tile pair) grid is smaller than the GPU (chunked
+// layers at N > 1: e.g. 40 CTAs), at most 4 and at most the KV blocks.
+int attn_fwd_splits(int64_t T, int64_t seq, int heads) {
+  const int64_t grid = ((seq / BQ + 1) / 2) * heads * (T / seq);
+  if (grid <= 0 || grid >= num_sms()) return 1;
+  int s = static_cast<int>((num_sms() + grid - 1) / grid);
+  s = min(s, 4);
+  s = min(s, static_cast<int>(seq / BKV));
+  return s < 1 ? 1 : s;
+}
+
+size_t attn_fwd_split_bytes(int64_t T, int64_t seq, int heads) {
+  const int s = attn_fwd_splits(T, seq, heads);
+  return s > 1 ? static_cast<size_t>(s) * T * heads * (HD + 2) * 4 : 0;
+}
+
 cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int heads, int causal, void* ctx,
-                            int64_t ld_ctx, float* lse, cudaStream_t st) {
+                            int64_t ld_ctx, float* lse, cudaStream_t st, void* ws, size_t ws_bytes) {
   alignas(64) CUtensorMap tm;
   if (!tmap_bf16_2d(&tm, qkv, T, 3 * heads * HD, ld_qkv, 128, 64)) return cudaErrorInvalidValue;
   // ATP_ATTN_FWD = 1 / 2 / 3: forward kernel version (default 2; v3, two
@@ -1495,7 +1583,22 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
   if (v1) {
     attn_fwd_kernel<<<(seq / BQ) * heads * (T / seq), 256, kFwdSmem, st>>>(tm, p);
   } else if (fwd_ver == 2) {
-    attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwdSmem, st>>>(tm, p);
+    // split-KV when the grid is smaller than the GPU and the caller gave the workspace
+    static const bool split_on = [] {
+      const char* e = getenv("ATP_ATTN_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    const int S = split_on ? attn_fwd_splits(T, seq, heads) : 1;
+    if (S > 1 && ws != nullptr && ws_bytes >= attn_fwd_split_bytes(T, seq, heads)) {
+      p.kv_split = S;
+      p.opart = static_cast<float*>(ws);
+      p.mlpart = p.opart + static_cast<size_t>(S) * T * heads * HD;
+      attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq) * S, 320, kFwdSmem, st>>>(tm, p);
+      const int64_t warps = static_cast<int64_t>(T) * heads;
+      attn_fwd_combine_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(p);
+    } else {
+      attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwdSmem, st>>>(tm, p);
+    }
   } else {
     attn_fwd3_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), kFwd3Threads, kFwd3Smem, st>>>(tm, p);
   }

@@ -286,7 +286,7 @@ cudaError_t ew_launch_t(const EwDesc& e, cudaStream_t st) {
 cudaError_t ew_launch(const EwDesc& e, cudaStream_t st) {
   if (e.kind == EW_ATTN_FWD)
     return attn_fwd_launch(e.a, e.lda, static_cast<int>(e.rows), e.seq, e.heads, e.causal, e.out, e.ldo,
-                           static_cast<float*>(e.out2), st);
+                           static_cast<float*>(e.out2), st, e.ws, static_cast<size_t>(e.n_total));
   if (e.kind == EW_ATTN_BWD)
     return attn_bwd_launch(e.a, e.lda, e.b, e.ldb, static_cast<const float*>(e.out2), e.res, e.ldres,
                            static_cast<int>(e.rows), e.seq, e.heads, e.causal, e.out, e.ldo, e.ws, st);

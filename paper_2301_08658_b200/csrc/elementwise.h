@@ -23,6 +23,7 @@ enum EwKind : int {
   EW_UNPACK = 12,        // out [rows, cols] (pitch ldo) = a [p][rows][cols/p]
   EW_ATTN_FWD = 13,      // out (ctx, ldo) , out2 (lse) = attention(a = qkv, lda)
   EW_ATTN_BWD = 14,      // out (dqkv, ldo) from a = qkv, b = ctx, res = dctx, out2 = lse, ws = workspace
+                         // (EW_ATTN_FWD: optional split-KV scratch ws of n_total bytes)
   // d2 == 1 (the whole row is local, no statistics all-reduce): one kernel per pass
   EW_LN_FWD = 15,        // EW_LN_STATS + EW_LN_APPLY (out2 unused)
   EW_LN_BWD = 16,        // EW_LN_BWD_STATS + EW_LN_BWD_APPLY (out2 unused)

@@ -641,6 +641,7 @@ namespace {
 // Per-rank workspace of the full layer (bytes, 256-aligned pieces).
 struct GptWs {
   size_t part, packed, ctxb, dctxp, dctxl, dqkvl, dqkvb, dqkv, dh, dbn, dy1, da, st1, st2, bs1, bs2, lnws, attn, total;
+  size_t attn_bytes = 0;
   GptWs(int d1, int d2, int64_t T, int64_t h, int64_t F, int64_t heads, int64_t seq, int chunks) {
     (void)seq;
     const int64_t hc = h / d2, h1 = h / d1, q1 = 3 * h / d1, F1 = F / d1, ql = q1 / d2, cl = h1 / d2;
@@ -668,7 +669,11 @@ struct GptWs {
     bs1 = take(T * 8);
     bs2 = take(T * 8);
     lnws = take(ln_param_workspace_bytes(hc));
-    attn = take(attn_workspace_bytes(Mc, static_cast<int>(hl)));
+    // backward scratch, also the forward's split-KV scratch on small grids
+    attn = take(std::max(attn_workspace_bytes(Mc, static_cast<int>(hl)),
+                         attn_fwd_split_bytes(Mc, seq, static_cast<int>(hl))));
+    attn_bytes = std::max(attn_workspace_bytes(Mc, static_cast<int>(hl)),
+                          attn_fwd_split_bytes(Mc, seq, static_cast<int>(hl)));
     total = off;
   }
 };
@@ -849,6 +854,8 @@ int build_gpt_layer(const RankView& rv, const atp_gpt_args& a, int64_t T, int64_
     at.lda = ql;
     at.out = R(ctx_loc, k, cl);
     at.ldo = cl;
+    at.ws = W(L.attn);  // split-KV scratch (the chunks' forwards run in stream order, before any backward)
+    at.n_total = static_cast<int64_t>(L.attn_bytes);
     ew_k(k, at);
     if (!c2) {
       EwDesc un = E::ewd(EW_UNPACK, R(a.ctx, k, h1), R(W(L.ctxb), k, h1), Mc, h1);
