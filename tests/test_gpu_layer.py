@@ -497,3 +497,42 @@ def test_layer_stack(d1, d2, chunks):
         _, fw, bw, _ = ref[l]
         compare(stack[l], fw, bw, d1, d2)
         check_replicas(stack[l], d1, d2)
+
+
+@pytest.mark.parametrize("d1,d2,fused,gated", [(2, 2, True, False), (4, 2, True, True), (2, 2, False, True)])
+def test_layer_stack_fused_and_gated(d1, d2, fused, gated):
+    """The layer stack with the fused GEMM -> RS -> AG stages (receive regions
+    alternate across all 8 x L stages of the pipeline) and / or chunk-gated
+    GEMMs (layer l+1's first GEMM gated on layer l's last stage), against the
+    oracle run layer by layer; replicas bit-identical."""
+    import torch
+    import datagen
+    import paper_2301_08658_b200 as atp
+    from oracle import layer as olayer
+
+    L, T, h, F, heads, chunks, seed = 2, 1024, 256, 1024, 4, 4, 67
+    gs = [{k: v.astype(np.float64) for k, v in datagen.layer_globals(T, h, F, seed=seed + l).items()}
+          for l in range(L)]
+    xs = [gs[0]["x"], olayer.dense_forward(dict(gs[0], x=gs[0]["x"]), heads)["z"]]
+    g1 = dict(gs[1], x=xs[1])
+    dzs = [olayer.dense_backward(g1, olayer.dense_forward(g1, heads), gs[1]["dz"], heads)["dx"], gs[1]["dz"]]
+    ref = [olayer.run_layer(dict(gs[l], x=xs[l], dz=dzs[l]), d1, d2, heads, chunks) for l in range(L)]
+    mesh = atp.Mesh.virtual(d1, d2)
+    try:
+        if gated:
+            mesh.set_gemm_ctas(16)
+            mesh.set_gating(True)
+        if fused:
+            mesh.enable_fused_ar(T * F * 2)
+        per_rank = [atp.alloc_layer_stack(d1, d2, r, T, h, F, "cuda", seed, L) for r in range(d1 * d2)]
+        stack = [[per_rank[r][l] for r in range(d1 * d2)] for l in range(L)]
+        call = atp.LayerStackCall(mesh, stack, T, h, F, heads, chunks)
+        for _ in range(2):
+            call()
+        torch.cuda.synchronize()
+    finally:
+        mesh.destroy()
+    for l in range(L):
+        _, fw, bw, _ = ref[l]
+        compare(stack[l], fw, bw, d1, d2)
+        check_replicas(stack[l], d1, d2)
