@@ -866,6 +866,318 @@ __global__ void __launch_bounds__(kFwd3Threads, 1) attn_fwd3_kernel(const __grid
   }
 }
 
+// ---------------------------------------------------------------- forward v4
+// v2 made persistent with Blackwell cluster launch control (CLC): the grid
+// is still one CTA per query-tile pair (heaviest first), but a running CTA
+// takes over not-yet-launched CTAs (`clusterlaunchcontrol.try_cancel`)
+// instead of exiting, so barrier init, TMEM allocation and the tensor-map
+// prefetch happen once per SM, the next item's Q / first K,V tiles load while
+// the current item's last steps run, and its first S MMA overlaps the O
+// drain.  The producer requests the successor with each item's last K/V
+// load (late enough that the CTAs finishing first take the next items, as
+// the hardware scheduler would); every role reads the 16-byte response from a two-slot ring
+// (clc_full / clc_empty).  Barrier phases run across items (per-tile step,
+// Q and O counters; one K/V ring counter).  kv_split == 1 only.
+struct FwdItem {
+  int qblk[2], nl[2], nkv, head, row0;
+};
+
+__device__ __forceinline__ FwdItem fwd_item(const FwdParams& p, int b) {
+  FwdItem I;
+  const int nq = p.seq / BQ, nm = (nq + 1) / 2, nseq = p.T / p.seq;
+  int m, rest;
+  cta_order(p.grouped, p.heads * nseq, nm, m, rest, b);
+  if (p.causal) m = nm - 1 - m;
+  I.head = rest % p.heads;
+  I.row0 = (rest / p.heads) * p.seq;
+  for (int t = 0; t < 2; ++t) {
+    I.qblk[t] = 2 * m + t;
+    I.nl[t] = I.qblk[t] < nq ? (p.causal ? I.qblk[t] + 1 : nq) : 0;
+  }
+  I.nkv = I.nl[0] > I.nl[1] ? I.nl[0] : I.nl[1];
+  return I;
+}
+
+__device__ __forceinline__ void clc_try_cancel(uint32_t resp, uint32_t bar) {
+  asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+                   resp),
+               "r"(bar)
+               : "memory");
+}
+// The stolen CTA's blockIdx.x, or -1 when no CTA was left to take.
+__device__ __forceinline__ int clc_next(uint32_t resp) {
+  uint32_t ok, x;
+  asm volatile(
+      "{\n\t.reg .b128 r;\n\t.reg .pred p;\n\t"
+      "ld.shared.b128 r, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r;\n\t}"
+      : "=r"(ok), "=r"(x)
+      : "r"(resp)
+      : "memory");
+  return ok ? static_cast<int>(x) : -1;
+}
+
+constexpr int kFwd4Smem = 6 * kTile + 256 + 1024;
+
+__global__ void __launch_bounds__(320, 1) attn_fwd4_kernel(const __grid_constant__ CUtensorMap tm_qkv, FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  auto sQ = [&](int t) { return base + t * kTile; };
+  auto sK = [&](int s) { return base + 2 * kTile + s * 2 * kTile; };
+  auto sV = [&](int s) { return base + 3 * kTile + s * 2 * kTile; };
+  const uint32_t bars = base + 6 * kTile;
+  auto kv_full = [&](int s) { return bars + 8 * s; };
+  auto kv_empty = [&](int s) { return bars + 16 + 8 * s; };
+  auto s_full = [&](int t) { return bars + 32 + 8 * t; };
+  auto p_full = [&](int t) { return bars + 48 + 8 * t; };
+  auto o_done = [&](int t) { return bars + 64 + 8 * t; };
+  auto q_full = [&](int t) { return bars + 80 + 8 * t; };
+  auto q_empty = [&](int t) { return bars + 96 + 8 * t; };
+  auto clc_full = [&](int s) { return bars + 112 + 8 * s; };
+  auto clc_empty = [&](int s) { return bars + 128 + 8 * s; };
+  auto clc_resp = [&](int s) { return bars + 160 + 16 * s; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 144 - raw));
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(kv_full(s), 1);
+      ptx::mbar_init(kv_empty(s), 1);
+      ptx::mbar_init(s_full(s), 1);
+      ptx::mbar_init(p_full(s), 128);
+      ptx::mbar_init(o_done(s), 1);
+      ptx::mbar_init(q_full(s), 1);
+      ptx::mbar_init(q_empty(s), 1);
+      ptx::mbar_init(clc_full(s), 1);
+      ptx::mbar_init(clc_empty(s), 9);  // the MMA warp + 8 softmax warps
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tm_qkv);
+      int qc[2] = {0, 0}, g = 0;
+      for (int b = static_cast<int>(blockIdx.x), it = 0; b >= 0; ++it) {
+        const FwdItem I = fwd_item(p, b);
+        const int qcol = I.head * 3 * HD;
+        for (int t = 0; t < 2; ++t) {
+          if (I.nl[t] == 0) continue;
+          ptx::mbar_wait(q_empty(t), (qc[t] & 1) ^ 1);
+          ++qc[t];
+          ptx::mbar_arrive_expect_tx(q_full(t), kTile);
+          const int qr = I.row0 + I.qblk[t] * BQ;
+          ptx::tma_load_2d(sQ(t), &tm_qkv, q_full(t), qcol, qr);
+          ptx::tma_load_2d(sQ(t) + kHalf, &tm_qkv, q_full(t), qcol + 64, qr);
+        }
+        for (int j = 0; j < I.nkv; ++j, ++g) {
+          const int s = g & 1;
+          ptx::mbar_wait(kv_empty(s), ((g >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(kv_full(s), 2 * kTile);
+          const int kr = I.row0 + j * BKV;
+          ptx::tma_load_2d(sK(s), &tm_qkv, kv_full(s), qcol + HD, kr);
+          ptx::tma_load_2d(sK(s) + kHalf, &tm_qkv, kv_full(s), qcol + HD + 64, kr);
+          ptx::tma_load_2d(sV(s), &tm_qkv, kv_full(s), qcol + 2 * HD, kr);
+          ptx::tma_load_2d(sV(s) + kHalf, &tm_qkv, kv_full(s), qcol + 2 * HD + 64, kr);
+          if (j + 1 == I.nkv) {
+            // ask for the successor item with the last K/V load (the MMA is ~2 steps
+            // behind): claiming earlier would bind work to a CTA before it is known to
+            // finish early (at s = 8192 a claim at the first load made the heaviest
+            // items' CTAs take a second item: 0.12 -> 0.17 ms).  The slot's readers
+            // are done with item it - 2.
+            const int cs = it & 1;
+            ptx::mbar_wait(clc_empty(cs), ((it >> 1) & 1) ^ 1);
+            ptx::fence_proxy_async();
+            ptx::mbar_arrive_expect_tx(clc_full(cs), 16);
+            clc_try_cancel(clc_resp(cs), clc_full(cs));
+          }
+        }
+        ptx::mbar_wait(clc_full(it & 1), (it >> 1) & 1);
+        b = clc_next(clc_resp(it & 1));
+      }
+    }
+  } else if (warp == 1) {
+    // the whole warp runs the issue loop; each tcgen05 op is issued by one elected lane
+    constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
+    constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(128, 128, 0, 1);
+    auto adv = [](uint64_t d, uint32_t bytes) { return d + (bytes >> 4); };
+    const uint64_t q_kmaj[2] = {ptx::smem_desc_sw128(sQ(0), 16, 1024), ptx::smem_desc_sw128(sQ(1), 16, 1024)};
+    const uint64_t k_kmaj[2] = {ptx::smem_desc_sw128(sK(0), 16, 1024), ptx::smem_desc_sw128(sK(1), 16, 1024)};
+    const uint64_t v_mnmaj[2] = {ptx::smem_desc_sw128(sV(0), kHalf, 1024), ptx::smem_desc_sw128(sV(1), kHalf, 1024)};
+    int qc[2] = {0, 0}, sc[2] = {0, 0}, g0 = 0, kv_seen = -1;
+    auto need_kv = [&](int gj) {  // global K/V block counter
+      if (gj > kv_seen) {
+        ptx::mbar_wait(kv_full(gj & 1), (gj >> 1) & 1);
+        ptx::tc_fence_after();
+        kv_seen = gj;
+      }
+    };
+    auto issue_s = [&](int t, int gj) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ptx::mma_bf16_ss_w(tmem + 256 * t, adv(q_kmaj[t], (kk >> 2) * kHalf + (kk & 3) * 32),
+                           adv(k_kmaj[gj & 1], (kk >> 2) * kHalf + (kk & 3) * 32), idesc_s, kk > 0 ? 1u : 0u);
+      ptx::mma_commit_w(s_full(t));
+    };
+    for (int b = static_cast<int>(blockIdx.x), it = 0; b >= 0; ++it) {
+      const FwdItem I = fwd_item(p, b);
+      need_kv(g0);
+      for (int t = 0; t < 2; ++t) {
+        if (I.nl[t] == 0) continue;
+        ptx::mbar_wait(q_full(t), qc[t] & 1);
+        ++qc[t];
+        ptx::tc_fence_after();
+        issue_s(t, g0);
+        if (I.nl[t] == 1) ptx::mma_commit_w(q_empty(t));
+      }
+      for (int j = 0; j < I.nkv; ++j) {  // tile t is active for j < nl[t]
+        for (int t = 0; t < 2; ++t) {
+          if (j >= I.nl[t]) continue;
+          ptx::mbar_wait(p_full(t), sc[t] & 1);
+          ++sc[t];
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            ptx::mma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, adv(v_mnmaj[(g0 + j) & 1], kk * 2048),
+                               idesc_o, (j | kk) != 0 ? 1u : 0u);
+          if (j + 1 == I.nl[t]) ptx::mma_commit_w(o_done(t));
+          if (j + 1 < I.nl[t]) {
+            need_kv(g0 + j + 1);
+            issue_s(t, g0 + j + 1);
+            if (j + 2 == I.nl[t]) ptx::mma_commit_w(q_empty(t));  // last S of this tile: Q may be replaced
+          }
+        }
+        ptx::mma_commit_w(kv_empty((g0 + j) & 1));
+      }
+      g0 += I.nkv;
+      ptx::mbar_wait(clc_full(it & 1), (it >> 1) & 1);
+      b = clc_next(clc_resp(it & 1));
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(clc_empty(it & 1));
+    }
+  } else {
+    // ------------------------------------------------ softmax of tile t, row r (as v2)
+    const int t = (warp - 2) / 4;
+    const int q4 = warp % 4;  // TMEM lane quarter this warp may access
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t tS = tmem + lane_off + 256 * t, tO = tS + 128;
+    int sc = 0, oc = 0;
+    for (int b = static_cast<int>(blockIdx.x), it = 0; b >= 0; ++it) {
+      const FwdItem I = fwd_item(p, b);
+      const int nt = I.nl[t], qbt = I.qblk[t];
+      float m_run = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt; ++j, ++sc) {
+        ptx::mbar_wait(s_full(t), sc & 1);
+        ptx::tc_fence_after();
+        uint32_t u[BKV / 32][32];
+#pragma unroll
+        for (int c = 0; c < BKV / 32; ++c) ptx::tmem_ld_32x32b_x32(tS + c * 32, u[c]);
+        ptx::tmem_wait_ld();
+        if (p.causal && j == qbt) {
+#pragma unroll
+          for (int c = 0; c < BKV; ++c)
+            if (c > r) u[c / 32][c % 32] = __float_as_uint(-INFINITY);
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(u[i / 32][i % 32]);
+#pragma unroll
+        for (int c = 8; c < BKV; c += 2)
+          mx[(c / 2) % 8] = fmax3(mx[(c / 2) % 8], __uint_as_float(u[c / 32][c % 32]), __uint_as_float(u[c / 32][c % 32 + 1]));
+        float mb = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
+        mb *= p.scale_log2;
+        const bool rescale = __any_sync(0xffffffffu, mb > m_run + 8.f);
+        float f = 1.f;
+        if (rescale) {
+          const float m_new = fmaxf(m_run, mb);
+          f = ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2), nm2 = f2pack(-m_run, -m_run);
+        uint64_t rsv[2] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < BKV / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x0, x1;
+            f2unpack(ffma2(f2pack(__uint_as_float(u[c][2 * i]), __uint_as_float(u[c][2 * i + 1])), sc2, nm2), x0, x1);
+            const float e0 = ex2(x0), e1 = ex2(x1);
+            rsv[i % 2] = fadd2(rsv[i % 2], f2pack(e0, e1));
+            pk[i] = pack_bf16(e0, e1);
+          }
+          ptx::tmem_st_32x32b_x16(tS + c * 16, pk);
+        }
+        float ra, rb, rc, rd;
+        f2unpack(rsv[0], ra, rb);
+        f2unpack(rsv[1], rc, rd);
+        l = l * f + ((ra + rb) + (rc + rd));
+        if (rescale && j > 0) {
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld_32x32b_x32(tO + c * 32, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+            ptx::tmem_st_32x32b_x32(tO + c * 32, o);
+          }
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(p_full(t));
+      }
+      if (nt > 0) {
+        ptx::mbar_wait(o_done(t), oc & 1);
+        ++oc;
+        ptx::tc_fence_after();
+        const int qrow = I.row0 + qbt * BQ + r;
+        const float inv = 1.f / l;
+        __nv_bfloat16* orow = p.ctx + static_cast<int64_t>(qrow) * p.ld_ctx + I.head * HD;
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t u[32];
+          ptx::tmem_ld_32x32b_x32(tO + c * 32, u);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+            w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+            w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+            w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + c * 32 + 8 * v) = w;
+          }
+        }
+        p.lse[static_cast<int64_t>(I.head) * p.T + qrow] = (m_run + log2f(l)) * kLn2;
+        ptx::tc_fence_before();  // the O reads complete before the next item's PV (ordered by p_full)
+      }
+      ptx::mbar_wait(clc_full(it & 1), (it >> 1) & 1);
+      b = clc_next(clc_resp(it & 1));
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(clc_empty(it & 1));
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 // ================================================================ backward
 // dV = P^T dO, dP = dO V^T, dS = P * (dP - D) with D = rowsum(dO * O),
 // dQ = dS K / sqrt(d), dK = dS^T Q / sqrt(d)   (FlashAttention-2 order).
@@ -1416,6 +1728,332 @@ __global__ void __launch_bounds__(448, 1) attn_bwd2_kernel(const __grid_constant
   }
 }
 
+// ---------------------------------------------------------------- backward v3
+// v2 made persistent with cluster launch control (as forward v4): the grid is
+// one CTA per (key block, head, sequence), but a running CTA takes over
+// not-yet-launched CTAs instead of exiting.  Per SM, barrier init and TMEM
+// allocation happen once; the next item's K / V load as soon as the current
+// item's last MMA has read them, and its first S^T / dP^T products run while
+// the softmax warps drain the current item's dK / dV (the first dV / dK MMA of
+// an item waits for that drain: acc_free).  Every ring (Q / dO slots, S^T /
+// dP^T / dS^T buffers) runs on one block counter across items.
+__device__ __forceinline__ void bwd_item(const BwdParams& p, int b, int& jb, int& head, int& row0, int& i0, int& n) {
+  const int nseq = p.T / p.seq, per = p.heads * nseq, nkb = p.seq / BKV;
+  int rest;
+  cta_order(p.grouped, per, nkb, jb, rest, b);
+  head = rest % p.heads;
+  row0 = (rest / p.heads) * p.seq;
+  const int nqb = p.seq / BQ2;
+  i0 = p.causal ? 2 * jb : 0;
+  n = nqb - i0;
+}
+
+__global__ void __launch_bounds__(448, 1) attn_bwd3_kernel(const __grid_constant__ CUtensorMap tm_kv,
+                                                           const __grid_constant__ CUtensorMap tm_q,
+                                                           const __grid_constant__ CUtensorMap tm_do,
+                                                           const __grid_constant__ CUtensorMap tm_dq, BwdParams p) {
+  using L = Bwd2Smem;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const float* lds = reinterpret_cast<const float*>(smem_raw + (base - raw) + L::LD);  // lse[3][64], D[3][64]
+  const uint32_t bars = base + L::Bars;
+  const uint32_t kv_full = bars;
+  auto q_full = [&](int q) { return bars + 8 + 8 * q; };    // [3]
+  auto q_empty = [&](int q) { return bars + 32 + 8 * q; };  // [3]
+  auto s_full = [&](int s) { return bars + 56 + 8 * s; };
+  auto ds_full = [&](int s) { return bars + 72 + 8 * s; };
+  auto p_free = [&](int s) { return bars + 88 + 8 * s; };
+  auto dq_full = [&](int s) { return bars + 104 + 8 * s; };
+  auto s_free = [&](int s) { return bars + 120 + 8 * s; };
+  const uint32_t done = bars + 136;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars + 144 - raw));
+  const uint32_t kv_empty = bars + 152, acc_free = bars + 160;
+  auto clc_full = [&](int s) { return bars + 168 + 8 * s; };
+  auto clc_empty = [&](int s) { return bars + 184 + 8 * s; };
+  auto clc_resp = [&](int s) { return bars + 208 + 16 * s; };
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(kv_full, 1);
+    ptx::mbar_init(kv_empty, 1);
+    ptx::mbar_init(acc_free, 256);
+    for (int q = 0; q < kQSlots; ++q) {
+      ptx::mbar_init(q_full(q), 1);
+      ptx::mbar_init(q_empty(q), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(s_full(s), 1);
+      ptx::mbar_init(ds_full(s), 256);
+      ptx::mbar_init(p_free(s), 1);
+      ptx::mbar_init(dq_full(s), 1);
+      ptx::mbar_init(s_free(s), 128);
+      ptx::mbar_init(clc_full(s), 1);
+      ptx::mbar_init(clc_empty(s), 13);  // MMA warp, 8 softmax warps, 4 dQ warps
+    }
+    ptx::mbar_init(done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  auto tS = [&](int s) { return tmem + 64u * s; };
+  auto tdP = [&](int s) { return tmem + 128u + 64u * s; };
+  const uint32_t tdV = tmem + 256, tdK = tmem + 384;
+  // successor item (every consumer role; the producer requested it)
+  auto next_item = [&](int it) {
+    ptx::mbar_wait(clc_full(it & 1), (it >> 1) & 1);
+    const int b = clc_next(clc_resp(it & 1));
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(clc_empty(it & 1));
+    return b;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tm_kv);
+      ptx::prefetch_tmap(&tm_q);
+      ptx::prefetch_tmap(&tm_do);
+      int g = 0;
+      for (int b = static_cast<int>(blockIdx.x), it = 0; b >= 0; ++it) {
+        int jb, head, row0, i0, n;
+        bwd_item(p, b, jb, head, row0, i0, n);
+        const int qcol = head * 3 * HD, kvrow = row0 + jb * BKV;
+        ptx::mbar_wait(kv_empty, (it & 1) ^ 1);  // the previous item's MMAs are done with K / V
+        ptx::mbar_arrive_expect_tx(kv_full, 2 * kTile);
+        ptx::tma_load_2d(base + L::K, &tm_kv, kv_full, qcol + HD, kvrow);
+        ptx::tma_load_2d(base + L::K + kHalf, &tm_kv, kv_full, qcol + HD + 64, kvrow);
+        ptx::tma_load_2d(base + L::V, &tm_kv, kv_full, qcol + 2 * HD, kvrow);
+        ptx::tma_load_2d(base + L::V + kHalf, &tm_kv, kv_full, qcol + 2 * HD + 64, kvrow);
+        for (int t = 0; t < n; ++t, ++g) {
+          const int q = g % kQSlots;
+          const int qr = row0 + (i0 + t) * BQ2;
+          ptx::mbar_wait(q_empty(q), ((g / kQSlots) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(q_full(q), 2 * kQ2 + 2 * BQ2 * 4);
+          const uint32_t sq_ = base + L::Q + q * kQ2, sdo = base + L::dO + q * kQ2;
+          ptx::tma_load_2d(sq_, &tm_q, q_full(q), qcol, qr);
+          ptx::tma_load_2d(sq_ + kBox64, &tm_q, q_full(q), qcol + 64, qr);
+          ptx::tma_load_2d(sdo, &tm_do, q_full(q), head * HD, qr);
+          ptx::tma_load_2d(sdo + kBox64, &tm_do, q_full(q), head * HD + 64, qr);
+          const int64_t lo = static_cast<int64_t>(head) * p.T + qr;
+          ptx::bulk_load_1d(base + L::LD + q * BQ2 * 4, p.lse + lo, BQ2 * 4, q_full(q));
+          ptx::bulk_load_1d(base + L::LD + (kQSlots + q) * BQ2 * 4, p.D + lo, BQ2 * 4, q_full(q));
+          if (t + 1 == n) {  // ask for the successor with the last Q / dO load (as forward v4)
+            const int cs = it & 1;
+            ptx::mbar_wait(clc_empty(cs), ((it >> 1) & 1) ^ 1);
+            ptx::fence_proxy_async();
+            ptx::mbar_arrive_expect_tx(clc_full(cs), 16);
+            clc_try_cancel(clc_resp(cs), clc_full(cs));
+          }
+        }
+        ptx::mbar_wait(clc_full(it & 1), (it >> 1) & 1);
+        b = clc_next(clc_resp(it & 1));
+      }
+      for (int t = g; t < g + kQSlots; ++t)  // tail: every slot released (each phase waited)
+        ptx::mbar_wait(q_empty(t % kQSlots), ((t / kQSlots) & 1) ^ 1);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_st = ptx::idesc_bf16_f32(128, BQ2, 0, 0);
+    constexpr uint32_t id_kv = ptx::idesc_bf16_f32(128, 128, 0, 1);
+    constexpr uint32_t id_dq = ptx::idesc_bf16_f32(128, BQ2, 1, 1);
+    auto adv = [](uint64_t d, uint32_t bytes) { return d + (bytes >> 4); };
+    const uint64_t k_kmaj = ptx::smem_desc_sw128(base + L::K, 16, 1024);
+    const uint64_t v_kmaj = ptx::smem_desc_sw128(base + L::V, 16, 1024);
+    const uint64_t k_mnmaj = ptx::smem_desc_sw128(base + L::K, kHalf, 1024);
+    auto issue_sdp = [&](int g) {
+      const int s = g & 1, q = g % kQSlots;
+      ptx::mbar_wait(q_full(q), (g / kQSlots) & 1);
+      if (g >= 2) ptx::mbar_wait(s_free(s), ((g - 2) >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint64_t q_kmaj = ptx::smem_desc_sw128(base + L::Q + q * kQ2, 16, 1024);
+      const uint64_t do_kmaj = ptx::smem_desc_sw128(base + L::dO + q * kQ2, 16, 1024);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ptx::mma_bf16_ss_w(tS(s), adv(k_kmaj, (kk >> 2) * kHalf + (kk & 3) * 32),
+                           adv(q_kmaj, (kk >> 2) * kBox64 + (kk & 3) * 32), id_st, kk > 0 ? 1u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ptx::mma_bf16_ss_w(tdP(s), adv(v_kmaj, (kk >> 2) * kHalf + (kk & 3) * 32),
+                           adv(do_kmaj, (kk >> 2) * kBox64 + (kk & 3) * 32), id_st, kk > 0 ? 1u : 0u);
+      ptx::mma_commit_w(s_full(s));
+    };
+    int g0 = 0;
+    for (int b = static_cast<int>(blockIdx.x), it = 0; b >= 0; ++it) {
+      int jb, head, row0, i0, n;
+      bwd_item(p, b, jb, head, row0, i0, n);
+      ptx::mbar_wait(kv_full, it & 1);
+      ptx::tc_fence_after();
+      if (n > 0) issue_sdp(g0);
+      for (int t = 0; t < n; ++t) {
+        const int g = g0 + t, s = g & 1, q = g % kQSlots;
+        if (t + 1 < n) issue_sdp(g + 1);
+        ptx::mbar_wait(ds_full(s), (g >> 1) & 1);
+        if (t == 0) ptx::mbar_wait(acc_free, (it & 1) ^ 1);  // the previous item's dK / dV drained
+        ptx::tc_fence_after();
+        const uint64_t q_mnmaj = ptx::smem_desc_sw128(base + L::Q + q * kQ2, kBox64, 1024);
+        const uint64_t do_mnmaj = ptx::smem_desc_sw128(base + L::dO + q * kQ2, kBox64, 1024);
+        const uint64_t ds_mnmaj = ptx::smem_desc_sw128(base + L::dS + s * kPS, kPS, 1024);
+#pragma unroll
+        for (int kk = 0; kk < BQ2 / 16; ++kk)
+          ptx::mma_bf16_ts_w(tdV, tS(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), adv(do_mnmaj, kk * 2048), id_kv,
+                             (t | kk) != 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BQ2 / 16; ++kk)
+          ptx::mma_bf16_ts_w(tdK, tdP(s) + (kk < 2 ? 8 * kk : 32 + 8 * (kk - 2)), adv(q_mnmaj, kk * 2048), id_kv,
+                             (t | kk) != 0 ? 1u : 0u);
+        ptx::mma_commit_w(q_empty(q));
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          ptx::mma_bf16_ss_w(tdP(s), adv(k_mnmaj, kk * 2048), adv(ds_mnmaj, kk * 2048), id_dq, kk > 0 ? 1u : 0u);
+        ptx::mma_commit_w(dq_full(s));
+        ptx::mma_commit_w(p_free(s));
+      }
+      ptx::mma_commit_w(done);      // dK / dV of this item complete
+      ptx::mma_commit_w(kv_empty);  // K / V no longer read
+      g0 += n;
+      b = next_item(it);
+    }
+    for (int t = g0; t < g0 + 2; ++t)  // tail: the last dQ^T read-outs (each phase waited)
+      if (t >= 2) ptx::mbar_wait(s_free(t & 1), ((t - 2) >> 1) & 1);
+  } else if (warp < 10) {
+    const int half = (warp - 2) / 4, q4 = warp % 4;
+    const int r = q4 * 32 + lane, c0 = 32 * half;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    int g = 0;
+    for (int b = static_cast<int>(blockIdx.x), it = 0; b >= 0; ++it) {
+      int jb, head, row0, i0, n;
+      bwd_item(p, b, jb, head, row0, i0, n);
+      const int key = jb * BKV + r;
+      for (int t = 0; t < n; ++t, ++g) {
+        const int s = g & 1, q = g % kQSlots, i = i0 + t;
+        ptx::mbar_wait(q_full(q), (g / kQSlots) & 1);
+        ptx::mbar_wait(s_full(s), (g >> 1) & 1);
+        ptx::tc_fence_after();
+        uint32_t su[32], du[32];
+        ptx::tmem_ld_32x32b_x32(tS(s) + lane_off + c0, su);
+        ptx::tmem_ld_32x32b_x32(tdP(s) + lane_off + c0, du);
+        ptx::tmem_wait_ld();
+        if (g >= 2) ptx::mbar_wait(p_free(s), ((g - 2) >> 1) & 1);
+        const float* lse_s = lds + q * BQ2;
+        const float* D_s = lds + (kQSlots + q) * BQ2;
+        const int qpos0 = i * BQ2 + c0;
+        const bool need_mask = p.causal && qpos0 < key;
+        uint32_t pk[16], dk[16];
+        const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2);
+        const uint64_t nlog2e = f2pack(-1.4426950408889634f, -1.4426950408889634f);
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          const float2 l2 = *reinterpret_cast<const float2*>(lse_s + c0 + k);
+          const float2 d2 = *reinterpret_cast<const float2*>(D_s + c0 + k);
+          float x0, x1;
+          f2unpack(ffma2(f2pack(__uint_as_float(su[k]), __uint_as_float(su[k + 1])), sc2,
+                         fmul2(f2pack(l2.x, l2.y), nlog2e)),
+                   x0, x1);
+          float pv[2] = {ex2(x0), ex2(x1)};
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (need_mask && qpos0 + k + u < key) pv[u] = 0.f;
+          const uint64_t pp = f2pack(pv[0], pv[1]);
+          float ds0, ds1;
+          f2unpack(fmul2(pp, fsub2(f2pack(__uint_as_float(du[k]), __uint_as_float(du[k + 1])), f2pack(d2.x, d2.y))),
+                   ds0, ds1);
+          pk[k / 2] = pack_bf16(pv[0], pv[1]);
+          dk[k / 2] = pack_bf16(ds0, ds1);
+        }
+        ptx::tmem_st_32x32b_x16(tS(s) + lane_off + c0, pk);
+        ptx::tmem_st_32x32b_x16(tdP(s) + lane_off + c0, dk);
+        const uint32_t sds = base + L::dS + s * kPS;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c16 = c0 / 8 + v;
+          const uint32_t off = static_cast<uint32_t>(r * 128 + ((c16 ^ (r & 7)) << 4));
+          st_shared_v4(sds + off, dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);
+        }
+        ptx::tmem_wait_st();
+        ptx::fence_proxy_async();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(ds_full(s));
+      }
+      // dK (scaled), dV of this item -> dqkv rows of its key block
+      ptx::mbar_wait(done, it & 1);
+      ptx::tc_fence_after();
+      const int cc = 64 * half, kvrow = row0 + jb * BKV;
+      __nv_bfloat16* drow = p.dqkv + static_cast<int64_t>(kvrow + r) * p.ld_dqkv + head * 3 * HD;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        const float f = which == 0 ? p.scale : 1.f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t u[32];
+          ptx::tmem_ld_32x32b_x32((which == 0 ? tdK : tdV) + lane_off + cc + 32 * c, u);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * f, __uint_as_float(u[8 * v + 1]) * f);
+            w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * f, __uint_as_float(u[8 * v + 3]) * f);
+            w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * f, __uint_as_float(u[8 * v + 5]) * f);
+            w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * f, __uint_as_float(u[8 * v + 7]) * f);
+            *reinterpret_cast<uint4*>(drow + (which == 0 ? HD : 2 * HD) + cc + 32 * c + 8 * v) = w;
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(acc_free);
+      b = next_item(it);
+    }
+    for (int t = g; t < g + 2; ++t)  // tail: the last dS^T buffers released (each phase waited)
+      if (t >= 2) ptx::mbar_wait(p_free(t & 1), ((t - 2) >> 1) & 1);
+  } else {
+    const int q4 = warp % 4;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t box = base + L::dQ + static_cast<uint32_t>(q4) * kDqBox;
+    int g = 0;
+    for (int b = static_cast<int>(blockIdx.x), it = 0; b >= 0; ++it) {
+      int jb, head, row0, i0, n;
+      bwd_item(p, b, jb, head, row0, i0, n);
+      for (int t = 0; t < n; ++t, ++g) {
+        const int s = g & 1, i = i0 + t;
+        ptx::mbar_wait(dq_full(s), (g >> 1) & 1);
+        ptx::tc_fence_after();
+        uint32_t qa[32], qb[32];
+        ptx::tmem_ld_32x32b_x32(tdP(s) + lane_off, qa);
+        ptx::tmem_ld_32x32b_x32(tdP(s) + lane_off + 32, qb);
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(s_free(s));
+        if (lane == 0) ptx::bulk_wait_read0();
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          const uint32_t addr = box + q * 128 + ((((lane >> 2) ^ (q & 7)) & 7) << 4) + (lane & 3) * 4;
+          const uint32_t val = q < 32 ? qa[q] : qb[q - 32];
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(val) : "memory");
+        }
+        ptx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_reduce_add_2d(&tm_dq, box, head * HD + 32 * q4, row0 + i * BQ2);
+          ptx::bulk_commit();
+        }
+      }
+      b = next_item(it);
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 // D[h][t] = sum_c dO[t, h*128 + c] * O[t, h*128 + c] (fp32); zero the dQ accumulator.
 // One warp per (row, head).
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o,
@@ -1531,11 +2169,15 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
                             int64_t ld_ctx, float* lse, cudaStream_t st, void* ws, size_t ws_bytes) {
   alignas(64) CUtensorMap tm;
   if (!tmap_bf16_2d(&tm, qkv, T, 3 * heads * HD, ld_qkv, 128, 64)) return cudaErrorInvalidValue;
-  // ATP_ATTN_FWD = 1 / 2 / 3: forward kernel version (default 2; v3, two
-  // softmax threads per row, measured 4-5% slower: profiles/r02_attn_fwd_v3.log)
+  // ATP_ATTN_FWD = 1 / 2 / 3 / 4: forward kernel version (default 4, v2 made
+  // persistent with cluster launch control: b4 s2048 32 heads causal 0.167 ->
+  // 0.152 ms, 40 heads 0.215 -> 0.193, non-causal 0.257 -> 0.250, s8192 0.120
+  // -> 0.123: profiles/r02_attn_persistent.log; v3, two softmax threads per
+  // row, measured 4-5% slower than v2: profiles/r02_attn_fwd_v3.log).  Grids
+  // smaller than the GPU take v2 with split-KV.
   static const int fwd_ver = [] {
     const char* e = getenv("ATP_ATTN_FWD");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 4;
   }();
   const bool v1 = fwd_ver == 1;
   static bool attr = [] {
@@ -1544,6 +2186,8 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
            cudaFuncSetAttribute(attn_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem) ==
                cudaSuccess &&
            cudaFuncSetAttribute(attn_fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwd3Smem) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(attn_fwd4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwd4Smem) ==
                cudaSuccess;
   }();
   (void)attr;
@@ -1582,7 +2226,7 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
   p.lse = lse;
   if (v1) {
     attn_fwd_kernel<<<(seq / BQ) * heads * (T / seq), 256, kFwdSmem, st>>>(tm, p);
-  } else if (fwd_ver == 2) {
+  } else if (fwd_ver == 2 || fwd_ver == 4) {
     // split-KV when the grid is smaller than the GPU and the caller gave the workspace
     static const bool split_on = [] {
       const char* e = getenv("ATP_ATTN_SPLIT");
@@ -1596,6 +2240,8 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
       attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq) * S, 320, kFwdSmem, st>>>(tm, p);
       const int64_t warps = static_cast<int64_t>(T) * heads;
       attn_fwd_combine_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(p);
+    } else if (fwd_ver == 4) {
+      attn_fwd4_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwd4Smem, st>>>(tm, p);
     } else {
       attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwdSmem, st>>>(tm, p);
     }
@@ -1663,11 +2309,14 @@ cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, in
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dqkv = ld_dqkv;
   const int grid = (seq / BKV) * heads * (T / seq);
-  static const bool v1 = [] {
+  // ATP_ATTN_BWD = 1 / 2 / 3: backward kernel version (default 3, v2 made
+  // persistent with cluster launch control: b4 s2048 32 heads causal 0.498 ->
+  // 0.470 ms, non-causal 0.776 -> 0.757: profiles/r02_attn_persistent.log)
+  static const int bwd_ver = [] {
     const char* e = getenv("ATP_ATTN_BWD");
-    return e && e[0] == '1';
+    return e ? atoi(e) : 3;
   }();
-  if (v1) {
+  if (bwd_ver == 1) {
     attn_bwd_kernel<<<grid, 320, kBwdSmem, st>>>(tq, td, tdq, p);
   } else {
     alignas(64) CUtensorMap tq64, td64, tdq64;
@@ -1677,7 +2326,14 @@ cudaError_t attn_bwd_launch(const void* qkv, int64_t ld_qkv, const void* ctx, in
     static bool attr2 = cudaFuncSetAttribute(attn_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Bwd2Smem::Bytes) == cudaSuccess;
     (void)attr2;
-    attn_bwd2_kernel<<<grid, 448, Bwd2Smem::Bytes, st>>>(tq, tq64, td64, tdq64, p);
+    if (bwd_ver == 3) {
+      static bool attr3 = cudaFuncSetAttribute(attn_bwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               Bwd2Smem::Bytes) == cudaSuccess;
+      (void)attr3;
+      attn_bwd3_kernel<<<grid, 448, Bwd2Smem::Bytes, st>>>(tq, tq64, td64, tdq64, p);
+    } else {
+      attn_bwd2_kernel<<<grid, 448, Bwd2Smem::Bytes, st>>>(tq, tq64, td64, tdq64, p);
+    }
   }
   attn_bwd_dq_kernel<<<sms * 8, 256, 0, st>>>(dq_acc, T, heads, p.scale, static_cast<__nv_bfloat16*>(dqkv), ld_dqkv);
   return cudaGetLastError();
