@@ -1,0 +1,6 @@
+# forward v5 (64-key blocks, double-buffered S): parity, A/B vs v4
+mkdir -p gpurun_out
+ATP_ATTN_FWD=5 timeout 300 python -m pytest tests/test_gpu_attention.py -q -p no:cacheprovider -k fwd -x 2>&1 | tail -3
+for v in 5 4 5 4; do
+  ATP_ATTN_FWD=$v timeout 300 python scripts/attn_bench.py > gpurun_out/attn5_v$v.log 2>&1; echo "fwd v$v"; cut -c1-120 gpurun_out/attn5_v$v.log
+done
