@@ -338,9 +338,27 @@ cudaError_t fused_ar_launch(const FusedArArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  fused_ar_kernel<0><<<a.n_ctas, kFusedThreads, smem, st>>>(a);
-  fused_ar_kernel<1><<<a.n_ctas, kFusedThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  // Launched as 2-CTA clusters: the CTA-pair GEMMs need both SMs of a pair
+  // free, and fused CTAs scattered one per SM pair could leave no pair for the
+  // GEMM clusters whose tiles those very CTAs wait for (with every rank of a
+  // virtual mesh on one GPU this deadlocked: DESIGN.md §10).  As clusters the
+  // fused CTAs take whole pairs.  The kernel uses no cluster feature.
+  cudaLaunchConfig_t cfg = {};
+  if (a.n_ctas % 2) return cudaErrorInvalidValue;  // the ready / done targets count n_ctas CTAs
+  cfg.gridDim = dim3(a.n_ctas);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute cl[1];
+  cl[0].id = cudaLaunchAttributeClusterDimension;
+  cl[0].val.clusterDim.x = 2;
+  cl[0].val.clusterDim.y = 1;
+  cl[0].val.clusterDim.z = 1;
+  cfg.attrs = cl;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fused_ar_kernel<0>, a);
+  if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, fused_ar_kernel<1>, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace atp

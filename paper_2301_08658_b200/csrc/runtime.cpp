@@ -113,7 +113,7 @@ int fused_ctas() {
   static const int v = [] {
     const char* e = getenv("ATP_FUSED_CTAS");
     const int n = e ? atoi(e) : 0;
-    return n > 0 ? n : kFusedCtas;
+    return n > 0 ? (n + 1) / 2 * 2 : kFusedCtas;  // even: the kernels launch as 2-CTA clusters
   }();
   return v;
 }

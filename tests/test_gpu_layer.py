@@ -271,6 +271,7 @@ def test_probe_single_rank_and_local_mesh():
         loc.destroy()
 
 
+@pytest.mark.isolated(timeout=240, retries=1)
 @pytest.mark.parametrize("d1,d2", [(2, 1), (1, 2), (2, 2), (4, 2), (2, 4), (8, 1), (1, 8)])
 @pytest.mark.parametrize("chunks", [1, 4])
 def test_layer_fused_peer_allreduce(d1, d2, chunks):
@@ -321,6 +322,7 @@ def _fused_launches(mesh, call):
     return kinds.count(4), kinds.count(2)
 
 
+@pytest.mark.isolated(timeout=240, retries=1)
 @pytest.mark.parametrize("d1,d2", [(4, 2), (2, 4), (8, 1), (1, 8)])
 def test_layer_fused_push_every_stage(d1, d2):
     """Fused GEMM -> reduce-scatter (TMA stores into the slice owners' receive
@@ -358,6 +360,7 @@ def test_layer_fused_push_every_stage(d1, d2):
             assert torch.equal(b[k], v), k
 
 
+@pytest.mark.isolated(timeout=240, retries=1)
 @pytest.mark.parametrize("d1,d2,cap", [(2, 2, 32), (4, 2, 16), (2, 4, 16), (8, 1, 16)])
 @pytest.mark.parametrize("fused", [False, True])
 def test_layer_chunk_gated(d1, d2, cap, fused):
@@ -386,6 +389,7 @@ def test_layer_chunk_gated(d1, d2, cap, fused):
     check_replicas(bufs, d1, d2)
 
 
+@pytest.mark.isolated(timeout=240, retries=1)
 @pytest.mark.gpu
 @pytest.mark.parametrize("fused", [False, True])
 def test_layer_gated_chunk_count_changes(fused):
@@ -499,6 +503,7 @@ def test_layer_stack(d1, d2, chunks):
         check_replicas(stack[l], d1, d2)
 
 
+@pytest.mark.isolated(timeout=240, retries=1)
 @pytest.mark.parametrize("d1,d2,fused,gated", [(2, 2, True, False), (4, 2, True, True), (2, 2, False, True)])
 def test_layer_stack_fused_and_gated(d1, d2, fused, gated):
     """The layer stack with the fused GEMM -> RS -> AG stages (receive regions
