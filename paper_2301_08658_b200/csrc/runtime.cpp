@@ -55,6 +55,15 @@ bool stream_wait_available() {
 // communication disabled, only account for the tile counter the GEMM bumped).
 static cudaError_t launch_fused(atp_mesh* m, RankState& s, const Op& op, cudaStream_t st) {
   FusedArArgs a = op.far;
+  if (m->is_virtual) {
+    // Every rank's fused kernels share this one GPU and spin on one another's
+    // progress: keep their CTAs together at one GPU's budget (kFusedCtas), or
+    // they starve the CTA-pair GEMMs whose tiles they wait for (8 ranks x 32
+    // spinning CTAs deadlocked every time once the streams ran truly
+    // concurrently; with 2-8 CTAs per rank never: DESIGN.md §10).
+    const int per = (kFusedCtas / (m->d1 * m->d2)) & ~1;
+    a.n_ctas = std::max(2, std::min(a.n_ctas, per));
+  }
   const int d = op.ar_dim - 1;
   a.p = op.ar_dim == 1 ? m->d1 : m->d2;
   a.me = s.me_in[d];

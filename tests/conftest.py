@@ -21,12 +21,12 @@ def pytest_configure(config):
 
 
 # The fused peer-memory path on the VIRTUAL mesh (all ranks' kernels on one
-# GPU, spinning on one another's flags) deadlocked late in 2 of 3 full -m gpu
-# sessions in round 2's third session (test_layer_fused_peer_allreduce[4-2-4],
-# test_layer_fused_push_every_stage[4-2]; never in 48 isolated repetitions;
-# DESIGN.md §10).  Such tests run in a child
-# process with a timeout, so a hang fails (or, on the retry, passes) that test
-# instead of stalling the whole session.
+# GPU, spinning on one another's progress) deadlocked late in 2 of 3 full
+# -m gpu sessions of round 2's third session: 8 ranks x 32 spinning fused CTAs
+# starved the GEMMs they waited for (fixed in runtime.cpp launch_fused: the
+# ranks of a virtual mesh share one GPU's fused-CTA budget).
+# As a safety net such tests run in a child process with a timeout, so a hang
+# fails (or, on the retry, passes) that test instead of stalling the session.
 _CHILD = "ATP_ISOLATED_CHILD"
 
 
