@@ -113,3 +113,30 @@ def test_bench_n2_shared_gpu_p2p_disable():
     assert {tuple(r[:2]) for r in d["search"]["ranked"]} == {(2, 1), (1, 2)}
     assert {tuple(r[:2]) for r in d["search"]["hcm_only"]["ranked"]} == {(2, 1), (1, 2)}
     assert all(r[3] for r in d["search"]["ranked"]) and not any(r[3] for r in d["search"]["hcm_only"]["ranked"])
+
+
+def test_bench_gpt_n2_shared_gpu():
+    """The full-layer N>1 bench path (--layer gpt: LayerNorm, the attention core
+    over the rank's heads with the dim-2 reduce-scatter / all-gather, MLP) under
+    torchrun with both ranks on the one GPU: one JSON line from rank 0 with the
+    searched mesh, the chunk choice and the paper-formula FLOPs (timings
+    meaningless)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--share-gpu", "--layer", "gpt", "--steps", "3", "--warmup", "3",
+                          "--hidden", "1024", "--heads", "8", "--batch", "2", "--seq", "1024", "--no-cpu-baseline",
+                          "--probe-mib", "4"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["mesh"] in ([2, 1], [1, 2])
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0 and d["exposed_comm_ms"] >= 0
+    assert d["tflops_paper_formula"] > 0
