@@ -2240,7 +2240,10 @@ cudaError_t attn_fwd_launch(const void* qkv, int64_t ld_qkv, int T, int seq, int
       attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq) * S, 320, kFwdSmem, st>>>(tm, p);
       const int64_t warps = static_cast<int64_t>(T) * heads;
       attn_fwd_combine_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(p);
-    } else if (fwd_ver == 4) {
+    } else if (fwd_ver == 4 && p.grouped > 0) {
+      // persistent for the chunked (grouped) CTA order, seq <= 4096; longer
+      // sequences (global heaviest-first order, items of 30+ steps) keep v2:
+      // b1 s8192 0.120 (v2) vs 0.123 ms (v4), profiles/r02_attn_persistent.log
       attn_fwd4_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwd4Smem, st>>>(tm, p);
     } else {
       attn_fwd2_kernel<<<((seq / BQ + 1) / 2) * heads * (T / seq), 320, kFwdSmem, st>>>(tm, p);
