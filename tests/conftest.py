@@ -37,7 +37,9 @@ def pytest_pyfunc_call(pyfuncitem):
         return None
     timeout = mark.kwargs.get("timeout", 180)
     retries = mark.kwargs.get("retries", 1)
-    cmd = [sys.executable, "-m", "pytest", pyfuncitem.nodeid, "-q", "-p", "no:cacheprovider", "-m", "gpu"]
+    cmd = [sys.executable, "-m", "pytest", pyfuncitem.nodeid, "-q", "-p", "no:cacheprovider"]
+    if pyfuncitem.get_closest_marker("gpu") is not None:
+        cmd += ["-m", "gpu"]
     env = dict(os.environ, **{_CHILD: "1"})
     tail = ""
     for attempt in range(retries + 1):
